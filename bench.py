@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Benchmark: volumes/s for 145x174x145 detect + describe (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ours|reference]
+
+One step = one batch of B synthetic 145x174x145 volumes per GPU through the
+whole hot path (Gaussian pyramid + DoG + 80-neighbour detection + orientation
++ SIFT-Rank descriptors), replayed as one CUDA graph.  Inputs are resident in
+HBM before the timed region; consecutive steps read different input slots
+(S*B*14.6 MB > L2), so no step starts with its input in L2.  Multi-GPU: one
+process per GPU (torchrun), each rank its own volumes, no collective in the
+data path (weak scaling); timing is CUDA events on the pipeline stream, max
+over ranks.  Rank 0 prints one JSON line.
+
+``--impl reference`` times the reference algorithm on the host cores instead:
+the oracle restatement (oracle/volkey_oracle.py -- the Python reference cannot
+travel to the GPU box), one full volume per process, all cores concurrently.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+DIMS = (145, 174, 145)
+with open(os.path.join(REPO, "BASELINE.json")) as _fh:
+    METRIC = json.load(_fh)["metric"]
+UNIT = "volumes/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=16, help="volumes per GPU per step")
+    ap.add_argument("--slots", type=int, default=2, help="distinct input batches cycled over steps")
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--descriptor", default="siftrank", choices=("siftrank", "brief", "rrief"))
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-steps", type=int, default=2, help="cap on timed reference steps (each ~30 s)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc, self.thread = gpu, [], None, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------ algorithmic bytes
+def pyramid_bytes(plan) -> int:
+    """Compulsory HBM bytes of the fused pyramid per volume: every Gaussian
+    level read once + written once, every DoG level written once, the handoff
+    subsample written once (SURVEY.md §8(d) minus the detection read)."""
+    L = plan.cfg.levels_per_octave
+    total = 0
+    for o, d in enumerate(plan.octave_dims):
+        n = int(np.prod(d))
+        if o == 0:
+            total += 8 * n                      # input -> level 0
+        total += (L - 1) * 12 * n               # read prev, write level, write DoG
+        if o + 1 < plan.n_octaves:
+            total += 4 * int(np.prod(plan.octave_dims[o + 1]))
+    return total
+
+
+def detect_bytes(plan) -> int:
+    """Detection reads each of the L-1 DoG levels once per octave."""
+    L = plan.cfg.levels_per_octave
+    return sum((L - 1) * 4 * int(np.prod(d)) for d in plan.octave_dims)
+
+
+# ------------------------------------------------------------ CPU oracle
+def _oracle_worker(args):
+    seed, kind, barrier = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    import threadpoolctl
+
+    from oracle import volkey_oracle as O
+    from paper_2112_10258_b200 import synthetic
+
+    with threadpoolctl.threadpool_limits(1):
+        base = synthetic.brain_volume()
+        vol = synthetic.batch_from(base, 1, seed=seed)[0] if seed else base
+        O.extract(np.ones((24, 24, 24), np.float32) * np.arange(24, dtype=np.float32), descriptor=kind)  # warm
+        if barrier is not None:
+            barrier.wait()
+        t0 = time.time()
+        res = O.extract(vol, descriptor=kind)
+        t1 = time.time()
+    return t0, t1, len(res["keypoints"]), len(res["records"])
+
+
+def cpu_oracle_volumes_per_s(kind: str, procs: int, steps: int):
+    """Reference algorithm on the host cores: `procs` concurrent processes,
+    one full volume each per step.  Returns (volumes/s, details)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    times, kps = [], []
+    for s in range(steps):
+        if procs == 1:
+            r = [_oracle_worker((s, kind, None))]
+        else:
+            with ctx.Manager() as mgr:
+                bar = mgr.Barrier(procs)
+                with ctx.Pool(procs) as pool:
+                    r = pool.map(_oracle_worker, [(s * procs + i, kind, bar) for i in range(procs)])
+        start, end = min(x[0] for x in r), max(x[1] for x in r)
+        times.append(end - start)
+        kps += [x[2] for x in r]
+    return procs * steps / sum(times), dict(step_s=times, keypoints=kps)
+
+
+# ---------------------------------------------------------------- ours
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2112_10258_b200 as vk
+    from paper_2112_10258_b200 import _lib, synthetic
+    from paper_2112_10258_b200.engine import Extractor
+
+    cfg = vk.PipelineConfig(descriptor=a.descriptor)
+    B, S = a.batch, max(1, a.slots)
+    # ---- inputs: distinct volumes per rank and slot, resident in HBM (x fastest)
+    base = synthetic.brain_volume()
+    host = synthetic.batch_from(base, B * S, seed=1000 + rank)            # (B*S, nx, ny, nz)
+    dev_in = torch.empty((B * S,) + DIMS[::-1], dtype=torch.float32, device="cuda")
+    tmp = torch.from_numpy(host).cuda()
+    _lib.call("vk_transpose_zfast_to_xfast", tmp.data_ptr(), dev_in.data_ptr(), B * S, *DIMS, _lib.stream_ptr())
+    del tmp
+    pinned = torch.from_numpy(np.ascontiguousarray(host.transpose(0, 3, 2, 1))).pin_memory()  # x-fastest host copy
+    del host
+    # ---- one extractor per slot (its input buffer is the resident slot)
+    exs = []
+    for s in range(S):
+        exs.append(Extractor(DIMS, cfg, batch=B, input=dev_in[s * B:(s + 1) * B]))
+    # capacity check on a first eager run, grow buffers if needed
+    for i, ex in enumerate(exs):
+        ex.enqueue()
+        c = ex.check_capacity()
+        if c["overflow"]:
+            ex2 = Extractor(DIMS, cfg, batch=B, kp_cap=2 * c["keypoints"] + 1024, frame_cap=2 * c["frames"] + 1024,
+                            input=ex.input)
+            exs[i] = ex2
+            ex2.enqueue()
+    torch.cuda.synchronize()
+    counts = exs[0].counts()
+    launches0 = _lib.load().vk_launch_count()
+    exs[0].enqueue()
+    torch.cuda.synchronize()
+    launches_per_step = _lib.load().vk_launch_count() - launches0
+    # ---- per-stage device times (eager, events on the pipeline stream)
+    st = torch.cuda.current_stream()
+    stage_ms = {k: [] for k in ("pyramid", "detect", "orient", "describe")}
+    for _ in range(3):
+        ex = exs[0]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        s = st.cuda_stream
+        ev[0].record(st)
+        ex.enqueue_pyramid(s)
+        ev[1].record(st)
+        ex.enqueue_detect(s)
+        ev[2].record(st)
+        ex.enqueue_orient(s)
+        ev[3].record(st)
+        ex.enqueue_describe(s)
+        ev[4].record(st)
+        torch.cuda.synchronize()
+        for k, (e0, e1) in zip(stage_ms, zip(ev[:-1], ev[1:])):
+            stage_ms[k].append(e0.elapsed_time(e1))
+    stage_ms = {k: statistics.median(v) for k, v in stage_ms.items()}
+    # ---- graphs
+    use_graph = not a.no_graph
+    if use_graph:
+        for ex in exs:
+            ex.capture()
+    # ---- warmup + timed region
+    for w in range(a.warmup):
+        exs[w % S].run()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for k in range(a.steps):
+        exs[k % S].run()
+    e1.record(st)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * B * a.steps / (ms / 1e3)
+
+    # ---- end to end through the public API: pinned host -> HBM -> results -> host
+    e2e = None
+    if not a.no_e2e:
+        ex = exs[0]
+        res_host = {}
+        h2d = B * int(np.prod(DIMS)) * 4
+        d2h_tot = 0
+
+        def one_step(slot):
+            nonlocal d2h_tot
+            ex.input.copy_(pinned[slot * B:(slot + 1) * B], non_blocking=True)
+            ex.run()
+            r = ex.results()   # reads counts, then copies exactly the produced SoA
+            d2h_tot += 16 + sum(v.nbytes for v in r.values() if isinstance(v, np.ndarray))
+            res_host["last"] = r
+
+        for w in range(max(1, a.warmup)):
+            one_step(w % S)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        d2h_tot = 0
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(st)
+        for k in range(a.steps):
+            one_step(k % S)
+        f1.record(st)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        # restore the resident slot-0 input for any later use
+        ex.input.copy_(dev_in[:B])
+        e2e = {"value": world * B * a.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": int(d2h_tot / a.steps), "ms_per_step": ems / a.steps,
+               "path": "Extractor.run(pinned x-fastest host batch) + Extractor.results() (SoA to host)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    plan = exs[0].plan
+    with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+        peaks = json.load(fh)
+    pbytes = pyramid_bytes(plan) * B
+    achieved = pbytes / (stage_ms["pyramid"] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "blur3d_ring_kernel (fused blur + DoG + subsample), all pyramid launches",
+                "achieved": round(achieved, 1), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm_gbs"], 4) if peaks.get("hbm_gbs") else None,
+                "traffic": None, "algorithmic_bytes_per_step": pbytes,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"}
+    det_gbs = detect_bytes(plan) * B / (stage_ms["detect"] / 1e3) / 1e9
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (pyramid, detection) + f64 (orientation, descriptors)",
+        "data": "synthetic (reference kernel-soup phantom, seed 20240817, flipped/shifted + fresh noise per volume)",
+        "config": {"workload": f"configs[2]-style batch: {B} x 145x174x145 volumes per GPU per step, detect + "
+                               f"describe ({a.descriptor}), defaults of PipelineConfig",
+                   "volume": list(DIMS), "batch_per_gpu": B, "descriptor": a.descriptor,
+                   "l2_policy": f"inputs larger than L2: {S} resident input slots x {B} volumes x 14.6 MB cycled",
+                   "cuda_graph": use_graph, "parallelism": f"dp{world} (independent volumes, no collective)"},
+        "roofline": roofline,
+        "stages_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
+        "detect_gbs": round(det_gbs, 1),
+        "keypoints_per_volume": counts["keypoints"] / B, "frames_per_volume": counts["frames"] / B,
+        "gpu_launches": int(launches_per_step * a.steps),
+        "clocks": clk,
+    }
+    if e2e:
+        out["e2e"] = e2e
+    if world == 1 and not a.no_cpu_baseline:
+        vps, det = cpu_oracle_volumes_per_s(a.descriptor, 1, 1)
+        out["cpu_baseline"] = {"value": round(vps, 5), "unit": UNIT, "cores": 1, "kind": "port",
+                               "sample": "1 full 145x174x145 volume through oracle/volkey_oracle.py (numpy "
+                                         "restatement of the reference), 1 thread", "seconds": det["step_s"]}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    procs = os.cpu_count() or 1
+    steps = max(1, min(a.steps, a.ref_steps))
+    vps, det = cpu_oracle_volumes_per_s(a.descriptor, procs, steps)
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(vps, 5), "unit": UNIT, "n_gpus": world,
+        "steps": steps, "steps_requested": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * statistics.mean(det["step_s"]),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 + f64 (numpy)",
+        "data": "synthetic (same phantom family as the GPU arm)",
+        "config": {"workload": f"1 x 145x174x145 volume per process per step, {procs} processes, detect + describe "
+                               f"({a.descriptor})", "volume": list(DIMS), "descriptor": a.descriptor},
+        "cpu_baseline": {"value": round(vps, 5), "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": f"{procs} concurrent single-threaded processes x {steps} step(s), one full volume "
+                                   "each, oracle/volkey_oracle.py (the Python reference cannot travel to the box)"},
+        "e2e": {"value": round(vps, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_seconds": det["step_s"],
+    }
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

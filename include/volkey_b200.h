@@ -1,0 +1,206 @@
+/*
+ * volkey_b200.h -- C ABI of the B200-native volkey hot path.
+ *
+ * The reference (/root/reference/pkg/src/volkey) is pure Python and has no
+ * FFI; the drop-in boundary is therefore this C ABI, bound from Python with
+ * ctypes (INTEGRATION.md shows the binding).  Every entry point names the
+ * reference function it replaces (file:line, paths relative to
+ * /root/reference/pkg/src/volkey).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  All array pointers are DEVICE pointers
+ *    unless the parameter name ends in _host.  Work is enqueued on `stream`
+ *    (a cudaStream_t passed as void*, NULL = legacy default stream) and is
+ *    stream-ordered; nothing synchronises unless the function says so.
+ *  - Volumes are float32, x-fastest ("on-disk" order, volume.py:4-5):
+ *    element (x, y, z) of volume b lives at ((b*nz + z)*ny + y)*nx + x.
+ *    The reference's in-memory numpy layout data[x, y, z] (z fastest) is
+ *    converted with vk_transpose_* at the boundary.
+ *  - Return value: VK_OK or an error code mirroring errors.py exit codes
+ *    (5 parameter, 7 data); CUDA failures are VK_ERR_CUDA.  The message of
+ *    the last failure on the calling thread is vk_last_error().  No C++
+ *    exception crosses the ABI.
+ *  - Caller owns every buffer.  Scratch space, when needed, is passed in.
+ */
+#ifndef VOLKEY_B200_H
+#define VOLKEY_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VK_ABI_VERSION 1
+
+#define VK_OK 0
+#define VK_ERR_PARAMETER 5 /* errors.py:32-36 ParameterError */
+#define VK_ERR_DATA 7      /* errors.py:46-50 DataError */
+#define VK_ERR_CUDA 20
+#define VK_ERR_CAPACITY 21 /* a caller-sized output buffer was too small */
+
+#define VK_MAX_TAPS 65        /* blur radius <= 32 */
+#define VK_MAX_DIRS 64        /* orientation direction-set size */
+#define VK_MAX_FRAMES 8       /* frames per keypoint */
+#define VK_MAX_PAIRS 256      /* BRIEF/RRIEF point pairs */
+
+/* One pyramid level of a batch: volume b starts at base + b*vol_stride. */
+typedef struct vk_level {
+    const float* base;
+    long long vol_stride;
+    int nx, ny, nz;
+    int pad_;
+} vk_level;
+
+/* One keypoint (device record). */
+typedef struct vk_kp {
+    int vol;      /* volume index within the batch */
+    int lvl;      /* index into the level table (orientation / SIFT-Rank level) */
+    int ix, iy, iz; /* lattice centre in that level's grid (orient.py:258-268) */
+    int ball;     /* index into the ball table */
+    int octave;
+    int level;
+} vk_kp;
+
+/* Integer ball of offsets (orient.py:244-255): `count` packed offsets
+ * starting at `start` in the offset table; windows[window_start + d2] is the
+ * orientation window for squared offset length d2 (orient.py:298-299). */
+typedef struct vk_ball {
+    int start;
+    int count;
+    int window_start;
+    int max_d2;
+} vk_ball;
+
+/* One oriented frame: keypoint index plus the (primary, secondary) direction
+ * pair that spawned it (-1 when the rotation was supplied directly). */
+typedef struct vk_frame {
+    int kp;
+    int prim;
+    int sec;
+    int pad_;
+} vk_frame;
+
+const char* vk_last_error(void);
+int vk_abi_version(void);
+int vk_device_sm_count(int device);
+/* Stream-ordered zero fill (graph-capturable); used for per-step counters. */
+int vk_memset_async(void* ptr, long long bytes, void* stream);
+/* Kernels launched by this library since load (instrumentation for bench.py). */
+long long vk_launch_count(void);
+
+/* ---------------------------------------------------------------- layout */
+/* volume.py:64-70 conversions: data[x,y,z] (z fastest) <-> x-fastest. */
+int vk_transpose_zfast_to_xfast(const float* src, float* dst, int nb, int nx, int ny, int nz, void* stream);
+int vk_transpose_xfast_to_zfast(const float* src, float* dst, int nb, int nx, int ny, int nz, void* stream);
+
+/* ----------------------------------------------------------- scale space */
+/* convolve_array / convolve_separable (scalespace.py:73-120): replicate-
+ * padded separable blur, x then y then z pass, fp32 products added in tap
+ * order (no FMA).  taps_host: 2*radius+1 float32 weights (gaussian_kernel,
+ * scalespace.py:63-70).  Optional fused epilogues:
+ *   dog_out  != NULL: dog_out = src - dst        (build_dog_pyramid, scalespace.py:237-251)
+ *   half_out != NULL: half_out = subsample_half(dst) (scalespace.py:123-137)  */
+int vk_blur3d(const float* src, float* dst, float* dog_out, float* half_out,
+              int nb, int nx, int ny, int nz, const float* taps_host, int radius, void* stream);
+
+/* subsample_half (scalespace.py:123-137): floor dims, ordered 8-sum, /8. */
+int vk_subsample_half(const float* src, float* dst, int nb, int nx, int ny, int nz, void* stream);
+
+/* DoG difference a - b over n elements (scalespace.py:247-248). */
+int vk_difference(const float* a, const float* b, float* out, long long n, void* stream);
+
+/* ------------------------------------------------------------- detection */
+/* sum_of_signs_map (detect.py:48-79): int16 80-neighbour map, border 0. */
+int vk_sum_of_signs(const float* prev, const float* cur, const float* next, int16_t* out,
+                    int nb, int nx, int ny, int nz, void* stream);
+
+/* extract_extrema over every interior DoG level of one octave
+ * (detect.py:82-140, 149-178).  dogs: ndog device pointers (host array) to
+ * batched DoG levels of one octave.  Appends candidate keys
+ *   key = seg << 52 | z << 35 | y << 18 | x << 1 | valley,  seg = seg_base + level
+ * to cand_keys[b*cap ...] and bumps cand_count[b].  contrast_min is compared
+ * in float32 (numpy NEP 50 semantics of detect.py:104). */
+int vk_detect_octave(const float* const* dogs_host, int ndog, int nb, int nx, int ny, int nz,
+                     int seg_base, int band, float contrast_min,
+                     unsigned long long* cand_keys, int* cand_count, int cap, void* stream);
+
+/* Candidates from a precomputed int16 sum-of-signs map of one DoG level
+ * (extract_extrema with a caller-supplied map, detect.py:82-140). */
+int vk_extrema_from_map(const int16_t* map, const float* dog_cur, int nx, int ny, int nz, int seg, int band,
+                        float contrast_min, unsigned long long* cand_keys, int* cand_count, int cap, void* stream);
+
+/* Order candidates (detect.py:179-181: octave, level, z, y, x) and emit the
+ * keypoint records of the whole batch, volume-major (total[0] = count,
+ * total[1] = 1 if a volume overflowed `cap`).  seg_info_host: per
+ * segment {octave, level, level_table_index, ball_index}; dog_levels: device
+ * vk_level table indexed like seg (for dog_value).  Writes kps[0..total),
+ * pos[3*i], sigma[i], dog[i], sign[i] (+1 peak, -1 valley), vol_offset[b]
+ * and total[0].  seg_sigma_host: keypoint sigma per segment (detect.py:110,143-146). */
+int vk_order_keypoints(const unsigned long long* cand_keys, const int* cand_count, int nb, int cap,
+                       const int* seg_info_host, const double* seg_sigma_host, int nseg,
+                       const vk_level* dog_levels, vk_kp* kps, double* pos, double* sigma, float* dog,
+                       int8_t* sign, int* vol_offset, int* total, int kp_cap, void* stream);
+
+/* ----------------------------------------------------------- orientation */
+/* gradient_histogram + dominant_orientations (orient.py:271-350) for n_kp
+ * keypoints (n_kp_dev: device count, read by the kernel; n_kp_max bounds it).
+ * dirs: K x 3 fp64 directions; pair_ok: K x K uint8 (norm of projection > 1e-6,
+ * orient.py:339-343).  Outputs: weights (n x K fp64, nullable), nframes[n],
+ * prim/sec[n*max_frames].  status[0] |= 1 when a keypoint's neighbourhood lies
+ * outside its volume (DataError, orient.py:291-292). */
+int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_level* levels,
+              const vk_ball* balls, const int* ball_offsets, const double* windows,
+              const double* dirs, int K, const uint8_t* pair_ok,
+              double secondary_ratio, int max_frames,
+              double* weights, int* nframes, int* prim, int* sec, int* status,
+              int exact_only, void* stream);
+
+/* dominant_orientations (orient.py:310-350) on n caller-supplied K-bin
+ * weight vectors (exact comparisons). */
+int vk_frames_from_weights(const double* weights, int n, int K, const uint8_t* pair_ok, double secondary_ratio,
+                           int max_frames, int* nframes, int* prim, int* sec, void* stream);
+
+/* Expand per-keypoint frames into the ordered frame list (pipeline.py:55-67:
+ * keypoints with zero frames are dropped).  rot_table: K*K*9 fp64 rotations
+ * (column-stacked axes, orient.py:346-347).  Writes frames[], rot[9*j],
+ * n_frames_dev[0], dropped_dev[0]. */
+int vk_expand_frames(const int* nframes, const int* prim, const int* sec, const int* n_kp_dev,
+                     int n_kp_max, int max_frames, const double* rot_table, int K,
+                     vk_frame* frames, double* rot, int* n_frames_dev, int* dropped_dev,
+                     int frame_cap, void* stream);
+
+/* ------------------------------------------------------------ descriptors */
+/* sift_rank_descriptor (descriptor.py:227-263): 64 stable ranks per frame
+ * (uint8).  rot: 9 fp64 per frame (row-major 3x3). */
+int vk_describe_siftrank(const vk_frame* frames, const double* rot, const int* n_frames_dev,
+                         int n_frames_max, const vk_kp* kps, const vk_level* levels,
+                         const vk_ball* balls, const int* ball_offsets, uint8_t* ranks_out,
+                         int exact_only, void* stream);
+
+/* extract_patch + preblur_patch + brief/rrief (descriptor.py:96-111,
+ * 196-224).  kind 1 = BRIEF (packed big-endian bits, ceil(n/8) bytes per
+ * frame, descriptor.py:309-316), kind 2 = RRIEF (n stable ranks, uint16).
+ * sources: level table of the unblurred source volumes (one entry, batch
+ * strided); pos/sigma: keypoint position (base coords) and sigma.
+ * grid_host: side linspace values; taps_host: pre-blur taps (radius 0 = off);
+ * pts: device, 2*n*3 fp64 pair sample points already mapped to patch
+ * index space (descriptor.py:205-212). */
+int vk_describe_patch(int kind, const vk_frame* frames, const double* rot, const int* n_frames_dev,
+                      int n_frames_max, const vk_kp* kps, const double* pos, const double* sigma,
+                      const vk_level* source, int side, const double* grid_host,
+                      const float* taps_host, int radius, const double* pts, int npairs,
+                      uint8_t* bits_out, uint16_t* ranks_out, void* stream);
+
+/* --------------------------------------------------------------- matching */
+/* nearest_neighbor_matches (match.py:81-121).  metric 0 = hamming on packed
+ * bytes (nbytes per row), 1 = euclidean on int16 rows (dim per row),
+ * 2 = euclidean on fp64 rows.  Outputs per query: best index, d1, d2 (fp64),
+ * keep (d1 <= ratio_max * d2). */
+int vk_match(int metric, const void* a, int na, const void* b, int nb_rows, int dim,
+             double ratio_max, int* best, double* d1, double* d2, uint8_t* keep, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOLKEY_B200_H */

@@ -1,0 +1,116 @@
+// vk_common.cuh -- shared helpers for the sm_100a volkey kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/volkey_b200.h"
+
+#define VK_HD __host__ __device__ __forceinline__
+#define VK_D __device__ __forceinline__
+
+namespace vk {
+
+// Thread-local last-error text (vk_api.cu) and the helpers that set it.
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+// Number of kernels this library has launched (vk_launch_count()).
+void count_launch(int n = 1);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+template <typename T>
+VK_HD T clampi(T v, T lo, T hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// ---- cp.async (LDGSTS) helpers -------------------------------------------
+VK_D void cp_async4(void* smem, const void* gmem) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+VK_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+VK_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---- exact-rounding arithmetic (no contraction) ---------------------------
+// The reference evaluates every product and sum as a separately rounded numpy
+// ufunc; these wrappers make that explicit (the build also uses -fmad=false).
+VK_D float fmul(float a, float b) { return __fmul_rn(a, b); }
+VK_D float fadd(float a, float b) { return __fadd_rn(a, b); }
+VK_D double dmul(double a, double b) { return __dmul_rn(a, b); }
+VK_D double dadd(double a, double b) { return __dadd_rn(a, b); }
+VK_D double dsub(double a, double b) { return __dsub_rn(a, b); }
+VK_D double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// OpenBLAS dgemm order for a K=3 inner product:
+// fma(x2, y2, fma(x1, y1, x0*y0)).
+VK_D double dot3_blas(double x0, double x1, double x2, double y0, double y1, double y2) {
+    return dfma(x2, y2, dfma(x1, y1, dmul(x0, y0)));
+}
+
+// np.linalg.norm(axis=1) on an (N, 3) float64 array: sqrt((x*x + y*y) + z*z).
+VK_D double norm3_numpy(double x, double y, double z) {
+    return __dsqrt_rn(dadd(dadd(dmul(x, x), dmul(y, y)), dmul(z, z)));
+}
+
+// Packed ball offset: 10 bits per axis, biased by 512 (|offset| <= 511).
+VK_HD int unpack_off(int p, int axis) { return ((p >> (20 - 10 * axis)) & 1023) - 512; }
+
+// Trilinear interpolation with clamping, fp64 arithmetic on fp32 samples --
+// sample_trilinear_array (volume.py:203-236) step for step.  `at(x, y, z)`
+// fetches one voxel.
+template <typename F>
+VK_D double trilinear(F at, int nx, int ny, int nz, double px, double py, double pz) {
+    const int n[3] = {nx, ny, nz};
+    double p[3] = {px, py, pz};
+    int i0[3], i1[3];
+    double f[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double hi = (double)n[a] - 1.0;
+        double q = fmin(fmax(p[a], 0.0), hi);  // np.clip(pts, 0.0, hi)
+        long long fl = (long long)floor(q);
+        long long cap = n[a] - 2 > 0 ? n[a] - 2 : 0;
+        if (fl > cap) fl = cap;
+        i0[a] = (int)fl;
+        f[a] = dsub(q, (double)fl);
+        i1[a] = i0[a] + 1 < n[a] - 1 ? i0[a] + 1 : n[a] - 1;
+    }
+    auto lerp = [](double a, double b, double t) { return dadd(dmul(a, dsub(1.0, t)), dmul(b, t)); };
+    double c000 = at(i0[0], i0[1], i0[2]), c100 = at(i1[0], i0[1], i0[2]);
+    double c010 = at(i0[0], i1[1], i0[2]), c110 = at(i1[0], i1[1], i0[2]);
+    double c001 = at(i0[0], i0[1], i1[2]), c101 = at(i1[0], i0[1], i1[2]);
+    double c011 = at(i0[0], i1[1], i1[2]), c111 = at(i1[0], i1[1], i1[2]);
+    double c00 = lerp(c000, c100, f[0]);
+    double c10 = lerp(c010, c110, f[0]);
+    double c01 = lerp(c001, c101, f[0]);
+    double c11 = lerp(c011, c111, f[0]);
+    double c0 = lerp(c00, c10, f[1]);
+    double c1 = lerp(c01, c11, f[1]);
+    return lerp(c0, c1, f[2]);
+}
+
+// Central / one-sided gradient in fp64 (volume.py:244-264) at lattice point
+// (x, y, z) of an x-fastest fp32 volume.
+VK_D void gradient_at(const float* __restrict__ d, int nx, int ny, int nz, int x, int y, int z,
+                      double& gx, double& gy, double& gz) {
+    const long long sy = nx, sz = (long long)nx * ny;
+    const long long c = (long long)z * sz + (long long)y * sy + x;
+    int xh = min(x + 1, nx - 1), xl = max(x - 1, 0);
+    int yh = min(y + 1, ny - 1), yl = max(y - 1, 0);
+    int zh = min(z + 1, nz - 1), zl = max(z - 1, 0);
+    double vxh = (double)__ldg(d + c + (xh - x)), vxl = (double)__ldg(d + c + (xl - x));
+    double vyh = (double)__ldg(d + c + (long long)(yh - y) * sy), vyl = (double)__ldg(d + c + (long long)(yl - y) * sy);
+    double vzh = (double)__ldg(d + c + (long long)(zh - z) * sz), vzl = (double)__ldg(d + c + (long long)(zl - z) * sz);
+    // (up - dn) / max(hi - lo, 1): the divisor is 1.0 or 2.0, both exact.
+    // x / 2.0 == x * 0.5 exactly, so multiply instead of dividing.
+    gx = dmul(dsub(vxh, vxl), (xh - xl) == 2 ? 0.5 : 1.0);
+    gy = dmul(dsub(vyh, vyl), (yh - yl) == 2 ? 0.5 : 1.0);
+    gz = dmul(dsub(vzh, vzl), (zh - zl) == 2 ? 0.5 : 1.0);
+}
+
+// Unit roundoff of fp64 and a rigorous bound factor for recursive summation:
+// |fl(sum) - sum| <= gamma_k * sum|x| with gamma_k = k u / (1 - k u).
+constexpr double kU64 = 1.1102230246251565e-16;
+VK_HD double gamma_k(double k) { return (k * kU64) / (1.0 - k * kU64); }
+
+}  // namespace vk

@@ -1,0 +1,304 @@
+// vk_detect.cu -- 80-neighbour scale-space extrema and ordered keypoint output.
+//
+// Reference: detect.py:48-79 (sum_of_signs_map), detect.py:82-140
+// (extract_extrema), detect.py:149-182 (detect_keypoints ordering).
+//
+// Detection never materialises the int16 map on the pipeline path: a voxel is
+// a peak iff its "peak deficit" dp = 80 - m is <= band (and m > 0), a valley
+// iff dv = 80 + m <= band (and m < 0).  Both deficits only grow, so a thread
+// stops at the first neighbour that pushes both past the band -- for band 0
+// that is after ~3 of the 80 comparisons on average.  Survivors are appended
+// as 64-bit keys (segment, z, y, x, valley) whose numeric order is exactly the
+// reference order (octave, level, z, y, x, peak-before-valley); a rank-by-count
+// kernel then scatters them into the final keypoint records.
+#include "vk_common.cuh"
+
+namespace vk {
+
+constexpr int kMaxDog = 32;
+constexpr int kMaxSeg = 128;
+
+struct DogPtrs {
+    const float* p[kMaxDog];
+};
+
+struct SegInfo {
+    int octave[kMaxSeg];
+    int level[kMaxSeg];
+    int lvl[kMaxSeg];
+    int ball[kMaxSeg];
+    double sigma[kMaxSeg];
+};
+
+VK_D unsigned long long make_key(int seg, int x, int y, int z, int valley) {
+    return ((unsigned long long)seg << 52) | ((unsigned long long)z << 35) | ((unsigned long long)y << 18) |
+           ((unsigned long long)x << 1) | (unsigned long long)valley;
+}
+
+__global__ void __launch_bounds__(128)
+detect_kernel(DogPtrs dogs, int nlev, int nx, int ny, int nz, int seg_base, int band, float cmin,
+              unsigned long long* __restrict__ keys, int* __restrict__ counts, int cap) {
+    const int x = 1 + blockIdx.x * 32 + threadIdx.x;
+    const int y = 1 + blockIdx.y * 4 + threadIdx.y;
+    const int iz = nz - 2;
+    const int z = 1 + blockIdx.z % iz;
+    const int rest = blockIdx.z / iz;
+    const int lev = 1 + rest % nlev;
+    const int b = rest / nlev;
+    const long long plane = (long long)nx * ny;
+    const long long vol = plane * nz;
+    const long long idx = (long long)b * vol + (long long)z * plane + (long long)y * nx + x;
+
+    bool peak = false, valley = false;
+    if (x < nx - 1 && y < ny - 1) {
+        const float c = __ldg(dogs.p[lev] + idx);
+        if (fabsf(c) >= cmin) {
+            int dp = 0, dv = 0;
+            bool dead = false;
+#pragma unroll 1
+            for (int dl = 0; dl < 3 && !dead; ++dl) {
+                // centre level first: most voxels die on an in-plane neighbour
+                const int L = dl == 0 ? lev : (dl == 1 ? lev - 1 : lev + 1);
+                const float* v = dogs.p[L] + idx;
+#pragma unroll
+                for (int o = 0; o < 27; ++o) {
+                    const int dz = o / 9 - 1, dy = (o / 3) % 3 - 1, dx = o % 3 - 1;
+                    if (dl == 0 && o == 13) continue;
+                    const float n = __ldg(v + (long long)dz * plane + (long long)dy * nx + dx);
+                    dp += (c > n) ? 0 : (c == n ? 1 : 2);
+                    dv += (c < n) ? 0 : (c == n ? 1 : 2);
+                    if (dp > band && dv > band) { dead = true; break; }
+                }
+            }
+            if (!dead) {
+                peak = dp <= band && dp < 80;
+                valley = dv <= band && dv < 80;
+            }
+        }
+    }
+    const bool hit = peak || valley;
+    // warp-aggregated append
+    const unsigned mask = __ballot_sync(0xffffffffu, hit);
+    if (mask == 0) return;
+    const int lane = (threadIdx.y * 32 + threadIdx.x) & 31;
+    const int leader = __ffs(mask) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(counts + b, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (hit) {
+        const int slot = base + __popc(mask & ((1u << lane) - 1));
+        if (slot < cap) keys[(long long)b * cap + slot] = make_key(seg_base + lev, x, y, z, valley ? 1 : 0);
+    }
+}
+
+__global__ void sum_of_signs_kernel(const float* __restrict__ prev, const float* __restrict__ cur,
+                                    const float* __restrict__ next, int16_t* __restrict__ out, int nx, int ny, int nz,
+                                    long long total) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const long long plane = (long long)nx * ny, vol = plane * nz;
+    long long rem = i % vol;
+    int z = (int)(rem / plane);
+    int y = (int)((rem - (long long)z * plane) / nx);
+    int x = (int)(rem - (long long)z * plane - (long long)y * nx);
+    if (x < 1 || y < 1 || z < 1 || x >= nx - 1 || y >= ny - 1 || z >= nz - 1) {
+        out[i] = 0;
+        return;
+    }
+    const float c = cur[i];
+    int m = 0;
+    const float* vols[3] = {prev, cur, next};
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+#pragma unroll
+        for (int o = 0; o < 27; ++o) {
+            if (l == 1 && o == 13) continue;
+            const float n = __ldg(vols[l] + i + (long long)(o / 9 - 1) * plane + (long long)((o / 3) % 3 - 1) * nx + (o % 3 - 1));
+            m += (c > n) - (c < n);
+        }
+    }
+    out[i] = (int16_t)m;
+}
+
+// Candidates from a precomputed sum-of-signs map (extract_extrema, detect.py:82-140).
+__global__ void extrema_from_map_kernel(const int16_t* __restrict__ map, const float* __restrict__ dogc, int nx, int ny,
+                                        int nz, int seg, int band, float cmin, unsigned long long* __restrict__ keys,
+                                        int* __restrict__ counts, int cap) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long plane = (long long)nx * ny, vol = plane * nz;
+    bool hit = false, valley = false;
+    int x = 0, y = 0, z = 0;
+    if (i < vol) {
+        z = (int)(i / plane);
+        y = (int)((i - (long long)z * plane) / nx);
+        x = (int)(i - (long long)z * plane - (long long)y * nx);
+        if (x >= 1 && y >= 1 && z >= 1 && x < nx - 1 && y < ny - 1 && z < nz - 1 && fabsf(dogc[i]) >= cmin) {
+            const int m = map[i];
+            const bool pk = m >= 80 - band && m > 0;
+            valley = m <= -80 + band && m < 0;
+            hit = pk || valley;
+        }
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, hit);
+    if (mask == 0) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(counts, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (hit) {
+        const int slot = base + __popc(mask & ((1u << lane) - 1));
+        if (slot < cap) keys[slot] = make_key(seg, x, y, z, valley ? 1 : 0);
+    }
+}
+
+// Exclusive prefix of min(count, cap) over the batch; total[0] = keypoints,
+// total[1] = 1 if any volume overflowed its candidate capacity.
+__global__ void batch_offsets_kernel(const int* __restrict__ counts, int nb, int cap, int* __restrict__ vol_offset,
+                                     int* __restrict__ total) {
+    if (threadIdx.x != 0) return;
+    int acc = 0, over = 0;
+    for (int b = 0; b < nb; ++b) {
+        vol_offset[b] = acc;
+        int c = counts[b];
+        if (c > cap) { over = 1; c = cap; }
+        acc += c;
+    }
+    total[0] = acc;
+    total[1] = over;
+}
+
+__global__ void __launch_bounds__(256)
+order_kernel(const unsigned long long* __restrict__ keys, const int* __restrict__ counts, int cap,
+             const int* __restrict__ vol_offset, SegInfo seg, const vk_level* __restrict__ dog_levels,
+             vk_kp* __restrict__ kps, double* __restrict__ pos, double* __restrict__ sigma, float* __restrict__ dogv,
+             int8_t* __restrict__ sign, int kp_cap) {
+    __shared__ unsigned long long sk[256];
+    const int b = blockIdx.y;
+    const int n = min(counts[b], cap);
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (blockIdx.x * 256 >= n) return;
+    const unsigned long long* kb = keys + (long long)b * cap;
+    const unsigned long long key = i < n ? kb[i] : ~0ull;
+    int rank = 0;
+    for (int t = 0; t < n; t += 256) {
+        __syncthreads();
+        sk[threadIdx.x] = t + threadIdx.x < n ? kb[t + threadIdx.x] : ~0ull;
+        __syncthreads();
+        const int m = min(256, n - t);
+        for (int j = 0; j < m; ++j) rank += sk[j] < key;
+    }
+    if (i >= n) return;
+    const int out = vol_offset[b] + rank;
+    if (out >= kp_cap) return;
+    const int s = (int)(key >> 52);
+    const int z = (int)((key >> 35) & 0x1FFFF), y = (int)((key >> 18) & 0x1FFFF), x = (int)((key >> 1) & 0x1FFFF);
+    const int octave = seg.octave[s];
+    vk_kp k;
+    k.vol = b;
+    k.lvl = seg.lvl[s];
+    k.ix = x;
+    k.iy = y;
+    k.iz = z;
+    k.ball = seg.ball[s];
+    k.octave = octave;
+    k.level = seg.level[s];
+    kps[out] = k;
+    // position = i * 2^o + (2^o - 1) / 2 in fp64 (detect.py:105-131)
+    const double scale = ldexp(1.0, octave);
+    const double off = (scale - 1.0) / 2.0;
+    pos[3 * out + 0] = dadd(dmul((double)x, scale), off);
+    pos[3 * out + 1] = dadd(dmul((double)y, scale), off);
+    pos[3 * out + 2] = dadd(dmul((double)z, scale), off);
+    sigma[out] = seg.sigma[s];
+    const vk_level L = dog_levels[s];
+    dogv[out] = L.base[b * L.vol_stride + ((long long)z * L.ny + y) * L.nx + x];
+    sign[out] = (key & 1ull) ? -1 : 1;
+}
+
+}  // namespace vk
+
+using namespace vk;
+
+extern "C" int vk_sum_of_signs(const float* prev, const float* cur, const float* next, int16_t* out, int nb, int nx,
+                               int ny, int nz, void* stream) {
+    if (!prev || !cur || !next || !out || nb < 0 || nx < 1 || ny < 1 || nz < 1) {
+        set_error("vk_sum_of_signs: bad arguments");
+        return VK_ERR_PARAMETER;
+    }
+    long long total = (long long)nb * nx * ny * nz;
+    if (total == 0) return VK_OK;
+    sum_of_signs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, as_stream(stream)>>>(prev, cur, next, out, nx, ny,
+                                                                                        nz, total);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "sum_of_signs launch");
+}
+
+extern "C" int vk_detect_octave(const float* const* dogs_host, int ndog, int nb, int nx, int ny, int nz, int seg_base,
+                                int band, float contrast_min, unsigned long long* cand_keys, int* cand_count, int cap,
+                                void* stream) {
+    if (!dogs_host || ndog < 3 || ndog > kMaxDog || nb < 0 || !cand_keys || !cand_count || cap < 0 || band < 0 ||
+        band > 80 || seg_base < 0 || seg_base + ndog > 4095 || nx > 131071 || ny > 131071 || nz > 131071) {
+        set_error("vk_detect_octave: bad arguments (ndog=%d band=%d)", ndog, band);
+        return VK_ERR_PARAMETER;
+    }
+    if (nb == 0 || nx < 3 || ny < 3 || nz < 3) return VK_OK;
+    const int nlev = ndog - 2;
+    const long long vol = (long long)nx * ny * nz;
+    // grid.z <= 65535: split the batch into chunks
+    const int per = (int)(65535 / ((long long)(nz - 2) * nlev)) > 0 ? (int)(65535 / ((long long)(nz - 2) * nlev)) : 1;
+    for (int b0 = 0; b0 < nb; b0 += per) {
+        const int nbc = nb - b0 < per ? nb - b0 : per;
+        DogPtrs d{};
+        for (int i = 0; i < ndog; ++i) d.p[i] = dogs_host[i] + (long long)b0 * vol;
+        dim3 grid((nx - 2 + 31) / 32, (ny - 2 + 3) / 4, (unsigned)((long long)(nz - 2) * nlev * nbc));
+        detect_kernel<<<grid, dim3(32, 4), 0, as_stream(stream)>>>(d, nlev, nx, ny, nz, seg_base, band, contrast_min,
+                                                                   cand_keys + (long long)b0 * cap, cand_count + b0, cap);
+        count_launch();
+    }
+    return cuda_status(cudaGetLastError(), "detect launch");
+}
+
+extern "C" int vk_order_keypoints(const unsigned long long* cand_keys, const int* cand_count, int nb, int cap,
+                                  const int* seg_info_host, const double* seg_sigma_host, int nseg,
+                                  const vk_level* dog_levels, vk_kp* kps, double* pos, double* sigma, float* dog,
+                                  int8_t* sign, int* vol_offset, int* total, int kp_cap, void* stream) {
+    if (!cand_keys || !cand_count || nb < 0 || cap < 0 || !seg_info_host || !seg_sigma_host || nseg < 1 ||
+        nseg > kMaxSeg || !dog_levels || !kps || !pos || !sigma || !dog || !sign || !vol_offset || !total) {
+        set_error("vk_order_keypoints: bad arguments (nseg=%d)", nseg);
+        return VK_ERR_PARAMETER;
+    }
+    cudaStream_t st = as_stream(stream);
+    if (nb == 0) return VK_OK;
+    SegInfo s{};
+    for (int i = 0; i < nseg; ++i) {
+        s.octave[i] = seg_info_host[4 * i + 0];
+        s.level[i] = seg_info_host[4 * i + 1];
+        s.lvl[i] = seg_info_host[4 * i + 2];
+        s.ball[i] = seg_info_host[4 * i + 3];
+        s.sigma[i] = seg_sigma_host[i];
+    }
+    batch_offsets_kernel<<<1, 32, 0, st>>>(cand_count, nb, cap, vol_offset, total);
+    count_launch();
+    if (cap > 0) {
+        dim3 grid((cap + 255) / 256, nb);
+        order_kernel<<<grid, 256, 0, st>>>(cand_keys, cand_count, cap, vol_offset, s, dog_levels, kps, pos, sigma, dog,
+                                           sign, kp_cap);
+        count_launch();
+    }
+    return cuda_status(cudaGetLastError(), "order launch");
+}
+
+extern "C" int vk_extrema_from_map(const int16_t* map, const float* dog_cur, int nx, int ny, int nz, int seg, int band,
+                                   float contrast_min, unsigned long long* cand_keys, int* cand_count, int cap,
+                                   void* stream) {
+    if (!map || !dog_cur || !cand_keys || !cand_count || nx < 1 || ny < 1 || nz < 1 || band < 0 || band > 80 ||
+        seg < 0 || seg > 4095 || cap < 0) {
+        set_error("vk_extrema_from_map: bad arguments");
+        return VK_ERR_PARAMETER;
+    }
+    const long long vol = (long long)nx * ny * nz;
+    extrema_from_map_kernel<<<(unsigned)((vol + 255) / 256), 256, 0, as_stream(stream)>>>(
+        map, dog_cur, nx, ny, nz, seg, band, contrast_min, cand_keys, cand_count, cap);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "extrema launch");
+}

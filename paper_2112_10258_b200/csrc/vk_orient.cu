@@ -1,0 +1,371 @@
+// vk_orient.cu -- spherical gradient histograms and orientation frames.
+//
+// Reference: orient.py:271-307 (gradient_histogram), orient.py:310-350
+// (dominant_orientations), pipeline.py:41-67 (assign_orientations).
+//
+// One CTA (128 threads) per keypoint, persistent over the keypoint list (the
+// count lives in device memory so the whole pipeline can be graph-captured).
+// Every vote is computed bit-exactly (fp64 gradients, numpy's norm order,
+// OpenBLAS's FMA chain for the direction dots, host-numpy window table).  The
+// reference then accumulates votes strictly sequentially (np.add.at); we
+// accumulate them in a parallel order instead (private per-thread bins +
+// ordered tree), and carry a rigorous bound on the difference between the two
+// summation orders.  Every decision the frames depend on (the full weight
+// order, the secondary_ratio threshold) is checked against that bound; if any
+// decision is not certain, the CTA recomputes the histogram in the exact
+// reference order (one warp, votes broadcast lane by lane).  Either way the
+// frames are identical to the reference's.
+#include "vk_common.cuh"
+
+namespace vk {
+
+constexpr int kOriThreads = 128;
+
+struct OriShared {
+    double dirs[VK_MAX_DIRS * 3];
+    double w[VK_MAX_DIRS];
+    int order[VK_MAX_DIRS];
+    uint8_t ok[VK_MAX_DIRS * VK_MAX_DIRS];
+    int n_inside;
+    int exact;
+};
+
+// Nearest direction: first index of the maximum fp64 dot (np.argmax).
+VK_D int nearest_dir(const double* dirs, int K, double gx, double gy, double gz) {
+    int best = 0;
+    double bv = dot3_blas(gx, gy, gz, dirs[0], dirs[1], dirs[2]);
+    for (int k = 1; k < K; ++k) {
+        double v = dot3_blas(gx, gy, gz, dirs[3 * k], dirs[3 * k + 1], dirs[3 * k + 2]);
+        if (v > bv) { bv = v; best = k; }
+    }
+    return best;
+}
+
+// Vote of ball entry j, or bin -1 (outside / zero gradient).
+VK_D int ori_vote(const float* data, int nx, int ny, int nz, int cx, int cy, int cz, int packed,
+                  const double* __restrict__ win, const double* dirs, int K, double& vote, bool& inside) {
+    const int ox = unpack_off(packed, 0), oy = unpack_off(packed, 1), oz = unpack_off(packed, 2);
+    const int x = cx + ox, y = cy + oy, z = cz + oz;
+    inside = x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz;
+    if (!inside) return -1;
+    double gx, gy, gz;
+    gradient_at(data, nx, ny, nz, x, y, z, gx, gy, gz);
+    const double mag = norm3_numpy(gx, gy, gz);
+    if (!(mag > 0.0)) return -1;
+    vote = dmul(mag, __ldg(win + (ox * ox + oy * oy + oz * oz)));
+    return nearest_dir(dirs, K, gx, gy, gz);
+}
+
+// Frames from a weight vector whose comparisons are exact (dominant_orientations).
+// order[] must hold the bins sorted by (-w, index).
+VK_D int frames_from(const double* w, const int* order, int K, const uint8_t* ok, double ratio, int max_frames,
+                     int* prim, int* sec) {
+    const double top = w[order[0]];
+    if (!(top > 0.0)) return 0;
+    const double thr = dmul(ratio, top);
+    int nf = 0, taken = 0;
+    for (int r = 0; r < K && taken < max_frames; ++r) {
+        const int p = order[r];
+        if (!(w[p] >= thr)) continue;
+        ++taken;
+        for (int q2 = 0; q2 < K; ++q2) {
+            const int q = order[q2];
+            if (q == p) continue;
+            if (ok[p * K + q]) {
+                prim[nf] = p;
+                sec[nf] = q;
+                ++nf;
+                break;
+            }
+        }
+    }
+    return nf;
+}
+
+// order[] by (-w, index): parallel rank computation over the CTA.
+VK_D void sort_desc(const double* w, int K, int* order) {
+    for (int b = threadIdx.x; b < K; b += blockDim.x) {
+        int r = 0;
+        const double wb = w[b];
+        for (int j = 0; j < K; ++j) r += (w[j] > wb) || (w[j] == wb && j < b);
+        order[r] = b;
+    }
+}
+
+// Are all decisions of frames_from() the same for every weight vector within
+// +-eps of w?  (adjacent-order separation + threshold margins)
+VK_D bool frames_certain(const double* w, const int* order, int K, double epsrel, double ratio) {
+    for (int r = 0; r + 1 < K; ++r) {
+        const double a = w[order[r]], b = w[order[r + 1]];
+        if (b == 0.0) continue;  // exact zero (no votes) ties are order-independent
+        if (!(dsub(a, a * epsrel) > dadd(b, b * epsrel))) return false;
+    }
+    const double top = w[order[0]];
+    if (!(top > 0.0)) return true;
+    const double thr_lo = dmul(ratio, dsub(top, top * epsrel));
+    const double thr_hi = dmul(ratio, dadd(top, top * epsrel));
+    for (int k = 0; k < K; ++k) {
+        const double v = w[k];
+        const bool yes = dsub(v, v * epsrel) >= thr_hi;
+        const bool no = dadd(v, v * epsrel) < thr_lo;
+        if (!yes && !no) return false;
+    }
+    return true;
+}
+
+__global__ void __launch_bounds__(kOriThreads)
+orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, int n_kp_max,
+              const vk_level* __restrict__ levels, const vk_ball* __restrict__ balls,
+              const int* __restrict__ ball_offsets, const double* __restrict__ windows, const double* __restrict__ dirs_g,
+              int K, const uint8_t* __restrict__ pair_ok, double ratio, int max_frames, double* __restrict__ weights,
+              int* __restrict__ nframes, int* __restrict__ prim, int* __restrict__ sec, int* __restrict__ status,
+              int exact_only) {
+    extern __shared__ double dyn[];
+    __shared__ OriShared sh;
+    double* part = dyn;  // [K][kOriThreads] private partial sums
+    const int tid = threadIdx.x;
+    for (int i = tid; i < 3 * K; i += kOriThreads) sh.dirs[i] = dirs_g[i];
+    for (int i = tid; i < K * K; i += kOriThreads) sh.ok[i] = pair_ok[i];
+    const int n_kp = n_kp_dev ? min(*n_kp_dev, n_kp_max) : n_kp_max;
+    __syncthreads();
+
+    for (int item = blockIdx.x; item < n_kp; item += gridDim.x) {
+        const vk_kp kp = kps[item];
+        const vk_level L = levels[kp.lvl];
+        const float* data = L.base + (long long)kp.vol * L.vol_stride;
+        const vk_ball ball = balls[kp.ball];
+        const double* win = windows + ball.window_start;
+        for (int b = 0; b < K; ++b) part[b * kOriThreads + tid] = 0.0;
+        if (tid == 0) { sh.n_inside = 0; sh.exact = exact_only; }
+        __syncthreads();
+        int inside_cnt = 0;
+        if (!exact_only) {
+            for (int j = tid; j < ball.count; j += kOriThreads) {
+                double vote;
+                bool inside;
+                const int bin = ori_vote(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz, __ldg(ball_offsets + ball.start + j),
+                                         win, sh.dirs, K, vote, inside);
+                inside_cnt += inside;
+                if (bin >= 0) part[bin * kOriThreads + tid] = dadd(part[bin * kOriThreads + tid], vote);
+            }
+        } else {
+            for (int j = tid; j < ball.count; j += kOriThreads) {
+                const int p = __ldg(ball_offsets + ball.start + j);
+                const int x = kp.ix + unpack_off(p, 0), y = kp.iy + unpack_off(p, 1), z = kp.iz + unpack_off(p, 2);
+                inside_cnt += x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz;
+            }
+        }
+        if (inside_cnt) atomicAdd(&sh.n_inside, inside_cnt);
+        __syncthreads();
+        if (sh.n_inside == 0) {
+            // DataError: orientation neighbourhood entirely outside (orient.py:291-292)
+            if (tid == 0) {
+                atomicOr(status, 1);
+                nframes[item] = 0;
+            }
+            __syncthreads();
+            continue;
+        }
+        if (!exact_only) {
+            for (int b = tid; b < K; b += kOriThreads) {
+                double s = 0.0;
+                for (int t = 0; t < kOriThreads; ++t) s = dadd(s, part[b * kOriThreads + t]);
+                sh.w[b] = s;
+            }
+            __syncthreads();
+            sort_desc(sh.w, K, sh.order);
+            __syncthreads();
+            if (tid == 0) {
+                const double per = (double)((ball.count + kOriThreads - 1) / kOriThreads) + kOriThreads;
+                const double epsrel = 1.001 * (gamma_k((double)sh.n_inside) + gamma_k(per)) + 1e-300;
+                if (!frames_certain(sh.w, sh.order, K, epsrel, ratio)) sh.exact = 1;
+            }
+            __syncthreads();
+        }
+        if (sh.exact) {
+            // Exact reference order: votes in ball order, each bin summed sequentially.
+            if (tid < 32) {
+                double acc0 = 0.0, acc1 = 0.0;
+                for (int base = 0; base < ball.count; base += 32) {
+                    const int j = base + tid;
+                    double vote = 0.0;
+                    bool inside;
+                    int bin = -1;
+                    if (j < ball.count)
+                        bin = ori_vote(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz, __ldg(ball_offsets + ball.start + j),
+                                       win, sh.dirs, K, vote, inside);
+                    for (int s = 0; s < 32; ++s) {
+                        const int bs = __shfl_sync(0xffffffffu, bin, s);
+                        const double vs = __shfl_sync(0xffffffffu, vote, s);
+                        if (bs == tid) acc0 = dadd(acc0, vs);
+                        else if (bs == tid + 32) acc1 = dadd(acc1, vs);
+                    }
+                }
+                if (tid < K) sh.w[tid] = acc0;
+                if (tid + 32 < K) sh.w[tid + 32] = acc1;
+            }
+            __syncthreads();
+            sort_desc(sh.w, K, sh.order);
+            __syncthreads();
+        }
+        if (weights)
+            for (int b = tid; b < K; b += kOriThreads) weights[(long long)item * K + b] = sh.w[b];
+        if (tid == 0) {
+            int pr[VK_MAX_FRAMES], se[VK_MAX_FRAMES];
+            const int nf = frames_from(sh.w, sh.order, K, sh.ok, ratio, max_frames, pr, se);
+            nframes[item] = nf;
+            for (int f = 0; f < nf; ++f) {
+                prim[item * max_frames + f] = pr[f];
+                sec[item * max_frames + f] = se[f];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Frames from host-supplied weights (dominant_orientations on a histogram).
+__global__ void frames_from_weights_kernel(const double* __restrict__ weights, int n, int K,
+                                           const uint8_t* __restrict__ pair_ok, double ratio, int max_frames,
+                                           int* __restrict__ nframes, int* __restrict__ prim, int* __restrict__ sec) {
+    __shared__ double w[VK_MAX_DIRS];
+    __shared__ int order[VK_MAX_DIRS];
+    __shared__ uint8_t ok[VK_MAX_DIRS * VK_MAX_DIRS];
+    for (int i = threadIdx.x; i < K * K; i += blockDim.x) ok[i] = pair_ok[i];
+    for (int item = blockIdx.x; item < n; item += gridDim.x) {
+        __syncthreads();
+        for (int b = threadIdx.x; b < K; b += blockDim.x) w[b] = weights[(long long)item * K + b];
+        __syncthreads();
+        sort_desc(w, K, order);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int pr[VK_MAX_FRAMES], se[VK_MAX_FRAMES];
+            const int nf = frames_from(w, order, K, ok, ratio, max_frames, pr, se);
+            nframes[item] = nf;
+            for (int f = 0; f < nf; ++f) {
+                prim[item * max_frames + f] = pr[f];
+                sec[item * max_frames + f] = se[f];
+            }
+        }
+    }
+}
+
+// Ordered expansion of per-keypoint frames (single CTA block scan).
+__global__ void __launch_bounds__(1024)
+expand_frames_kernel(const int* __restrict__ nframes, const int* __restrict__ prim, const int* __restrict__ sec,
+                     const int* __restrict__ n_kp_dev, int n_kp_max, int max_frames, const double* __restrict__ rot_table,
+                     int K, vk_frame* __restrict__ frames, double* __restrict__ rot, int* __restrict__ n_frames_dev,
+                     int* __restrict__ dropped_dev, int frame_cap) {
+    __shared__ int warp_sums[32];
+    __shared__ int carry_s, dropped_s;
+    const int n = n_kp_dev ? min(*n_kp_dev, n_kp_max) : n_kp_max;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) { carry_s = 0; dropped_s = 0; }
+    __syncthreads();
+    for (int base = 0; base < n; base += 1024) {
+        const int i = base + tid;
+        const int nf = i < n ? nframes[i] : 0;
+        if (i < n && nf == 0) atomicAdd(&dropped_s, 1);
+        int v = nf;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (lane == 31) warp_sums[wid] = v;
+        __syncthreads();
+        if (wid == 0) {
+            int s = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += t;
+            }
+            warp_sums[lane] = s;
+        }
+        __syncthreads();
+        const int carry = carry_s;
+        const int excl = carry + v - nf + (wid > 0 ? warp_sums[wid - 1] : 0);
+        for (int f = 0; f < nf; ++f) {
+            const int o = excl + f;
+            if (o >= frame_cap) break;
+            const int p = prim[i * max_frames + f], q = sec[i * max_frames + f];
+            vk_frame fr;
+            fr.kp = i;
+            fr.prim = p;
+            fr.sec = q;
+            fr.pad_ = 0;
+            frames[o] = fr;
+            const double* R = rot_table + ((long long)p * K + q) * 9;
+            for (int e = 0; e < 9; ++e) rot[(long long)o * 9 + e] = R[e];
+        }
+        __syncthreads();
+        if (tid == 1023) carry_s = excl + nf;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        n_frames_dev[0] = carry_s;
+        dropped_dev[0] = dropped_s;
+    }
+}
+
+}  // namespace vk
+
+using namespace vk;
+
+extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_level* levels,
+                         const vk_ball* balls, const int* ball_offsets, const double* windows, const double* dirs, int K,
+                         const uint8_t* pair_ok, double secondary_ratio, int max_frames, double* weights, int* nframes,
+                         int* prim, int* sec, int* status, int exact_only, void* stream) {
+    if (!kps || n_kp_max < 0 || !levels || !balls || !ball_offsets || !windows || !dirs || K < 1 || K > VK_MAX_DIRS ||
+        !pair_ok || !nframes || !prim || !sec || !status || max_frames < 1 || max_frames > VK_MAX_FRAMES ||
+        !(secondary_ratio > 0.0 && secondary_ratio <= 1.0)) {
+        set_error("vk_orient: bad arguments (K=%d max_frames=%d)", K, max_frames);
+        return VK_ERR_PARAMETER;
+    }
+    if (n_kp_max == 0) return VK_OK;
+    const int smem = K * kOriThreads * (int)sizeof(double);
+    static int configured = 0;
+    if (configured < smem) {
+        cudaError_t e = cudaFuncSetAttribute(orient_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, VK_MAX_DIRS * kOriThreads * 8);
+        if (e != cudaSuccess) return cuda_status(e, "orient attribute");
+        configured = VK_MAX_DIRS * kOriThreads * 8;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = n_kp_max < sms * 4 ? n_kp_max : sms * 4;
+    orient_kernel<<<grid, kOriThreads, smem, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
+                                                                  windows, dirs, K, pair_ok, secondary_ratio, max_frames,
+                                                                  weights, nframes, prim, sec, status, exact_only);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "orient launch");
+}
+
+extern "C" int vk_frames_from_weights(const double* weights, int n, int K, const uint8_t* pair_ok,
+                                      double secondary_ratio, int max_frames, int* nframes, int* prim, int* sec,
+                                      void* stream) {
+    if (!weights || n < 0 || K < 1 || K > VK_MAX_DIRS || !pair_ok || !nframes || !prim || !sec || max_frames < 1 ||
+        max_frames > VK_MAX_FRAMES || !(secondary_ratio > 0.0 && secondary_ratio <= 1.0)) {
+        set_error("vk_frames_from_weights: bad arguments");
+        return VK_ERR_PARAMETER;
+    }
+    if (n == 0) return VK_OK;
+    frames_from_weights_kernel<<<n < 1024 ? n : 1024, 64, 0, as_stream(stream)>>>(weights, n, K, pair_ok, secondary_ratio,
+                                                                                   max_frames, nframes, prim, sec);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "frames launch");
+}
+
+extern "C" int vk_expand_frames(const int* nframes, const int* prim, const int* sec, const int* n_kp_dev, int n_kp_max,
+                                int max_frames, const double* rot_table, int K, vk_frame* frames, double* rot,
+                                int* n_frames_dev, int* dropped_dev, int frame_cap, void* stream) {
+    if (!nframes || !prim || !sec || n_kp_max < 0 || max_frames < 1 || !rot_table || K < 1 || !frames || !rot ||
+        !n_frames_dev || !dropped_dev || frame_cap < 0) {
+        set_error("vk_expand_frames: bad arguments");
+        return VK_ERR_PARAMETER;
+    }
+    expand_frames_kernel<<<1, 1024, 0, as_stream(stream)>>>(nframes, prim, sec, n_kp_dev, n_kp_max, max_frames, rot_table,
+                                                            K, frames, rot, n_frames_dev, dropped_dev, frame_cap);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "expand launch");
+}

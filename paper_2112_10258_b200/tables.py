@@ -1,0 +1,195 @@
+"""Host-side constant tables uploaded to the GPU.
+
+These are the small per-configuration constants the reference also computes
+on the host: Gaussian taps, the icosphere, integer balls and their Gaussian
+windows, the 42 x 42 frame table, the patch grid and the BRIEF point pairs.
+They are evaluated with the same numpy expressions as the reference (same
+ufuncs, same evaluation order), so every table is bit-identical to the values
+the reference uses -- including numpy's SIMD ``exp`` and OpenBLAS's ``dot``,
+which a device re-implementation would not reproduce.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from functools import lru_cache
+
+import numpy as np
+
+from .errors import ParameterError
+
+
+# ---------------------------------------------------------------- Gaussians
+@dataclass(frozen=True)
+class GaussianKernel1D:
+    """Sampled normalised 1-D Gaussian, radius ceil(3 sigma) (scalespace.py:54-70)."""
+
+    sigma: float
+    radius: int
+    weights: np.ndarray
+
+
+@lru_cache(maxsize=256)
+def gaussian_kernel(sigma: float) -> GaussianKernel1D:
+    if sigma <= 0:
+        raise ParameterError(f"sigma must be > 0, got {sigma}")
+    radius = max(1, math.ceil(3.0 * sigma))
+    k = np.arange(-radius, radius + 1, dtype=np.float64)
+    w = np.exp(-(k ** 2) / (2.0 * sigma * sigma))
+    w /= w.sum()
+    w = w.astype(np.float32)
+    w.setflags(write=False)
+    return GaussianKernel1D(float(sigma), radius, w)
+
+
+def incremental_sigma(current: float, target: float) -> float:
+    """scalespace.py:182-183."""
+    return math.sqrt(max(target * target - current * current, 0.0))
+
+
+def octave_sigmas(base_sigma: float, levels: int):
+    """kappa and octave-local sigmas (scalespace.py:207-209)."""
+    kappa = 2.0 ** (1.0 / (levels - 3))
+    return kappa, [base_sigma * kappa ** i for i in range(levels)]
+
+
+# --------------------------------------------------------------- directions
+@lru_cache(maxsize=1)
+def icosphere_directions() -> np.ndarray:
+    """42 lexsorted unit vectors: icosahedron vertices + edge midpoints (orient.py:215-241)."""
+    phi = (1.0 + math.sqrt(5.0)) / 2.0
+    pts = []
+    for a in (-1.0, 1.0):
+        for b in (-phi, phi):
+            pts += [(0.0, a, b), (a, b, 0.0), (b, 0.0, a)]
+    v = np.array(pts, dtype=np.float64)
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    d2 = np.sum((v[:, None, :] - v[None, :, :]) ** 2, axis=2)
+    edge = np.min(d2[d2 > 1e-9])
+    mids = []
+    for i in range(len(v)):
+        for j in range(i + 1, len(v)):
+            if abs(d2[i, j] - edge) < 1e-9:
+                m = v[i] + v[j]
+                mids.append(m / np.linalg.norm(m))
+    allv = np.vstack([v, np.array(mids)])
+    allv = allv[np.lexsort((allv[:, 2].round(9), allv[:, 1].round(9), allv[:, 0].round(9)))]
+    allv.setflags(write=False)
+    return allv
+
+
+def frame_tables(dirs: np.ndarray):
+    """For every (primary p, candidate secondary q): whether q's projection
+    orthogonal to p is usable (norm > 1e-6) and the resulting right-handed
+    frame [a1, a2, a1 x a2] (orient.py:333-349), evaluated with the reference's
+    own numpy calls so the rotations are bit-identical."""
+    dirs = np.asarray(dirs, dtype=np.float64)
+    K = len(dirs)
+    ok = np.zeros((K, K), dtype=np.uint8)
+    rot = np.zeros((K, K, 3, 3), dtype=np.float64)
+    for p in range(K):
+        a1 = dirs[p]
+        for q in range(K):
+            if q == p:
+                continue
+            proj = dirs[q] - np.dot(dirs[q], a1) * a1
+            nrm = np.linalg.norm(proj)
+            if nrm > 1e-6:
+                a2 = proj / nrm
+                ok[p, q] = 1
+                rot[p, q] = np.column_stack([a1, a2, np.cross(a1, a2)])
+    return ok, rot
+
+
+@lru_cache(maxsize=4)
+def default_frame_tables():
+    return frame_tables(icosphere_directions())
+
+
+# -------------------------------------------------------------------- balls
+@lru_cache(maxsize=256)
+def ball_offsets(radius_q: int) -> np.ndarray:
+    """Integer offsets with |o| <= radius_q/1024, x-major / z-minor (orient.py:244-255)."""
+    rad = radius_q / 1024.0
+    r = int(math.floor(rad))
+    ax = np.arange(-r, r + 1)
+    g = np.stack([a.ravel() for a in np.meshgrid(ax, ax, ax, indexing="ij")], axis=1)
+    out = g[np.sum(g * g, axis=1) <= rad * rad].astype(np.intp)
+    out.setflags(write=False)
+    return out
+
+
+def pack_offsets(offs: np.ndarray) -> np.ndarray:
+    """10 bits per axis, biased by 512 (vk_common.cuh unpack_off)."""
+    o = np.asarray(offs, dtype=np.int64)
+    if len(o) and np.abs(o).max() > 511:
+        raise ParameterError("neighbourhood radius above 511 voxels is not supported")
+    return (((o[:, 0] + 512) << 20) | ((o[:, 1] + 512) << 10) | (o[:, 2] + 512)).astype(np.int32)
+
+
+def window_table(radius: float, max_d2: int) -> np.ndarray:
+    """Orientation window exp(-|o|^2 / (2 (radius/2)^2)) for |o|^2 = 0..max_d2,
+    the exact numpy expression of orient.py:298-299 (host numpy exp)."""
+    window_sd = radius / 2.0
+    d2 = np.arange(max_d2 + 1, dtype=np.float64)
+    return np.exp(-d2 / (2.0 * window_sd * window_sd))
+
+
+class BallTable:
+    """Concatenated balls for a set of radii, as uploaded to the device."""
+
+    def __init__(self):
+        self.radii: list[float] = []
+        self._index: dict[float, int] = {}
+        self.records: list[tuple[int, int, int, int]] = []
+        self._off: list[np.ndarray] = []
+        self._win: list[np.ndarray] = []
+        self._noff = 0
+        self._nwin = 0
+
+    def index(self, radius: float) -> int:
+        """Ball id for an orientation / SIFT-Rank radius (radius_factor * sigma_local)."""
+        key = float(radius)
+        if key in self._index:
+            return self._index[key]
+        offs = ball_offsets(int(round(radius * 1024)))
+        max_d2 = int(np.max(np.sum(offs * offs, axis=1))) if len(offs) else 0
+        self._index[key] = len(self.records)
+        self.records.append((self._noff, len(offs), self._nwin, max_d2))
+        self._off.append(pack_offsets(offs))
+        self._win.append(window_table(radius, max_d2))
+        self._noff += len(offs)
+        self._nwin += max_d2 + 1
+        self.radii.append(key)
+        return self._index[key]
+
+    def arrays(self):
+        from ._lib import BALL_DTYPE
+
+        rec = np.array(self.records, dtype=np.int32).reshape(-1, 4)
+        balls = np.zeros(len(rec), dtype=BALL_DTYPE)
+        for i, name in enumerate(BALL_DTYPE.names):
+            balls[name] = rec[:, i] if len(rec) else 0
+        off = np.concatenate(self._off) if self._off else np.zeros(1, np.int32)
+        win = np.concatenate(self._win) if self._win else np.zeros(1, np.float64)
+        return balls, off, win
+
+
+# ------------------------------------------------------------ patch & pairs
+PAIR_SUPPORT_RADIUS = 2.0  # descriptor.py:34
+
+
+@lru_cache(maxsize=32)
+def patch_axis(side: int) -> np.ndarray:
+    """One axis of descriptor.py:86-93's grid (linspace(-1, 1, side))."""
+    a = np.linspace(-1.0, 1.0, side) if side > 1 else np.zeros(1)
+    a.setflags(write=False)
+    return a
+
+
+def pair_points(p1: np.ndarray, p2: np.ndarray, side: int, sigma_unit: float) -> np.ndarray:
+    """Pair sample positions in patch index space (descriptor.py:205-212)."""
+    center = (side - 1) / 2.0
+    scale = (side - 1) / (2.0 * PAIR_SUPPORT_RADIUS) / sigma_unit
+    return np.stack([center + p1 * scale, center + p2 * scale]).astype(np.float64)

@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path against golden vectors made by the real reference.
+
+Every comparison is exact (np.array_equal / sha256 of float32 bytes): the
+hot path is integer / fixed-order IEEE arithmetic and the kernels reproduce
+the reference's rounding sequence.  Inputs are
+regenerated from seeds with ``paper_2112_10258_b200.synthetic`` and checked
+against the input hash stored in the fixture.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, sha
+
+pytestmark = pytest.mark.gpu
+
+vk = pytest.importorskip("paper_2112_10258_b200")
+from paper_2112_10258_b200 import synthetic  # noqa: E402
+from paper_2112_10258_b200.config import PipelineConfig  # noqa: E402
+
+CFG2 = dict(levels_per_octave=5, threshold_band=2, contrast_min=0.003, num_octaves=3, secondary_ratio=0.7,
+            max_frames=3, pairs=48, method=1, blur_sigma=1.3, seed=4)
+KINDS = ("siftrank", "brief", "rrief")
+
+
+def small_volume(g):
+    dims = tuple(int(d) for d in g["dims"])
+    return synthetic.random_blob_phantom(dims, np.random.default_rng(int(g["seed"])), n_blobs=10, margin=6, noise=0.02)
+
+
+def case_inputs(name):
+    g = load_golden(name)
+    if name.startswith("small"):
+        vol = small_volume(g)
+        cfg = PipelineConfig()
+    elif name == "soup_cfg2.npz":
+        vol = synthetic.soup_volume(tuple(int(d) for d in g["dims"]), np.random.default_rng(5), noise=0.01)
+        cfg = PipelineConfig(**CFG2)
+    else:
+        vol = synthetic.brain_volume()
+        cfg = PipelineConfig()
+    assert sha(vol) == str(g["input_sha"]), "synthetic input generator diverged from the golden input"
+    return g, vol, cfg
+
+
+def check_extraction(g, vol, cfg, prefix=""):
+    for kind in KINDS:
+        res = vk.extract_features(vk.Volume(vol), cfg.model_copy(update={"descriptor": kind}))
+        if kind == "siftrank":
+            dims = [o.levels[0].dims for o in res.pyramid.octaves]
+            assert np.array_equal(np.array(dims), g[prefix + "pyr_dims"])
+            got = np.array([[sha(lv.data) for lv in o.levels] for o in res.pyramid.octaves])
+            assert np.array_equal(got, g[prefix + "pyr_sha"]), "gaussian pyramid differs"
+            got = np.array([[sha(lv.data) for lv in o.levels] for o in res.dog.octaves])
+            assert np.array_equal(got, g[prefix + "dog_sha"]), "DoG pyramid differs"
+            kps = res.keypoints
+            assert len(kps) == len(g[prefix + "kp_sigma"])
+            assert np.array_equal(np.array([k.position for k in kps]).reshape(-1, 3), g[prefix + "kp_pos"])
+            assert np.array_equal(np.array([k.sigma for k in kps]), g[prefix + "kp_sigma"])
+            assert np.array_equal(np.array([k.octave for k in kps]), g[prefix + "kp_octave"])
+            assert np.array_equal(np.array([k.level for k in kps]), g[prefix + "kp_level"])
+            assert np.array_equal(np.array([k.dog_value for k in kps]), g[prefix + "kp_dog"])
+            assert np.array_equal(np.array([1 if k.sign == "peak" else -1 for k in kps]), g[prefix + "kp_sign"])
+            idx = {id(k): i for i, k in enumerate(kps)}
+            assert np.array_equal(np.array([idx[id(k)] for k, _ in res.oriented]), g[prefix + "fr_kp"])
+            assert np.array_equal(np.array([f.rotation for _, f in res.oriented]).reshape(-1, 3, 3), g[prefix + "fr_rot"])
+            assert res.dropped_orientation == int(g[prefix + "dropped_orientation"])
+        arr = vk.descriptor.descriptor_array(res.records, kind)
+        want = g[prefix + f"desc_{kind}"]
+        assert arr.shape == want.shape, kind
+        assert np.array_equal(arr.astype(np.int64), want.astype(np.int64)), f"{kind} descriptors differ"
+
+
+# ------------------------------------------------------------------- units
+def test_blur_units(golden_unit):
+    g = golden_unit
+    i = 0
+    while f"blur{i}_dims" in g:
+        dims = tuple(int(d) for d in g[f"blur{i}_dims"])
+        a = np.random.default_rng(100 + i).random(dims, dtype=np.float32)
+        k = vk.scalespace.gaussian_kernel(float(g[f"blur{i}_sigma"]))
+        out = vk.scalespace.convolve_array(a, k)
+        assert np.array_equal(out, g[f"blur{i}_out"]), f"blur case {i} {dims}"
+        i += 1
+    assert i >= 7
+
+
+def test_blur_all_radii_match_oracle():
+    """Every radius the ring kernel instantiates (1..10) plus the generic path."""
+    from oracle import volkey_oracle as O
+
+    rng = np.random.default_rng(7)
+    for sigma in (0.3, 0.6, 0.9, 1.2, 1.5, 1.9, 2.2, 2.6, 2.9, 3.2, 3.6, 4.5, 6.0):
+        dims = tuple(int(d) for d in rng.integers(3, 40, size=3))
+        a = rng.random(dims, dtype=np.float32)
+        r, w = O.gauss_taps(sigma)
+        want = O.blur3(a, w)
+        got = vk.scalespace.convolve_array(a, vk.scalespace.gaussian_kernel(sigma))
+        assert np.array_equal(got, want), f"sigma {sigma} radius {r} dims {dims}"
+
+
+def test_subsample_units(golden_unit):
+    g = golden_unit
+    for i in range(4):
+        dims = tuple(int(d) for d in g[f"sub{i}_dims"])
+        a = np.random.default_rng(200 + i).random(dims, dtype=np.float32)
+        out = vk.scalespace.subsample_half(vk.Volume(a))
+        assert np.array_equal(out.data, g[f"sub{i}_out"])
+
+
+def test_sum_of_signs_units(golden_unit):
+    g = golden_unit
+    for i in range(3):
+        dims = tuple(int(d) for d in g[f"sos{i}_dims"])
+        r = np.random.default_rng(300 + i)
+        tri = [vk.Volume(r.random(dims, dtype=np.float32)) for _ in range(3)]
+        assert np.array_equal(vk.detect.sum_of_signs_map(*tri), g[f"sos{i}_map"])
+
+
+def test_nn_units(golden_unit):
+    g = golden_unit
+    for metric, a, b, want in (("euclidean", g["nn_eu_a"].astype(np.int64), g["nn_eu_b"].astype(np.int64), g["nn_eu"]),
+                               ("hamming", g["nn_ha_a"], g["nn_ha_b"], g["nn_ha"])):
+        ms = vk.nearest_neighbor_matches(a, b, 0.9, metric)
+        got = np.array([(m.index_a, m.index_b, m.distance, m.second_distance) for m in ms])
+        assert np.array_equal(got, want), metric
+
+
+def test_nn_float_and_ties():
+    from oracle import volkey_oracle as O
+
+    rng = np.random.default_rng(3)
+    a, b = rng.random((40, 16)), rng.random((55, 16))
+    ms = vk.nearest_neighbor_matches(a, b, 1.0)
+    ref = O.nn_match(a, b, 1.0)
+    assert [(m.index_a, m.index_b) for m in ms] == [(r[0], r[1]) for r in ref]
+    np.testing.assert_allclose([m.distance for m in ms], [r[2] for r in ref], rtol=1e-9)
+    # identical rows: ties keep the lower index and d2 == d1
+    c = rng.integers(0, 64, size=(10, 64))
+    b2 = np.concatenate([c, c])
+    ms = vk.nearest_neighbor_matches(c, b2, 1.0)
+    assert [(m.index_a, m.index_b, m.distance, m.second_distance) for m in ms] == [(i, i, 0.0, 0.0) for i in range(10)]
+
+
+# ------------------------------------------------------------ end to end
+@pytest.mark.parametrize("name", ["small0.npz", "small1.npz", "small2.npz", "soup_cfg2.npz"])
+def test_small_cases(name):
+    g, vol, cfg = case_inputs(name)
+    check_extraction(g, vol, cfg)
+
+
+@pytest.mark.parametrize("name", ["small0.npz", "small2.npz", "soup_cfg2.npz"])
+def test_gradient_histograms_exact(name):
+    g, vol, cfg = case_inputs(name)
+    pyr = vk.build_gaussian_pyramid(vk.Volume(vol), cfg.base_sigma, cfg.levels_per_octave, cfg.num_octaves,
+                                    min_octave_dim=cfg.min_octave_dim)
+    for i in range(len(g["kp_sigma"])):
+        kp = vk.Keypoint(tuple(g["kp_pos"][i]), float(g["kp_sigma"][i]), int(g["kp_octave"][i]), int(g["kp_level"][i]),
+                         float(g["kp_dog"][i]), "peak" if g["kp_sign"][i] > 0 else "valley")
+        h = vk.orient.gradient_histogram(pyr, kp, cfg.radius_factor)
+        assert np.array_equal(h.weights, g["hist"][i]), f"keypoint {i}"
+
+
+def test_stage_api_composition():
+    """build_gaussian_pyramid -> build_dog_pyramid -> detect_keypoints ->
+    assign_orientations -> describe_all, the composition of
+    tests/test_acceptance.py:53-89, equals the fused pipeline."""
+    g, vol, cfg = case_inputs("small2.npz")
+    v = vk.Volume(vol)
+    pyr = vk.build_gaussian_pyramid(v)
+    dog = vk.build_dog_pyramid(pyr)
+    assert np.array_equal(np.array([[sha(lv.data) for lv in o.levels] for o in dog.octaves]), g["dog_sha"])
+    kps = vk.detect_keypoints(dog)
+    assert np.array_equal(np.array([k.position for k in kps]), g["kp_pos"])
+    oriented, dropped = vk.assign_orientations(pyr, kps, cfg)
+    assert np.array_equal(np.array([f.rotation for _, f in oriented]), g["fr_rot"])
+    for kind in KINDS:
+        pairs = None if kind == "siftrank" else vk.descriptor.sample_point_pairs(cfg.method, cfg.pairs, 1.0, cfg.seed)
+        recs, dd = vk.descriptor.describe_all(pyr, oriented, kind, pairs)
+        assert dd == 0
+        assert np.array_equal(vk.descriptor.descriptor_array(recs, kind).astype(np.int64),
+                              g[f"desc_{kind}"].astype(np.int64)), kind
+
+
+@pytest.mark.slow
+def test_brain_volume():
+    """configs[0]: 145x174x145 soup phantom -> 1924 keypoints / 3400 frames, all exact."""
+    g, vol, cfg = case_inputs("brain.npz")
+    assert len(g["kp_sigma"]) == 1924 and len(g["fr_kp"]) == 3400
+    check_extraction(g, vol, cfg)
+
+
+@pytest.mark.slow
+def test_fast_and_exact_accumulation_agree():
+    """The bounded parallel accumulation must give the same frames and ranks
+    as forcing the reference-order accumulation everywhere."""
+    g, vol, cfg = case_inputs("brain.npz")
+    outs = []
+    for exact in (False, True):
+        ex = vk.Extractor(vol.shape, cfg, batch=1, exact_only=exact)
+        ex.input[0].copy_(vk.volume.to_device(vol))
+        ex.enqueue()
+        outs.append(ex.results())
+    a, b = outs
+    assert np.array_equal(a["frame_prim"], b["frame_prim"]) and np.array_equal(a["frame_sec"], b["frame_sec"])
+    assert np.array_equal(a["desc"], b["desc"])
+    assert np.array_equal(a["desc"], g["desc_siftrank"])
+
+
+@pytest.mark.slow
+def test_pair_matching():
+    """configs[1]: two-volume matching, all three descriptor kinds."""
+    g = load_golden("pair.npz")
+    va, vb = synthetic.match_pair()
+    assert sha(va) == str(g["a_input_sha"]) and sha(vb) == str(g["b_input_sha"])
+    cfg = PipelineConfig()
+    for kind, metric in (("siftrank", "euclidean"), ("brief", "hamming"), ("rrief", "euclidean")):
+        c = cfg.model_copy(update={"descriptor": kind})
+        ra = vk.extract_features(vk.Volume(va), c)
+        rb = vk.extract_features(vk.Volume(vb), c)
+        da = vk.descriptor.descriptor_array(ra.records, kind)
+        db = vk.descriptor.descriptor_array(rb.records, kind)
+        assert np.array_equal(da.astype(np.int64), g[f"a_desc_{kind}"].astype(np.int64))
+        assert np.array_equal(db.astype(np.int64), g[f"b_desc_{kind}"].astype(np.int64))
+        ms = vk.nearest_neighbor_matches(da, db, cfg.ratio_max, metric)
+        got = np.array([(m.index_a, m.index_b, m.distance, m.second_distance) for m in ms])
+        assert np.array_equal(got, g[f"nn_{kind}"]), kind
+
+
+def test_batch_equals_single():
+    """Batched extraction (volume-major SoA) equals one-volume extraction."""
+    vols = [small_volume(load_golden(f"small{i}.npz")) for i in (0, 2)]
+    vols = [v[:40, :44, :36] for v in vols]
+    batch = np.stack(vols)
+    res = vk.extract_batch(batch, PipelineConfig())
+    off = list(res["vol_offset"]) + [res["n_keypoints"]]
+    for b, v in enumerate(vols):
+        single = vk.extract_features(vk.Volume(v))
+        n = off[b + 1] - off[b]
+        assert n == len(single.keypoints)
+        assert np.array_equal(res["pos"][off[b]:off[b + 1]], np.array([k.position for k in single.keypoints]).reshape(-1, 3))
+        sel = (res["frame_kp"] >= off[b]) & (res["frame_kp"] < off[b + 1])
+        assert np.array_equal(res["desc"][sel].astype(np.int64),
+                              vk.descriptor.descriptor_array(single.records, "siftrank"))
+
+
+def test_edge_cases():
+    # tiny volumes: octave truncation, no keypoints, 1-voxel dims
+    for dims in ((1, 1, 1), (2, 3, 2), (5, 5, 5), (9, 3, 12)):
+        a = np.random.default_rng(1).random(dims, dtype=np.float32)
+        from oracle import volkey_oracle as O
+
+        res = vk.extract_features(vk.Volume(a), PipelineConfig(num_octaves=3))
+        want = O.extract(a, num_octaves=3)
+        assert [len(o.levels) for o in res.pyramid.octaves] == [len(o) for o in want["pyramid"]["octaves"]]
+        for o, oc in enumerate(res.pyramid.octaves):
+            for i, lv in enumerate(oc.levels):
+                assert np.array_equal(lv.data, want["pyramid"]["octaves"][o][i])
+        assert len(res.keypoints) == len(want["keypoints"])
+    # constant volume: no keypoints, no frames
+    res = vk.extract_features(vk.Volume(np.full((20, 20, 20), 3.0, np.float32)))
+    assert res.stats["keypoints"] == 0 and res.records == []
+    # errors mirror the reference
+    with pytest.raises(vk.ParameterError):
+        vk.scalespace.subsample_half(vk.Volume(np.zeros((1, 4, 4), np.float32)))
+    with pytest.raises(vk.ParameterError):
+        vk.build_gaussian_pyramid(vk.Volume(np.zeros((8, 8, 8), np.float32)), levels_per_octave=3)
+    with pytest.raises(vk.ParameterError):
+        vk.nearest_neighbor_matches(np.zeros((3, 8)), np.zeros((1, 8)))
