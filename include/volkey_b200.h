@@ -148,13 +148,17 @@ int vk_order_keypoints(const unsigned long long* cand_keys, const int* cand_coun
  * dirs: K x 3 fp64 directions; pair_ok: K x K uint8 (norm of projection > 1e-6,
  * orient.py:339-343).  Outputs: weights (n x K fp64, nullable), nframes[n],
  * prim/sec[n*max_frames].  status[0] |= 1 when a keypoint's neighbourhood lies
- * outside its volume (DataError, orient.py:291-292). */
+ * outside its volume (DataError, orient.py:291-292).  ico_host (nullable, K==42
+ * only): 12 icosahedron-vertex indices into dirs followed by 12x5 indices of
+ * the edge midpoints around each vertex, enabling the screened argmax.
+ * exact_only != 0 forces the reference accumulation order and the brute-force
+ * argmax for every keypoint (weights then bit-identical to the reference). */
 int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_level* levels,
               const vk_ball* balls, const int* ball_offsets, const double* windows,
               const double* dirs, int K, const uint8_t* pair_ok,
               double secondary_ratio, int max_frames,
               double* weights, int* nframes, int* prim, int* sec, int* status,
-              int exact_only, void* stream);
+              int exact_only, const int* ico_host, void* stream);
 
 /* dominant_orientations (orient.py:310-350) on n caller-supplied K-bin
  * weight vectors (exact comparisons). */
@@ -164,11 +168,11 @@ int vk_frames_from_weights(const double* weights, int n, int K, const uint8_t* p
 /* Expand per-keypoint frames into the ordered frame list (pipeline.py:55-67:
  * keypoints with zero frames are dropped).  rot_table: K*K*9 fp64 rotations
  * (column-stacked axes, orient.py:346-347).  Writes frames[], rot[9*j],
- * n_frames_dev[0], dropped_dev[0]. */
+ * n_frames_dev[0], dropped_dev[0].  scratch: n_kp_max ints (device). */
 int vk_expand_frames(const int* nframes, const int* prim, const int* sec, const int* n_kp_dev,
                      int n_kp_max, int max_frames, const double* rot_table, int K,
                      vk_frame* frames, double* rot, int* n_frames_dev, int* dropped_dev,
-                     int frame_cap, void* stream);
+                     int frame_cap, int* scratch, void* stream);
 
 /* ------------------------------------------------------------ descriptors */
 /* sift_rank_descriptor (descriptor.py:227-263): 64 stable ranks per frame

@@ -108,6 +108,58 @@ VK_D void gradient_at(const float* __restrict__ d, int nx, int ny, int nz, int x
     gz = dmul(dsub(vzh, vzl), (zh - zl) == 2 ? 0.5 : 1.0);
 }
 
+// The six axis neighbours of (x, y, z) as loaded fp32 values plus the
+// central/one-sided divisor scale per axis (volume.py:244-264).
+struct Nb6 {
+    float xh, xl, yh, yl, zh, zl;
+    float sx, sy, sz;  // 0.5 (central) or 1.0 (one-sided)
+};
+
+VK_D Nb6 load_nb6(const float* __restrict__ d, int nx, int ny, int nz, int x, int y, int z) {
+    const long long sy = nx, sz = (long long)nx * ny;
+    const long long c = (long long)z * sz + (long long)y * sy + x;
+    const int xh = min(x + 1, nx - 1), xl = max(x - 1, 0);
+    const int yh = min(y + 1, ny - 1), yl = max(y - 1, 0);
+    const int zh = min(z + 1, nz - 1), zl = max(z - 1, 0);
+    Nb6 n;
+    n.xh = __ldg(d + c + (xh - x));
+    n.xl = __ldg(d + c + (xl - x));
+    n.yh = __ldg(d + c + (long long)(yh - y) * sy);
+    n.yl = __ldg(d + c + (long long)(yl - y) * sy);
+    n.zh = __ldg(d + c + (long long)(zh - z) * sz);
+    n.zl = __ldg(d + c + (long long)(zl - z) * sz);
+    n.sx = (xh - xl) == 2 ? 0.5f : 1.0f;
+    n.sy = (yh - yl) == 2 ? 0.5f : 1.0f;
+    n.sz = (zh - zl) == 2 ? 0.5f : 1.0f;
+    return n;
+}
+
+// Exact fp64 gradient from the loaded neighbours: the fp64 difference of two
+// fp32 values is exact and the scale is a power of two.
+VK_D void grad64(const Nb6& n, double& gx, double& gy, double& gz) {
+    gx = dmul(dsub((double)n.xh, (double)n.xl), (double)n.sx);
+    gy = dmul(dsub((double)n.yh, (double)n.yl), (double)n.sy);
+    gz = dmul(dsub((double)n.zh, (double)n.zl), (double)n.sz);
+}
+
+// fp32 gradient: each component within u32 relative of the exact value.
+VK_D void grad32(const Nb6& n, float& gx, float& gy, float& gz) {
+    gx = fmul(__fsub_rn(n.xh, n.xl), n.sx);
+    gy = fmul(__fsub_rn(n.yh, n.yl), n.sy);
+    gz = fmul(__fsub_rn(n.zh, n.zl), n.sz);
+}
+
+// |v| in fp32, within 4 u32 relative of the exact Euclidean norm.
+VK_D float norm3_f32(float x, float y, float z) {
+    return __fsqrt_rn(fadd(fadd(fmul(x, x), fmul(y, y)), fmul(z, z)));
+}
+
+// Relative error bound of fp32 votes against the reference's fp64 votes
+// (4 u32 for the norm, 1 u32 for the window cast, 1 u32 for the product,
+// rounded up generously), and an absolute allowance for fp32 subnormals.
+constexpr double kVoteRel = 1.0e-6;
+constexpr double kVoteAbs = 1.0e-43;
+
 // Unit roundoff of fp64 and a rigorous bound factor for recursive summation:
 // |fl(sum) - sum| <= gamma_k * sum|x| with gamma_k = k u / (1 - k u).
 constexpr double kU64 = 1.1102230246251565e-16;

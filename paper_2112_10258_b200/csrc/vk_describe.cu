@@ -53,6 +53,50 @@ VK_D int sr_vote(const float* data, int nx, int ny, int nz, int cx, int cy, int 
     return sp * 8 + orr;
 }
 
+// Fast vote: fp32 magnitude (|R^T g| = |g|, relative error <= kVoteRel against
+// the reference's fp64 |R^T g|) and octant bits decided in fp32 whenever the
+// rotated component clears its error bound; otherwise that voxel's bits are
+// recomputed with the reference's fp64 FMA chain.  Returns -1 for zero
+// gradients (their reference vote is exactly 0.0 and changes no bin).
+VK_D int sr_vote_fast(const float* data, int nx, int ny, int nz, int cx, int cy, int cz, int packed, const double* R,
+                      const float* Rf, float& mag, bool& inside) {
+    const int ox = unpack_off(packed, 0), oy = unpack_off(packed, 1), oz = unpack_off(packed, 2);
+    const int x = cx + ox, y = cy + oy, z = cz + oz;
+    inside = x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz;
+    if (!inside) return -1;
+    const Nb6 n = load_nb6(data, nx, ny, nz, x, y, z);
+    float gx, gy, gz;
+    grad32(n, gx, gy, gz);
+    if (gx == 0.f && gy == 0.f && gz == 0.f) return -1;
+    mag = norm3_f32(gx, gy, gz);
+    const float fx = (float)ox, fy = (float)oy, fz = (float)oz;
+    // rotated offset / gradient (error <= ~5 u32 of the L1 norms; bound 1e-6)
+    const float eo = 1.0e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
+    const float eg = 1.0e-6f * (fabsf(gx) + fabsf(gy) + fabsf(gz)) + 1.0e-40f;
+    float r[3], g[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        r[j] = fmaf(fz, Rf[6 + j], fmaf(fy, Rf[3 + j], fx * Rf[j]));
+        g[j] = fmaf(gz, Rf[6 + j], fmaf(gy, Rf[3 + j], gx * Rf[j]));
+    }
+    const bool zero_off = (ox | oy | oz) == 0;
+    const bool sure = (zero_off || (fabsf(r[0]) > eo && fabsf(r[1]) > eo && fabsf(r[2]) > eo)) &&
+                      fabsf(g[0]) > eg && fabsf(g[1]) > eg && fabsf(g[2]) > eg;
+    if (sure)
+        return 8 * ((r[0] > 0.f) + 2 * (r[1] > 0.f) + 4 * (r[2] > 0.f)) + (g[0] > 0.f) + 2 * (g[1] > 0.f) +
+               4 * (g[2] > 0.f);
+    double x64, y64, z64;
+    grad64(n, x64, y64, z64);
+    const double o0 = (double)ox, o1 = (double)oy, o2 = (double)oz;
+    const double r0 = dot3_blas(o0, o1, o2, R[0], R[3], R[6]);
+    const double r1 = dot3_blas(o0, o1, o2, R[1], R[4], R[7]);
+    const double r2 = dot3_blas(o0, o1, o2, R[2], R[5], R[8]);
+    const double g0 = dot3_blas(x64, y64, z64, R[0], R[3], R[6]);
+    const double g1 = dot3_blas(x64, y64, z64, R[1], R[4], R[7]);
+    const double g2 = dot3_blas(x64, y64, z64, R[2], R[5], R[8]);
+    return 8 * ((r0 > 0.0) + 2 * (r1 > 0.0) + 4 * (r2 > 0.0)) + (g0 > 0.0) + 2 * (g1 > 0.0) + 4 * (g2 > 0.0);
+}
+
 // Stable ascending ranks of 64 values: rank_b = #{j : w_j < w_b or (w_j == w_b and j < b)}.
 VK_D int stable_rank(const double* w, int n, int b) {
     const double wb = w[b];
@@ -70,6 +114,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
     __shared__ double w[kSrBins];
     __shared__ int order[kSrBins];
     __shared__ double Rs[9];
+    __shared__ float Rfs[9];
     __shared__ int n_inside, exact;
     const int tid = threadIdx.x;
     const int n = n_dev ? min(*n_dev, n_max) : n_max;
@@ -79,22 +124,29 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
         const vk_level L = levels[kp.lvl];
         const float* data = L.base + (long long)kp.vol * L.vol_stride;
         const vk_ball ball = balls[kp.ball];
-        if (tid < 9) Rs[tid] = rot[(long long)item * 9 + tid];
+        if (tid < 9) {
+            Rs[tid] = rot[(long long)item * 9 + tid];
+            Rfs[tid] = (float)Rs[tid];
+        }
         if (tid == 0) { n_inside = 0; exact = exact_only; }
         for (int b = 0; b < kSrBins; ++b) part[b * kSrThreads + tid] = 0.0;
         __syncthreads();
         double R[9];
+        float Rf[9];
 #pragma unroll
-        for (int e = 0; e < 9; ++e) R[e] = Rs[e];
+        for (int e = 0; e < 9; ++e) {
+            R[e] = Rs[e];
+            Rf[e] = Rfs[e];
+        }
         int cnt = 0;
         if (!exact_only) {
             for (int j = tid; j < ball.count; j += kSrThreads) {
-                double mag;
+                float mag;
                 bool inside;
-                const int bin = sr_vote(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz, __ldg(ball_offsets + ball.start + j), R,
-                                        mag, inside);
+                const int bin = sr_vote_fast(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz,
+                                             __ldg(ball_offsets + ball.start + j), R, Rf, mag, inside);
                 cnt += inside;
-                if (bin >= 0) part[bin * kSrThreads + tid] = dadd(part[bin * kSrThreads + tid], mag);
+                if (bin >= 0) part[bin * kSrThreads + tid] = dadd(part[bin * kSrThreads + tid], (double)mag);
             }
             if (cnt) atomicAdd(&n_inside, cnt);
             __syncthreads();
@@ -108,11 +160,14 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
             __syncthreads();
             if (tid == 0) {
                 const double per = (double)((ball.count + kSrThreads - 1) / kSrThreads) + kSrThreads;
-                const double epsrel = 2.0 * (gamma_k((double)n_inside) + gamma_k(per)) + 8.0 * kU64;
+                const double epsrel = 2.0 * (kVoteRel + gamma_k((double)n_inside) + gamma_k(per));
+                const double epsabs = kVoteAbs * n_inside;
                 for (int r = 0; r + 1 < kSrBins; ++r) {
                     const double a = w[order[r]], b = w[order[r + 1]];
                     if (a == 0.0 && b == 0.0) continue;  // exact empty-bin ties
-                    if (!(dadd(a, a * epsrel) < dsub(b, b * epsrel))) { exact = 1; break; }
+                    const double ahi = a == 0.0 ? 0.0 : dadd(a, a * epsrel + epsabs);
+                    const double blo = dsub(b, b * epsrel + epsabs);
+                    if (!(ahi < blo)) { exact = 1; break; }
                 }
             }
             __syncthreads();

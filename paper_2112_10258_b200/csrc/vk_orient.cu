@@ -41,7 +41,8 @@ VK_D int nearest_dir(const double* dirs, int K, double gx, double gy, double gz)
     return best;
 }
 
-// Vote of ball entry j, or bin -1 (outside / zero gradient).
+// Exact vote of ball entry j (reference arithmetic, brute-force argmax), or
+// bin -1 (outside / zero gradient).  Used by the reference-order path.
 VK_D int ori_vote(const float* data, int nx, int ny, int nz, int cx, int cy, int cz, int packed,
                   const double* __restrict__ win, const double* dirs, int K, double& vote, bool& inside) {
     const int ox = unpack_off(packed, 0), oy = unpack_off(packed, 1), oz = unpack_off(packed, 2);
@@ -54,6 +55,68 @@ VK_D int ori_vote(const float* data, int nx, int ny, int nz, int cx, int cy, int
     if (!(mag > 0.0)) return -1;
     vote = dmul(mag, __ldg(win + (ox * ox + oy * oy + oz * oz)));
     return nearest_dir(dirs, K, gx, gy, gz);
+}
+
+// Icosphere structure for the screened argmax: the 12 icosahedron vertices
+// (indices into the 42 lexsorted directions) and the 5 edge midpoints around
+// each.  The nearest of the 42 directions is always the nearest vertex or one
+// of its 5 midpoints (the midpoint Voronoi cells lie inside the union of the
+// two endpoint vertex cells), so a fp32 screen over the 12 vertices with a
+// generous margin, followed by exact fp64 dots over the surviving candidates,
+// reproduces np.argmax over all 42 (ties -> lowest index) exactly.
+struct IcoT {
+    int valid;
+    int vert[12];
+    int adj[12][5];
+};
+
+VK_D int nearest_dir_ico(const double* dirs, const float* vdir, const IcoT& ico, float gx, float gy, float gz,
+                         double x64, double y64, double z64) {
+    float dv[12];
+    float best = -INFINITY;
+#pragma unroll
+    for (int v = 0; v < 12; ++v) {
+        dv[v] = fmaf(gz, vdir[3 * v + 2], fmaf(gy, vdir[3 * v + 1], gx * vdir[3 * v]));
+        best = fmaxf(best, dv[v]);
+    }
+    const float thr = best - 1.0e-5f * (fabsf(gx) + fabsf(gy) + fabsf(gz));
+    double bv = -INFINITY;
+    int bi = 1 << 30;
+    auto consider = [&](int k) {
+        const double val = dot3_blas(x64, y64, z64, dirs[3 * k], dirs[3 * k + 1], dirs[3 * k + 2]);
+        if (val > bv || (val == bv && k < bi)) {
+            bv = val;
+            bi = k;
+        }
+    };
+#pragma unroll 1
+    for (int v = 0; v < 12; ++v) {
+        if (dv[v] < thr) continue;
+        consider(ico.vert[v]);
+#pragma unroll
+        for (int m = 0; m < 5; ++m) consider(ico.adj[v][m]);
+    }
+    return bi;
+}
+
+// Fast vote: fp32 magnitude x window (relative error <= kVoteRel against the
+// reference vote) into the exactly determined nearest direction.
+VK_D int ori_vote_fast(const float* data, int nx, int ny, int nz, int cx, int cy, int cz, int packed,
+                       const double* __restrict__ win, const double* dirs, const float* vdir, const IcoT& ico, int K,
+                       float& vote, bool& inside) {
+    const int ox = unpack_off(packed, 0), oy = unpack_off(packed, 1), oz = unpack_off(packed, 2);
+    const int x = cx + ox, y = cy + oy, z = cz + oz;
+    inside = x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz;
+    if (!inside) return -1;
+    const Nb6 n = load_nb6(data, nx, ny, nz, x, y, z);
+    float gx, gy, gz;
+    grad32(n, gx, gy, gz);
+    if (gx == 0.f && gy == 0.f && gz == 0.f) return -1;  // exact: mag == 0 in the reference
+    vote = fmul(norm3_f32(gx, gy, gz), (float)__ldg(win + (ox * ox + oy * oy + oz * oz)));
+    double x64, y64, z64;
+    grad64(n, x64, y64, z64);
+    if (ico.valid) return nearest_dir_ico(dirs, vdir, ico, gx, gy, gz, x64, y64, z64);
+    return nearest_dir(dirs, K, x64, y64, z64);
 }
 
 // Frames from a weight vector whose comparisons are exact (dominant_orientations).
@@ -94,20 +157,22 @@ VK_D void sort_desc(const double* w, int K, int* order) {
 
 // Are all decisions of frames_from() the same for every weight vector within
 // +-eps of w?  (adjacent-order separation + threshold margins)
-VK_D bool frames_certain(const double* w, const int* order, int K, double epsrel, double ratio) {
+VK_D bool frames_certain(const double* w, const int* order, int K, double epsrel, double epsabs, double ratio) {
+    auto lo = [&](double v) { return v == 0.0 ? 0.0 : dsub(v, v * epsrel + epsabs); };
+    auto hi = [&](double v) { return v == 0.0 ? 0.0 : dadd(v, v * epsrel + epsabs); };
     for (int r = 0; r + 1 < K; ++r) {
         const double a = w[order[r]], b = w[order[r + 1]];
         if (b == 0.0) continue;  // exact zero (no votes) ties are order-independent
-        if (!(dsub(a, a * epsrel) > dadd(b, b * epsrel))) return false;
+        if (!(lo(a) > hi(b))) return false;
     }
     const double top = w[order[0]];
     if (!(top > 0.0)) return true;
-    const double thr_lo = dmul(ratio, dsub(top, top * epsrel));
-    const double thr_hi = dmul(ratio, dadd(top, top * epsrel));
+    const double thr_lo = dmul(ratio, lo(top));
+    const double thr_hi = dmul(ratio, hi(top));
     for (int k = 0; k < K; ++k) {
         const double v = w[k];
-        const bool yes = dsub(v, v * epsrel) >= thr_hi;
-        const bool no = dadd(v, v * epsrel) < thr_lo;
+        const bool yes = lo(v) >= thr_hi;
+        const bool no = hi(v) < thr_lo;
         if (!yes && !no) return false;
     }
     return true;
@@ -119,12 +184,14 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
               const int* __restrict__ ball_offsets, const double* __restrict__ windows, const double* __restrict__ dirs_g,
               int K, const uint8_t* __restrict__ pair_ok, double ratio, int max_frames, double* __restrict__ weights,
               int* __restrict__ nframes, int* __restrict__ prim, int* __restrict__ sec, int* __restrict__ status,
-              int exact_only) {
+              int exact_only, IcoT ico) {
     extern __shared__ double dyn[];
     __shared__ OriShared sh;
+    __shared__ float vdir[36];
     double* part = dyn;  // [K][kOriThreads] private partial sums
     const int tid = threadIdx.x;
     for (int i = tid; i < 3 * K; i += kOriThreads) sh.dirs[i] = dirs_g[i];
+    if (ico.valid && tid < 36) vdir[tid] = (float)dirs_g[3 * ico.vert[tid / 3] + tid % 3];
     for (int i = tid; i < K * K; i += kOriThreads) sh.ok[i] = pair_ok[i];
     const int n_kp = n_kp_dev ? min(*n_kp_dev, n_kp_max) : n_kp_max;
     __syncthreads();
@@ -141,12 +208,13 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         int inside_cnt = 0;
         if (!exact_only) {
             for (int j = tid; j < ball.count; j += kOriThreads) {
-                double vote;
+                float vote;
                 bool inside;
-                const int bin = ori_vote(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz, __ldg(ball_offsets + ball.start + j),
-                                         win, sh.dirs, K, vote, inside);
+                const int bin = ori_vote_fast(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz,
+                                              __ldg(ball_offsets + ball.start + j), win, sh.dirs, vdir, ico, K, vote,
+                                              inside);
                 inside_cnt += inside;
-                if (bin >= 0) part[bin * kOriThreads + tid] = dadd(part[bin * kOriThreads + tid], vote);
+                if (bin >= 0) part[bin * kOriThreads + tid] = dadd(part[bin * kOriThreads + tid], (double)vote);
             }
         } else {
             for (int j = tid; j < ball.count; j += kOriThreads) {
@@ -177,8 +245,9 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
             __syncthreads();
             if (tid == 0) {
                 const double per = (double)((ball.count + kOriThreads - 1) / kOriThreads) + kOriThreads;
-                const double epsrel = 1.001 * (gamma_k((double)sh.n_inside) + gamma_k(per)) + 1e-300;
-                if (!frames_certain(sh.w, sh.order, K, epsrel, ratio)) sh.exact = 1;
+                const double epsrel = 2.0 * (kVoteRel + gamma_k((double)sh.n_inside) + gamma_k(per));
+                const double epsabs = kVoteAbs * sh.n_inside;
+                if (!frames_certain(sh.w, sh.order, K, epsrel, epsabs, ratio)) sh.exact = 1;
             }
             __syncthreads();
         }
@@ -249,12 +318,11 @@ __global__ void frames_from_weights_kernel(const double* __restrict__ weights, i
     }
 }
 
-// Ordered expansion of per-keypoint frames (single CTA block scan).
+// Ordered expansion of per-keypoint frames: a single-CTA scan writes each
+// keypoint's first frame slot, then a wide kernel scatters the frames.
 __global__ void __launch_bounds__(1024)
-expand_frames_kernel(const int* __restrict__ nframes, const int* __restrict__ prim, const int* __restrict__ sec,
-                     const int* __restrict__ n_kp_dev, int n_kp_max, int max_frames, const double* __restrict__ rot_table,
-                     int K, vk_frame* __restrict__ frames, double* __restrict__ rot, int* __restrict__ n_frames_dev,
-                     int* __restrict__ dropped_dev, int frame_cap) {
+frame_offsets_kernel(const int* __restrict__ nframes, const int* __restrict__ n_kp_dev, int n_kp_max,
+                     int* __restrict__ first, int* __restrict__ n_frames_dev, int* __restrict__ dropped_dev) {
     __shared__ int warp_sums[32];
     __shared__ int carry_s, dropped_s;
     const int n = n_kp_dev ? min(*n_kp_dev, n_kp_max) : n_kp_max;
@@ -264,40 +332,28 @@ expand_frames_kernel(const int* __restrict__ nframes, const int* __restrict__ pr
     for (int base = 0; base < n; base += 1024) {
         const int i = base + tid;
         const int nf = i < n ? nframes[i] : 0;
-        if (i < n && nf == 0) atomicAdd(&dropped_s, 1);
+        const unsigned zero_mask = __ballot_sync(0xffffffffu, i < n && nf == 0);
+        if (lane == 0 && zero_mask) atomicAdd(&dropped_s, __popc(zero_mask));
         int v = nf;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(0xffffffffu, v, o);
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
             if (lane >= o) v += t;
         }
         if (lane == 31) warp_sums[wid] = v;
         __syncthreads();
         if (wid == 0) {
-            int s = warp_sums[lane];
+            int sacc = warp_sums[lane];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                int t = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += t;
+                const int t = __shfl_up_sync(0xffffffffu, sacc, o);
+                if (lane >= o) sacc += t;
             }
-            warp_sums[lane] = s;
+            warp_sums[lane] = sacc;
         }
         __syncthreads();
-        const int carry = carry_s;
-        const int excl = carry + v - nf + (wid > 0 ? warp_sums[wid - 1] : 0);
-        for (int f = 0; f < nf; ++f) {
-            const int o = excl + f;
-            if (o >= frame_cap) break;
-            const int p = prim[i * max_frames + f], q = sec[i * max_frames + f];
-            vk_frame fr;
-            fr.kp = i;
-            fr.prim = p;
-            fr.sec = q;
-            fr.pad_ = 0;
-            frames[o] = fr;
-            const double* R = rot_table + ((long long)p * K + q) * 9;
-            for (int e = 0; e < 9; ++e) rot[(long long)o * 9 + e] = R[e];
-        }
+        const int excl = carry_s + v - nf + (wid > 0 ? warp_sums[wid - 1] : 0);
+        if (i < n) first[i] = excl;
         __syncthreads();
         if (tid == 1023) carry_s = excl + nf;
         __syncthreads();
@@ -308,6 +364,35 @@ expand_frames_kernel(const int* __restrict__ nframes, const int* __restrict__ pr
     }
 }
 
+__global__ void frame_write_kernel(const int* __restrict__ nframes, const int* __restrict__ prim,
+                                   const int* __restrict__ sec, const int* __restrict__ first,
+                                   const int* __restrict__ n_kp_dev, int n_kp_max, int max_frames,
+                                   const double* __restrict__ rot_table, int K, vk_frame* __restrict__ frames,
+                                   double* __restrict__ rot, int frame_cap) {
+    const int n = n_kp_dev ? min(*n_kp_dev, n_kp_max) : n_kp_max;
+    // one thread per (keypoint, frame slot, rotation entry)
+    const long long total = (long long)n * max_frames * 9;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int e = (int)(t % 9);
+        const long long kf = t / 9;
+        const int i = (int)(kf / max_frames), f = (int)(kf % max_frames);
+        if (f >= nframes[i]) continue;
+        const int o = first[i] + f;
+        if (o >= frame_cap) continue;
+        const int p = prim[i * max_frames + f], q = sec[i * max_frames + f];
+        rot[(long long)o * 9 + e] = rot_table[((long long)p * K + q) * 9 + e];
+        if (e == 0) {
+            vk_frame fr;
+            fr.kp = i;
+            fr.prim = p;
+            fr.sec = q;
+            fr.pad_ = 0;
+            frames[o] = fr;
+        }
+    }
+}
+
 }  // namespace vk
 
 using namespace vk;
@@ -315,7 +400,7 @@ using namespace vk;
 extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_level* levels,
                          const vk_ball* balls, const int* ball_offsets, const double* windows, const double* dirs, int K,
                          const uint8_t* pair_ok, double secondary_ratio, int max_frames, double* weights, int* nframes,
-                         int* prim, int* sec, int* status, int exact_only, void* stream) {
+                         int* prim, int* sec, int* status, int exact_only, const int* ico_host, void* stream) {
     if (!kps || n_kp_max < 0 || !levels || !balls || !ball_offsets || !windows || !dirs || K < 1 || K > VK_MAX_DIRS ||
         !pair_ok || !nframes || !prim || !sec || !status || max_frames < 1 || max_frames > VK_MAX_FRAMES ||
         !(secondary_ratio > 0.0 && secondary_ratio <= 1.0)) {
@@ -334,9 +419,17 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = n_kp_max < sms * 4 ? n_kp_max : sms * 4;
+    IcoT ico{};
+    if (ico_host && K == 42) {
+        ico.valid = 1;
+        for (int v = 0; v < 12; ++v) {
+            ico.vert[v] = ico_host[v];
+            for (int m = 0; m < 5; ++m) ico.adj[v][m] = ico_host[12 + 5 * v + m];
+        }
+    }
     orient_kernel<<<grid, kOriThreads, smem, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
                                                                   windows, dirs, K, pair_ok, secondary_ratio, max_frames,
-                                                                  weights, nframes, prim, sec, status, exact_only);
+                                                                  weights, nframes, prim, sec, status, exact_only, ico);
     count_launch();
     return cuda_status(cudaGetLastError(), "orient launch");
 }
@@ -358,14 +451,22 @@ extern "C" int vk_frames_from_weights(const double* weights, int n, int K, const
 
 extern "C" int vk_expand_frames(const int* nframes, const int* prim, const int* sec, const int* n_kp_dev, int n_kp_max,
                                 int max_frames, const double* rot_table, int K, vk_frame* frames, double* rot,
-                                int* n_frames_dev, int* dropped_dev, int frame_cap, void* stream) {
+                                int* n_frames_dev, int* dropped_dev, int frame_cap, int* scratch, void* stream) {
     if (!nframes || !prim || !sec || n_kp_max < 0 || max_frames < 1 || !rot_table || K < 1 || !frames || !rot ||
-        !n_frames_dev || !dropped_dev || frame_cap < 0) {
+        !n_frames_dev || !dropped_dev || frame_cap < 0 || (n_kp_max > 0 && !scratch)) {
         set_error("vk_expand_frames: bad arguments");
         return VK_ERR_PARAMETER;
     }
-    expand_frames_kernel<<<1, 1024, 0, as_stream(stream)>>>(nframes, prim, sec, n_kp_dev, n_kp_max, max_frames, rot_table,
-                                                            K, frames, rot, n_frames_dev, dropped_dev, frame_cap);
+    cudaStream_t st = as_stream(stream);
+    frame_offsets_kernel<<<1, 1024, 0, st>>>(nframes, n_kp_dev, n_kp_max, scratch, n_frames_dev, dropped_dev);
     count_launch();
+    if (n_kp_max > 0) {
+        const long long work = (long long)n_kp_max * max_frames * 9;
+        long long blocks = (work + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        frame_write_kernel<<<(unsigned)blocks, 256, 0, st>>>(nframes, prim, sec, scratch, n_kp_dev, n_kp_max, max_frames,
+                                                           rot_table, K, frames, rot, frame_cap);
+        count_launch();
+    }
     return cuda_status(cudaGetLastError(), "expand launch");
 }

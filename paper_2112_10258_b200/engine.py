@@ -126,6 +126,7 @@ class DeviceTables:
         self.dirs = t.from_numpy(np.ascontiguousarray(dirs).copy()).cuda()
         self.pair_ok = t.from_numpy(ok.copy()).cuda()
         self.rot_table = t.from_numpy(rot.reshape(-1).copy()).cuda()
+        self.ico = np.ascontiguousarray(T.icosphere_structure())
         balls, off, win = plan.balls.arrays()
         self.balls = _lib.to_device_records(balls)
         self.ball_offsets = t.from_numpy(off.copy()).cuda()
@@ -200,6 +201,7 @@ class Extractor:
         self.vol_offset = t.zeros(B, dtype=i32, device="cuda")
         self.total = t.zeros(2, dtype=i32, device="cuda")
         self.nframes = t.zeros(self.kp_cap, dtype=i32, device="cuda")
+        self.frame_first = t.zeros(self.kp_cap, dtype=i32, device="cuda")
         self.prim = t.zeros(self.kp_cap * self.maxf, dtype=i32, device="cuda")
         self.sec = t.zeros(self.kp_cap * self.maxf, dtype=i32, device="cuda")
         self.status = t.zeros(1, dtype=i32, device="cuda")
@@ -265,11 +267,12 @@ class Extractor:
         _lib.call("vk_orient", self.kps.data_ptr(), self.total.data_ptr(), self.kp_cap, self.level_table.data_ptr(),
                   tb.balls.data_ptr(), tb.ball_offsets.data_ptr(), tb.windows.data_ptr(), tb.dirs.data_ptr(), tb.K,
                   tb.pair_ok.data_ptr(), float(cfg.secondary_ratio), self.maxf, None, self.nframes.data_ptr(),
-                  self.prim.data_ptr(), self.sec.data_ptr(), self.status.data_ptr(), self.exact_only, s)
+                  self.prim.data_ptr(), self.sec.data_ptr(), self.status.data_ptr(), self.exact_only,
+                  tb.ico.ctypes.data, s)
         _lib.call("vk_expand_frames", self.nframes.data_ptr(), self.prim.data_ptr(), self.sec.data_ptr(),
                   self.total.data_ptr(), self.kp_cap, self.maxf, tb.rot_table.data_ptr(), tb.K,
                   self.frames.data_ptr(), self.rot.data_ptr(), self.n_frames.data_ptr(), self.dropped.data_ptr(),
-                  self.frame_cap, s)
+                  self.frame_cap, self.frame_first.data_ptr(), s)
 
     def enqueue_describe(self, s: int) -> None:
         """describe_all (descriptor.py:266-306)."""

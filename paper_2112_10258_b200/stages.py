@@ -100,10 +100,11 @@ def run_orientation(pyr, keypoints, radius_factor=4.0, secondary_ratio=0.8, max_
     prim = t.zeros(n * mf, dtype=t.int32, device="cuda")
     sec = t.zeros(n * mf, dtype=t.int32, device="cuda")
     status = t.zeros(1, dtype=t.int32, device="cuda")
+    ico = np.ascontiguousarray(T.icosphere_structure()) if directions is None else None
     _lib.call("vk_orient", d_kps.data_ptr(), None, n, view.table.data_ptr(), d_balls.data_ptr(), d_off.data_ptr(),
               d_win.data_ptr(), d_dirs.data_ptr(), K, d_ok.data_ptr(), float(secondary_ratio), mf, _lib.ptr(weights),
               nframes.data_ptr(), prim.data_ptr(), sec.data_ptr(), status.data_ptr(), int(bool(exact)),
-              _lib.stream_ptr())
+              None if ico is None else ico.ctypes.data, _lib.stream_ptr())
     if int(status.item()) & 1:
         raise DataError("orientation neighborhood lies entirely outside the volume")
     out = dict(nframes=nframes.cpu().numpy(), prim=prim.cpu().numpy().reshape(n, mf),

@@ -79,6 +79,37 @@ def icosphere_directions() -> np.ndarray:
     return allv
 
 
+@lru_cache(maxsize=1)
+def icosphere_structure() -> np.ndarray:
+    """int32[12 + 60]: indices (into icosphere_directions()) of the 12
+    icosahedron vertices, then for each vertex the 5 edge midpoints around it.
+    Enables the screened exact argmax of csrc/vk_orient.cu."""
+    dirs = icosphere_directions()
+    phi = (1.0 + math.sqrt(5.0)) / 2.0
+    pts = []
+    for a in (-1.0, 1.0):
+        for b in (-phi, phi):
+            pts += [(0.0, a, b), (a, b, 0.0), (b, 0.0, a)]
+    v = np.array(pts, dtype=np.float64)
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    vidx = [int(np.argmin(np.linalg.norm(dirs - p, axis=1))) for p in v]
+    d2 = np.sum((v[:, None, :] - v[None, :, :]) ** 2, axis=2)
+    edge = np.min(d2[d2 > 1e-9])
+    adj = []
+    for i in range(12):
+        mids = []
+        for j in range(12):
+            if j != i and abs(d2[i, j] - edge) < 1e-9:
+                m = v[i] + v[j]
+                mids.append(int(np.argmin(np.linalg.norm(dirs - m / np.linalg.norm(m), axis=1))))
+        assert len(mids) == 5
+        adj.append(sorted(mids))
+    out = np.array(vidx + [m for a in adj for m in a], dtype=np.int32)
+    assert len(set(vidx)) == 12
+    out.setflags(write=False)
+    return out
+
+
 def frame_tables(dirs: np.ndarray):
     """For every (primary p, candidate secondary q): whether q's projection
     orthogonal to p is usable (norm > 1e-6) and the resulting right-handed

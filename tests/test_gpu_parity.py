@@ -267,3 +267,31 @@ def test_edge_cases():
         vk.build_gaussian_pyramid(vk.Volume(np.zeros((8, 8, 8), np.float32)), levels_per_octave=3)
     with pytest.raises(vk.ParameterError):
         vk.nearest_neighbor_matches(np.zeros((3, 8)), np.zeros((1, 8)))
+
+
+@pytest.mark.parametrize("kind", ["siftrank", "brief"])
+def test_fast_path_adversarial(kind):
+    """Quantised / plateau volumes (exact ties, zero gradients, axis-aligned
+    gradients): the bounded fast path must equal forced reference order, and
+    both must equal the oracle."""
+    from oracle import volkey_oracle as O
+
+    rng = np.random.default_rng(11)
+    smooth = synthetic.random_blob_phantom((36, 38, 34), rng, n_blobs=14, margin=4)
+    vols = [np.round(smooth * 8.0).astype(np.float32) / 8.0,                       # plateaus + ties
+            rng.integers(0, 3, size=(30, 32, 28)).astype(np.float32),              # integer noise
+            np.where(smooth > 0.05, 1.0, 0.0).astype(np.float32) + smooth * 1e-3]  # near-binary
+    cfg = PipelineConfig(descriptor=kind, num_octaves=2)
+    for vol in vols:
+        outs = []
+        for exact in (False, True):
+            ex = vk.Extractor(vol.shape, cfg, batch=1, exact_only=exact)
+            ex.input[0].copy_(vk.volume.to_device(vol))
+            ex.enqueue()
+            outs.append(ex.results())
+        a, b = outs
+        assert np.array_equal(a["frame_prim"], b["frame_prim"]) and np.array_equal(a["frame_sec"], b["frame_sec"])
+        assert np.array_equal(a["desc"], b["desc"])
+        want = O.extract(vol, descriptor=kind, num_octaves=2)
+        assert a["n_keypoints"] == len(want["keypoints"])
+        assert np.array_equal(a["desc"].astype(np.int64), O.desc_array(want["records"], kind).astype(np.int64))

@@ -1,0 +1,61 @@
+"""CPU: host-side logic of the device path (no GPU needed)."""
+
+import math
+
+import numpy as np
+
+from paper_2112_10258_b200 import tables as T
+from paper_2112_10258_b200.config import PipelineConfig
+from paper_2112_10258_b200.engine import Plan
+
+
+def test_icosphere_screening_claim():
+    """The nearest of the 42 directions is the nearest icosahedron vertex or one
+    of its 5 edge midpoints (what csrc/vk_orient.cu's screened argmax relies on;
+    the kernel additionally keeps every vertex within a margin)."""
+    d = T.icosphere_directions()
+    st = T.icosphere_structure()
+    vert, adj = st[:12], st[12:].reshape(12, 5)
+    rng = np.random.default_rng(0)
+    g = rng.normal(size=(400000, 3))
+    # plus directions near Voronoi boundaries: midpoints of random direction pairs
+    i, j = rng.integers(0, 42, size=(2, 50000))
+    g = np.vstack([g, d[i] + d[j] + 1e-9 * rng.normal(size=(50000, 3))])
+    best = np.argmax(g @ d.T, axis=1)
+    vb = np.argmax(g @ d[vert].T, axis=1)
+    cand = np.concatenate([vert[vb][:, None], adj[vb]], axis=1)
+    assert (cand == best[:, None]).any(axis=1).all()
+
+
+def test_plan_matches_reference_schedule():
+    p = Plan.build((145, 174, 145), PipelineConfig())
+    assert p.octave_dims == [(145, 174, 145), (72, 87, 72), (36, 43, 36), (18, 21, 18), (9, 10, 9), (4, 5, 4)]
+    assert [k.radius for k in p.taps] == [5, 4, 5, 6, 8, 10]
+    assert p.kappa == 2 ** (1 / 3)
+    assert p.sigmas[0][3] == 1.6 * (2 ** (1 / 3)) ** 3
+    # detection segments: octave o, DoG levels 1..3, sigma = level_sigma_local * 2^o
+    L = 6
+    for o in range(6):
+        for i in (1, 2, 3):
+            s = o * L + i
+            oo, ii, lvl, ball = p.seg_info[s]
+            assert (oo, ii, lvl) == (o, i, o * L + i)
+            want = p.sigmas[o][i] / 2.0 ** o * math.sqrt(p.kappa) * math.sqrt(1.5) * 2.0 ** o
+            assert p.seg_sigma[s] == want
+    # octave truncation rule (scalespace.py:227-231): 20 -> 10 -> 5 -> (2 < 4)
+    assert len(Plan.build((20, 20, 20), PipelineConfig()).octave_dims) == 3
+
+
+def test_ball_table_and_windows():
+    bt = T.BallTable()
+    i0 = bt.index(4.0 * 1.6)
+    assert bt.index(4.0 * 1.6) == i0
+    balls, off, win = bt.arrays()
+    n = balls[i0]["count"]
+    offs = T.ball_offsets(int(round(4.0 * 1.6 * 1024)))
+    assert n == len(offs)
+    unpacked = np.stack([((off[:n] >> s) & 1023) - 512 for s in (20, 10, 0)], axis=1)
+    assert np.array_equal(unpacked, offs)
+    sd = 4.0 * 1.6 / 2.0
+    d2 = np.sum(offs * offs, axis=1).astype(np.float64)
+    assert np.array_equal(win[balls[i0]["window_start"] + d2.astype(int)], np.exp(-d2 / (2.0 * sd * sd)))
