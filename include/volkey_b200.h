@@ -63,13 +63,20 @@ typedef struct vk_kp {
 } vk_kp;
 
 /* Integer ball of offsets (orient.py:244-255): `count` packed offsets
- * starting at `start` in the offset table; windows[window_start + d2] is the
- * orientation window for squared offset length d2 (orient.py:298-299). */
+ * starting at `start` in the offset table (reference x-major order);
+ * windows[window_start + d2] is the orientation window for squared offset
+ * length d2 (orient.py:298-299); windows32 (where taken) is its fp32 cast.
+ * The same points in z-major order (ox fastest: coalesced gathers) start at
+ * `zstart`; plane starts (pstart, r) are kept for tools. */
 typedef struct vk_ball {
     int start;
     int count;
     int window_start;
     int max_d2;
+    int zstart;
+    int pstart;
+    int r;
+    int pad_;
 } vk_ball;
 
 /* One oriented frame: keypoint index plus the (primary, secondary) direction
@@ -147,7 +154,7 @@ int vk_order_keypoints(const unsigned long long* cand_keys, const int* cand_coun
  * keypoints (n_kp_dev: device count, read by the kernel; n_kp_max bounds it).
  * dirs: K x 3 fp64 directions; pair_ok: K x K uint8 (norm of projection > 1e-6,
  * orient.py:339-343).  Outputs: weights (n x K fp64, nullable), nframes[n],
- * prim/sec[n*max_frames].  status[0] |= 1 when a keypoint's neighbourhood lies
+ * prim/sec[n*max_frames].  status[1] counts exact-order fallbacks.  status[0] |= 1 when a keypoint's neighbourhood lies
  * outside its volume (DataError, orient.py:291-292).  ico_host (nullable, K==42
  * only): 12 icosahedron-vertex indices into dirs followed by 12x5 indices of
  * the edge midpoints around each vertex, enabling the screened argmax.
@@ -155,7 +162,7 @@ int vk_order_keypoints(const unsigned long long* cand_keys, const int* cand_coun
  * argmax for every keypoint (weights then bit-identical to the reference). */
 int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_level* levels,
               const vk_ball* balls, const int* ball_offsets, const double* windows,
-              const double* dirs, int K, const uint8_t* pair_ok,
+              const float* windows32, const double* dirs, int K, const uint8_t* pair_ok,
               double secondary_ratio, int max_frames,
               double* weights, int* nframes, int* prim, int* sec, int* status,
               int exact_only, const int* ico_host, void* stream);
@@ -175,12 +182,18 @@ int vk_expand_frames(const int* nframes, const int* prim, const int* sec, const 
                      int frame_cap, int* scratch, void* stream);
 
 /* ------------------------------------------------------------ descriptors */
-/* sift_rank_descriptor (descriptor.py:227-263): 64 stable ranks per frame
- * (uint8).  rot: 9 fp64 per frame (row-major 3x3). */
-int vk_describe_siftrank(const vk_frame* frames, const double* rot, const int* n_frames_dev,
-                         int n_frames_max, const vk_kp* kps, const vk_level* levels,
-                         const vk_ball* balls, const int* ball_offsets, uint8_t* ranks_out,
-                         int exact_only, void* stream);
+/* sift_rank_descriptor (descriptor.py:227-263): 64 stable ranks (uint8) per
+ * frame.  Work item i = one keypoint and its item_count[i] frames starting at
+ * frame item_first[i] (frames of an item share a keypoint; the pipeline uses
+ * one item per keypoint so gradients are computed once for all its frames,
+ * the stage API one item per frame).  rot: 9 fp64 per frame (row-major 3x3).
+ * max_f bounds item_count.  stats (nullable): stats[0] counts frames that fell
+ * back to the exact accumulation order.  exact_only forces that order. */
+int vk_describe_siftrank(const vk_frame* frames, const double* rot, const int* item_first,
+                         const int* item_count, const int* n_items_dev, int n_items_max, int max_f,
+                         const vk_kp* kps, const vk_level* levels, const vk_ball* balls,
+                         const int* ball_offsets, uint8_t* ranks_out,
+                         int exact_only, int* stats, void* stream);
 
 /* extract_patch + preblur_patch + brief/rrief (descriptor.py:96-111,
  * 196-224).  kind 1 = BRIEF (packed big-endian bits, ceil(n/8) bytes per

@@ -116,21 +116,24 @@ struct Nb6 {
 };
 
 VK_D Nb6 load_nb6(const float* __restrict__ d, int nx, int ny, int nz, int x, int y, int z) {
-    const long long sy = nx, sz = (long long)nx * ny;
-    const long long c = (long long)z * sz + (long long)y * sy + x;
-    const int xh = min(x + 1, nx - 1), xl = max(x - 1, 0);
-    const int yh = min(y + 1, ny - 1), yl = max(y - 1, 0);
-    const int zh = min(z + 1, nz - 1), zl = max(z - 1, 0);
+    // Unsigned 32-bit element indices (a volume holds < 2^31 voxels) so each
+    // address is one wide multiply-add; clamped neighbours collapse onto the
+    // voxel itself (one-sided differences, volume.py:259-263).
+    const unsigned plane = (unsigned)nx * (unsigned)ny;
+    const unsigned c = ((unsigned)z * (unsigned)ny + (unsigned)y) * (unsigned)nx + (unsigned)x;
+    const unsigned hx = x < nx - 1, lx = x > 0;
+    const unsigned hy = y < ny - 1 ? (unsigned)nx : 0u, ly = y > 0 ? (unsigned)nx : 0u;
+    const unsigned hz = z < nz - 1 ? plane : 0u, lz = z > 0 ? plane : 0u;
     Nb6 n;
-    n.xh = __ldg(d + c + (xh - x));
-    n.xl = __ldg(d + c + (xl - x));
-    n.yh = __ldg(d + c + (long long)(yh - y) * sy);
-    n.yl = __ldg(d + c + (long long)(yl - y) * sy);
-    n.zh = __ldg(d + c + (long long)(zh - z) * sz);
-    n.zl = __ldg(d + c + (long long)(zl - z) * sz);
-    n.sx = (xh - xl) == 2 ? 0.5f : 1.0f;
-    n.sy = (yh - yl) == 2 ? 0.5f : 1.0f;
-    n.sz = (zh - zl) == 2 ? 0.5f : 1.0f;
+    n.xh = __ldg(d + (c + hx));
+    n.xl = __ldg(d + (c - lx));
+    n.yh = __ldg(d + (c + hy));
+    n.yl = __ldg(d + (c - ly));
+    n.zh = __ldg(d + (c + hz));
+    n.zl = __ldg(d + (c - lz));
+    n.sx = (hx & lx) ? 0.5f : 1.0f;
+    n.sy = (hy && ly) ? 0.5f : 1.0f;
+    n.sz = (hz && lz) ? 0.5f : 1.0f;
     return n;
 }
 
@@ -158,6 +161,9 @@ VK_D float norm3_f32(float x, float y, float z) {
 // (4 u32 for the norm, 1 u32 for the window cast, 1 u32 for the product,
 // rounded up generously), and an absolute allowance for fp32 subnormals.
 constexpr double kVoteRel = 1.0e-6;
+// Relative error of an fp32 run / butterfly sum of <= 32 votes (depth-5
+// addition tree: gamma_5 in fp32 ~ 3e-7, rounded up).
+constexpr double kRunRel = 5.0e-7;
 constexpr double kVoteAbs = 1.0e-43;
 
 // Unit roundoff of fp64 and a rigorous bound factor for recursive summation:

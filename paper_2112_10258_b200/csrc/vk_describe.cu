@@ -17,11 +17,12 @@
 // memory, pre-blurred there with the same non-FMA separable blur as the
 // pyramid, then the point pairs are sampled (fp64 trilinear on the fp32 patch)
 // and turned into packed bits or stable ranks.
-#include "vk_common.cuh"
+#include "vk_hood.cuh"
 
 namespace vk {
 
-constexpr int kSrThreads = 128;
+constexpr int kSrThreads = 256;
+constexpr int kSrWarps = kSrThreads / 32;
 constexpr int kSrBins = 64;
 constexpr int kPatchThreads = 256;
 constexpr int kMaxSide = 31;
@@ -53,40 +54,9 @@ VK_D int sr_vote(const float* data, int nx, int ny, int nz, int cx, int cy, int 
     return sp * 8 + orr;
 }
 
-// Fast vote: fp32 magnitude (|R^T g| = |g|, relative error <= kVoteRel against
-// the reference's fp64 |R^T g|) and octant bits decided in fp32 whenever the
-// rotated component clears its error bound; otherwise that voxel's bits are
-// recomputed with the reference's fp64 FMA chain.  Returns -1 for zero
-// gradients (their reference vote is exactly 0.0 and changes no bin).
-VK_D int sr_vote_fast(const float* data, int nx, int ny, int nz, int cx, int cy, int cz, int packed, const double* R,
-                      const float* Rf, float& mag, bool& inside) {
-    const int ox = unpack_off(packed, 0), oy = unpack_off(packed, 1), oz = unpack_off(packed, 2);
-    const int x = cx + ox, y = cy + oy, z = cz + oz;
-    inside = x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz;
-    if (!inside) return -1;
-    const Nb6 n = load_nb6(data, nx, ny, nz, x, y, z);
-    float gx, gy, gz;
-    grad32(n, gx, gy, gz);
-    if (gx == 0.f && gy == 0.f && gz == 0.f) return -1;
-    mag = norm3_f32(gx, gy, gz);
-    const float fx = (float)ox, fy = (float)oy, fz = (float)oz;
-    // rotated offset / gradient (error <= ~5 u32 of the L1 norms; bound 1e-6)
-    const float eo = 1.0e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
-    const float eg = 1.0e-6f * (fabsf(gx) + fabsf(gy) + fabsf(gz)) + 1.0e-40f;
-    float r[3], g[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        r[j] = fmaf(fz, Rf[6 + j], fmaf(fy, Rf[3 + j], fx * Rf[j]));
-        g[j] = fmaf(gz, Rf[6 + j], fmaf(gy, Rf[3 + j], gx * Rf[j]));
-    }
-    const bool zero_off = (ox | oy | oz) == 0;
-    const bool sure = (zero_off || (fabsf(r[0]) > eo && fabsf(r[1]) > eo && fabsf(r[2]) > eo)) &&
-                      fabsf(g[0]) > eg && fabsf(g[1]) > eg && fabsf(g[2]) > eg;
-    if (sure)
-        return 8 * ((r[0] > 0.f) + 2 * (r[1] > 0.f) + 4 * (r[2] > 0.f)) + (g[0] > 0.f) + 2 * (g[1] > 0.f) +
-               4 * (g[2] > 0.f);
-    double x64, y64, z64;
-    grad64(n, x64, y64, z64);
+// Rare path, out of line: the reference's fp64 FMA-chain octant bits.
+__device__ __noinline__ int sr_bin_exact(int ox, int oy, int oz, double x64, double y64, double z64,
+                                         const double* R) {
     const double o0 = (double)ox, o1 = (double)oy, o2 = (double)oz;
     const double r0 = dot3_blas(o0, o1, o2, R[0], R[3], R[6]);
     const double r1 = dot3_blas(o0, o1, o2, R[1], R[4], R[7]);
@@ -97,6 +67,73 @@ VK_D int sr_vote_fast(const float* data, int nx, int ny, int nz, int cx, int cy,
     return 8 * ((r0 > 0.0) + 2 * (r1 > 0.0) + 4 * (r2 > 0.0)) + (g0 > 0.0) + 2 * (g1 > 0.0) + 4 * (g2 > 0.0);
 }
 
+// Fast SIFT-Rank bin of one voxel for one frame: octant bits decided in fp32
+// whenever each rotated component clears its error bound (<= ~5 u32 of the L1
+// norm; bound 1e-6), otherwise recomputed with the reference's fp64 FMA chain.
+VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const Nb6& n, const double* R,
+                     const float* Rf) {
+    const float fx = (float)ox, fy = (float)oy, fz = (float)oz;
+    const float eo = 1.0e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
+    const float eg = 1.0e-6f * (fabsf(gx) + fabsf(gy) + fabsf(gz)) + 1.0e-40f;
+    float r[3], g[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        r[j] = fmaf(fz, Rf[6 + j], fmaf(fy, Rf[3 + j], fx * Rf[j]));
+        g[j] = fmaf(gz, Rf[6 + j], fmaf(gy, Rf[3 + j], gx * Rf[j]));
+    }
+    const bool zero_off = (ox | oy | oz) == 0;  // rotated zero offset is exactly 0: spatial octant 0
+    const bool sure = (zero_off || (fabsf(r[0]) > eo && fabsf(r[1]) > eo && fabsf(r[2]) > eo)) &&
+                      fabsf(g[0]) > eg && fabsf(g[1]) > eg && fabsf(g[2]) > eg;
+    if (sure)
+        return 8 * ((r[0] > 0.f) + 2 * (r[1] > 0.f) + 4 * (r[2] > 0.f)) + (g[0] > 0.f) + 2 * (g[1] > 0.f) +
+               4 * (g[2] > 0.f);
+    double x64, y64, z64;
+    grad64(n, x64, y64, z64);
+    return sr_bin_exact(ox, oy, oz, x64, y64, z64, R);
+}
+
+// Fast walk of one keypoint's ball for NF frames (rotations in registers);
+// returns the number of in-volume ball voxels seen by this thread.
+template <int NF>
+VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
+                 const int* __restrict__ ball_offsets, const double* Rs, const float* Rfs, double* hist, int F) {
+    float Rf[NF][9];
+#pragma unroll
+    for (int f = 0; f < NF; ++f)
+#pragma unroll
+        for (int e = 0; e < 9; ++e) Rf[f][e] = Rfs[9 * f + e];
+    const int tid = threadIdx.x, wid = tid >> 5;
+    int cnt = 0;
+    for (int base = 0; base < ball.count; base += blockDim.x) {
+        const int j = base + tid;
+        bool has = false;
+        int ox = 0, oy = 0, oz = 0;
+        float gx = 0.f, gy = 0.f, gz = 0.f, mag = 0.f;
+        Nb6 nb{};
+        if (j < ball.count) {
+            const int p = __ldg(ball_offsets + ball.zstart + j);
+            ox = unpack_off(p, 0);
+            oy = unpack_off(p, 1);
+            oz = unpack_off(p, 2);
+            const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
+            if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
+                ++cnt;
+                nb = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
+                grad32(nb, gx, gy, gz);
+                has = !(gx == 0.f && gy == 0.f && gz == 0.f);  // zero vote: no bin changes
+                if (has) mag = norm3_f32(gx, gy, gz);
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            if (f >= F) break;
+            const int bin = has ? sr_bin_fast(ox, oy, oz, gx, gy, gz, nb, Rs + 9 * f, Rf[f]) : -1;
+            warp_accum(hist + (f * (blockDim.x >> 5) + wid) * 64, bin, mag);
+        }
+    }
+    return cnt;
+}
+
 // Stable ascending ranks of 64 values: rank_b = #{j : w_j < w_b or (w_j == w_b and j < b)}.
 VK_D int stable_rank(const double* w, int n, int b) {
     const double wb = w[b];
@@ -105,98 +142,131 @@ VK_D int stable_rank(const double* w, int n, int b) {
     return r;
 }
 
-__global__ void __launch_bounds__(kSrThreads)
-siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ rot, const int* __restrict__ n_dev,
-                int n_max, const vk_kp* __restrict__ kps, const vk_level* __restrict__ levels,
-                const vk_ball* __restrict__ balls, const int* __restrict__ ball_offsets, uint8_t* __restrict__ out,
-                int exact_only) {
-    extern __shared__ double part[];  // [64][kSrThreads]
+// One CTA per work item = one keypoint and its F frames (contiguous in the
+// frame list).  The ball is walked in z-major order (coalesced gathers);
+// each voxel's gradient is computed once and voted into all F frames.
+__global__ void __launch_bounds__(kSrThreads, 3)
+siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ rot,
+                const int* __restrict__ item_first, const int* __restrict__ item_count,
+                const int* __restrict__ n_items_dev, int n_items_max, const vk_kp* __restrict__ kps,
+                const vk_level* __restrict__ levels, const vk_ball* __restrict__ balls,
+                const int* __restrict__ ball_offsets, int max_f,
+                uint8_t* __restrict__ out, int exact_only, int* __restrict__ stats) {
+    extern __shared__ double hist[];  // [max_f][kSrWarps][64]
     __shared__ double w[kSrBins];
     __shared__ int order[kSrBins];
-    __shared__ double Rs[9];
-    __shared__ float Rfs[9];
+    __shared__ double Rs[VK_MAX_FRAMES * 9];
+    __shared__ float Rfs[VK_MAX_FRAMES * 9];
+    __shared__ int xb[kSrThreads];
+    __shared__ double xv[kSrThreads];
     __shared__ int n_inside, exact;
     const int tid = threadIdx.x;
-    const int n = n_dev ? min(*n_dev, n_max) : n_max;
+    const int n = n_items_dev ? min(*n_items_dev, n_items_max) : n_items_max;
     for (int item = blockIdx.x; item < n; item += gridDim.x) {
-        const vk_frame fr = frames[item];
-        const vk_kp kp = kps[fr.kp];
+        const int F = min(item_count[item], max_f);
+        if (F <= 0) continue;
+        const int first = item_first[item];
+        const vk_kp kp = kps[frames[first].kp];
         const vk_level L = levels[kp.lvl];
         const float* data = L.base + (long long)kp.vol * L.vol_stride;
         const vk_ball ball = balls[kp.ball];
-        if (tid < 9) {
-            Rs[tid] = rot[(long long)item * 9 + tid];
-            Rfs[tid] = (float)Rs[tid];
+        __syncthreads();  // previous item done with the shared buffers
+        for (int i = tid; i < F * 9; i += kSrThreads) {
+            Rs[i] = rot[(long long)first * 9 + i];
+            Rfs[i] = (float)Rs[i];
         }
-        if (tid == 0) { n_inside = 0; exact = exact_only; }
-        for (int b = 0; b < kSrBins; ++b) part[b * kSrThreads + tid] = 0.0;
+        for (int i = tid; i < F * kSrWarps * kSrBins; i += kSrThreads) hist[i] = 0.0;
+        if (tid == 0) n_inside = 0;
         __syncthreads();
-        double R[9];
-        float Rf[9];
-#pragma unroll
-        for (int e = 0; e < 9; ++e) {
-            R[e] = Rs[e];
-            Rf[e] = Rfs[e];
-        }
         int cnt = 0;
-        if (!exact_only) {
+        const bool fast = !exact_only;
+        if (fast) {
+            // z-major ball walk: consecutive lanes take consecutive x -> coalesced gathers
+            switch (F) {
+                case 1: cnt = sr_walk<1>(kp, L, data, ball, ball_offsets, Rs, Rfs, hist, F); break;
+                case 2: cnt = sr_walk<2>(kp, L, data, ball, ball_offsets, Rs, Rfs, hist, F); break;
+                case 3: cnt = sr_walk<3>(kp, L, data, ball, ball_offsets, Rs, Rfs, hist, F); break;
+                case 4: cnt = sr_walk<4>(kp, L, data, ball, ball_offsets, Rs, Rfs, hist, F); break;
+                default:  // > 4 frames: two passes of up to 4 frames (gradients recomputed)
+                    cnt = sr_walk<4>(kp, L, data, ball, ball_offsets, Rs, Rfs, hist, 4);
+                    sr_walk<4>(kp, L, data, ball, ball_offsets, Rs + 36, Rfs + 36, hist + 4 * kSrWarps * kSrBins, F - 4);
+                    break;
+            }
+        } else {
             for (int j = tid; j < ball.count; j += kSrThreads) {
-                float mag;
-                bool inside;
-                const int bin = sr_vote_fast(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz,
-                                             __ldg(ball_offsets + ball.start + j), R, Rf, mag, inside);
-                cnt += inside;
-                if (bin >= 0) part[bin * kSrThreads + tid] = dadd(part[bin * kSrThreads + tid], (double)mag);
+                const int p = __ldg(ball_offsets + ball.start + j);
+                const int x = kp.ix + unpack_off(p, 0), y = kp.iy + unpack_off(p, 1), z = kp.iz + unpack_off(p, 2);
+                cnt += x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz;
             }
-            if (cnt) atomicAdd(&n_inside, cnt);
-            __syncthreads();
-            if (tid < kSrBins) {
-                double s = 0.0;
-                for (int t = 0; t < kSrThreads; ++t) s = dadd(s, part[tid * kSrThreads + t]);
-                w[tid] = s;
-            }
-            __syncthreads();
-            if (tid < kSrBins) order[stable_rank(w, kSrBins, tid)] = tid;
-            __syncthreads();
-            if (tid == 0) {
-                const double per = (double)((ball.count + kSrThreads - 1) / kSrThreads) + kSrThreads;
-                const double epsrel = 2.0 * (kVoteRel + gamma_k((double)n_inside) + gamma_k(per));
-                const double epsabs = kVoteAbs * n_inside;
-                for (int r = 0; r + 1 < kSrBins; ++r) {
-                    const double a = w[order[r]], b = w[order[r + 1]];
-                    if (a == 0.0 && b == 0.0) continue;  // exact empty-bin ties
-                    const double ahi = a == 0.0 ? 0.0 : dadd(a, a * epsrel + epsabs);
-                    const double blo = dsub(b, b * epsrel + epsabs);
-                    if (!(ahi < blo)) { exact = 1; break; }
-                }
-            }
-            __syncthreads();
         }
-        if (exact) {
-            if (tid < 32) {
+        if (cnt) atomicAdd(&n_inside, cnt);
+        __syncthreads();
+        for (int f = 0; f < F; ++f) {
+            if (tid == 0) exact = fast ? 0 : 1;
+            if (fast && tid < kSrBins) {
+                double sacc = 0.0;
+                for (int wi = 0; wi < kSrWarps; ++wi) sacc = dadd(sacc, hist[(f * kSrWarps + wi) * kSrBins + tid]);
+                w[tid] = sacc;
+            }
+            __syncthreads();
+            if (fast) {
+                if (tid < kSrBins) order[stable_rank(w, kSrBins, tid)] = tid;
+                __syncthreads();
+                if (tid == 0) {
+                    const double epsrel = 2.0 * (kVoteRel + kRunRel + gamma_k((double)n_inside + 64.0));
+                    const double epsabs = kVoteAbs * n_inside;
+                    for (int q = 0; q + 1 < kSrBins; ++q) {
+                        const double a = w[order[q]], b = w[order[q + 1]];
+                        if (a == 0.0 && b == 0.0) continue;  // exact empty-bin ties
+                        const double ahi = a == 0.0 ? 0.0 : dadd(a, a * epsrel + epsabs);
+                        const double blo = dsub(b, b * epsrel + epsabs);
+                        if (!(ahi < blo)) {
+                            exact = 1;
+                            if (stats) atomicAdd(stats, 1);  // fallback counter (diagnostics)
+                            break;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            if (exact) {
+                // Exact reference order: chunked exact votes, warp 0 adds in ball order.
+                double R[9];
+#pragma unroll
+                for (int e = 0; e < 9; ++e) R[e] = Rs[9 * f + e];
                 double acc0 = 0.0, acc1 = 0.0;
-                for (int base = 0; base < ball.count; base += 32) {
+                for (int base = 0; base < ball.count; base += kSrThreads) {
                     const int j = base + tid;
-                    double mag = 0.0;
+                    double mg = 0.0;
                     bool inside;
                     int bin = -1;
                     if (j < ball.count)
                         bin = sr_vote(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz, __ldg(ball_offsets + ball.start + j), R,
-                                      mag, inside);
-                    for (int s = 0; s < 32; ++s) {
-                        const int bs = __shfl_sync(0xffffffffu, bin, s);
-                        const double vs = __shfl_sync(0xffffffffu, mag, s);
-                        if (bs == tid) acc0 = dadd(acc0, vs);
-                        else if (bs == tid + 32) acc1 = dadd(acc1, vs);
+                                      mg, inside);
+                    xb[tid] = bin;
+                    xv[tid] = mg;
+                    __syncthreads();
+                    if (tid < 32) {
+                        const int m = min(kSrThreads, ball.count - base);
+#pragma unroll 8
+                        for (int q = 0; q < m; ++q) {
+                            const int bs = xb[q];
+                            const double vs = xv[q];
+                            if (bs == tid) acc0 = dadd(acc0, vs);
+                            else if (bs == tid + 32) acc1 = dadd(acc1, vs);
+                        }
                     }
+                    __syncthreads();
                 }
-                w[tid] = acc0;
-                w[tid + 32] = acc1;
+                if (tid < 32) {
+                    w[tid] = acc0;
+                    w[tid + 32] = acc1;
+                }
+                __syncthreads();
             }
+            if (tid < kSrBins) out[(long long)(first + f) * kSrBins + tid] = (uint8_t)stable_rank(w, kSrBins, tid);
             __syncthreads();
         }
-        if (tid < kSrBins) out[(long long)item * kSrBins + tid] = (uint8_t)stable_rank(w, kSrBins, tid);
-        __syncthreads();
     }
 }
 
@@ -300,23 +370,28 @@ static int grid_for(int n, int per_sm) {
     return n < sms * per_sm ? n : sms * per_sm;
 }
 
-extern "C" int vk_describe_siftrank(const vk_frame* frames, const double* rot, const int* n_frames_dev, int n_frames_max,
+extern "C" int vk_describe_siftrank(const vk_frame* frames, const double* rot, const int* item_first,
+                                    const int* item_count, const int* n_items_dev, int n_items_max, int max_f,
                                     const vk_kp* kps, const vk_level* levels, const vk_ball* balls,
-                                    const int* ball_offsets, uint8_t* ranks_out, int exact_only, void* stream) {
-    if (!frames || !rot || n_frames_max < 0 || !kps || !levels || !balls || !ball_offsets || !ranks_out) {
+                                    const int* ball_offsets, uint8_t* ranks_out,
+                                    int exact_only, int* stats, void* stream) {
+    if (!frames || !rot || !item_first || !item_count || n_items_max < 0 || max_f < 1 || max_f > VK_MAX_FRAMES ||
+        !kps || !levels || !balls || !ball_offsets || !ranks_out) {
         set_error("vk_describe_siftrank: bad arguments");
         return VK_ERR_PARAMETER;
     }
-    if (n_frames_max == 0) return VK_OK;
-    const int smem = kSrBins * kSrThreads * 8;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(siftrank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (n_items_max == 0) return VK_OK;
+    const int smem = max_f * kSrWarps * kSrBins * 8;
+    static int configured = 0;
+    if (smem > 48 * 1024 && configured < smem) {
+        cudaError_t e = cudaFuncSetAttribute(siftrank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             VK_MAX_FRAMES * kSrWarps * kSrBins * 8);
         if (e != cudaSuccess) return cuda_status(e, "siftrank attribute");
-        configured = true;
+        configured = VK_MAX_FRAMES * kSrWarps * kSrBins * 8;
     }
-    siftrank_kernel<<<grid_for(n_frames_max, 3), kSrThreads, smem, as_stream(stream)>>>(
-        frames, rot, n_frames_dev, n_frames_max, kps, levels, balls, ball_offsets, ranks_out, exact_only);
+    siftrank_kernel<<<grid_for(n_items_max, 4), kSrThreads, smem, as_stream(stream)>>>(
+        frames, rot, item_first, item_count, n_items_dev, n_items_max, kps, levels, balls, ball_offsets, max_f,
+        ranks_out, exact_only, stats);
     count_launch();
     return cuda_status(cudaGetLastError(), "siftrank launch");
 }

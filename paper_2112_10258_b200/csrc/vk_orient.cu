@@ -15,13 +15,16 @@
 // decision is not certain, the CTA recomputes the histogram in the exact
 // reference order (one warp, votes broadcast lane by lane).  Either way the
 // frames are identical to the reference's.
-#include "vk_common.cuh"
+#include "vk_hood.cuh"
 
 namespace vk {
 
-constexpr int kOriThreads = 128;
+constexpr int kOriThreads = 256;
+constexpr int kOriWarps = kOriThreads / 32;
 
 struct OriShared {
+    double xv[kOriThreads];
+    int xb[kOriThreads];
     double dirs[VK_MAX_DIRS * 3];
     double w[VK_MAX_DIRS];
     int order[VK_MAX_DIRS];
@@ -57,65 +60,113 @@ VK_D int ori_vote(const float* data, int nx, int ny, int nz, int cx, int cy, int
     return nearest_dir(dirs, K, gx, gy, gz);
 }
 
-// Icosphere structure for the screened argmax: the 12 icosahedron vertices
-// (indices into the 42 lexsorted directions) and the 5 edge midpoints around
-// each.  The nearest of the 42 directions is always the nearest vertex or one
-// of its 5 midpoints (the midpoint Voronoi cells lie inside the union of the
-// two endpoint vertex cells), so a fp32 screen over the 12 vertices with a
-// generous margin, followed by exact fp64 dots over the surviving candidates,
-// reproduces np.argmax over all 42 (ties -> lowest index) exactly.
+// Icosphere structure for the screened argmax.  The 12 icosahedron vertices
+// are (0, +-1, +-phi), (+-1, +-phi, 0), (+-phi, 0, +-1) (normalised); for a
+// gradient g the best vertex of each of the three groups follows from the
+// signs of g and its dot is |gy| + phi|gz|, |gx| + phi|gy|, phi|gx| + |gz| (up
+// to the common norm).  The nearest of all 42 directions is always the
+// nearest vertex or one of its 5 edge midpoints (a midpoint's Voronoi cell lies
+// in the union of its two endpoints' vertex cells; tests/test_host_logic.py),
+// so: screen vertices analytically with a generous margin, score the
+// surviving vertices + their midpoints with fp32 dots, and fall back to the
+// reference's fp64 FMA-chain dots only when the fp32 winner is not separated
+// by more than its error bound.  Ties keep the lowest index (np.argmax).
 struct IcoT {
     int valid;
-    int vert[12];
+    int vert[12];  // vertex of construction order 6*a + 3*b + group (tables.icosphere_structure)
     int adj[12][5];
 };
 
-VK_D int nearest_dir_ico(const double* dirs, const float* vdir, const IcoT& ico, float gx, float gy, float gz,
-                         double x64, double y64, double z64) {
-    float dv[12];
-    float best = -INFINITY;
-#pragma unroll
-    for (int v = 0; v < 12; ++v) {
-        dv[v] = fmaf(gz, vdir[3 * v + 2], fmaf(gy, vdir[3 * v + 1], gx * vdir[3 * v]));
-        best = fmaxf(best, dv[v]);
-    }
-    const float thr = best - 1.0e-5f * (fabsf(gx) + fabsf(gy) + fabsf(gz));
+struct IcoSh {
+    float4 cd[12 * 6];  // per vertex slot: the vertex and its 5 midpoints (fp32 xyz)
+    int ci[12 * 6];     // their direction indices
+};
+
+// Rare path (kept out of line so its fp64 work is never hoisted): exact
+// reference dots over the candidates whose fp32 score is within the window.
+__device__ __noinline__ int nearest_dir_ico_exact(const double* dirs, const IcoSh& ic, unsigned slots, float gx,
+                                                  float gy, float gz, float floor32, double x64, double y64,
+                                                  double z64) {
     double bv = -INFINITY;
     int bi = 1 << 30;
-    auto consider = [&](int k) {
-        const double val = dot3_blas(x64, y64, z64, dirs[3 * k], dirs[3 * k + 1], dirs[3 * k + 2]);
-        if (val > bv || (val == bv && k < bi)) {
-            bv = val;
-            bi = k;
+    for (unsigned t = slots; t; t &= t - 1) {
+        const int v = __ffs(t) - 1;
+        for (int c = 0; c < 6; ++c) {
+            const float4 dd = ic.cd[6 * v + c];
+            const int k = ic.ci[6 * v + c];
+            if (fmaf(gz, dd.z, fmaf(gy, dd.y, gx * dd.x)) < floor32) continue;
+            const double val = dot3_blas(x64, y64, z64, dirs[3 * k], dirs[3 * k + 1], dirs[3 * k + 2]);
+            if (val > bv || (val == bv && k < bi)) {
+                bv = val;
+                bi = k;
+            }
         }
-    };
-#pragma unroll 1
-    for (int v = 0; v < 12; ++v) {
-        if (dv[v] < thr) continue;
-        consider(ico.vert[v]);
-#pragma unroll
-        for (int m = 0; m < 5; ++m) consider(ico.adj[v][m]);
     }
     return bi;
 }
 
-// Fast vote: fp32 magnitude x window (relative error <= kVoteRel against the
-// reference vote) into the exactly determined nearest direction.
-VK_D int ori_vote_fast(const float* data, int nx, int ny, int nz, int cx, int cy, int cz, int packed,
-                       const double* __restrict__ win, const double* dirs, const float* vdir, const IcoT& ico, int K,
-                       float& vote, bool& inside) {
-    const int ox = unpack_off(packed, 0), oy = unpack_off(packed, 1), oz = unpack_off(packed, 2);
-    const int x = cx + ox, y = cy + oy, z = cz + oz;
-    inside = x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz;
-    if (!inside) return -1;
-    const Nb6 n = load_nb6(data, nx, ny, nz, x, y, z);
+VK_D int nearest_dir_ico(const double* dirs, const IcoSh& ic, float gx, float gy, float gz, const Nb6& nb) {
+    constexpr float PHI = 1.6180339887498949f;
+    const float ax = fabsf(gx), ay = fabsf(gy), az = fabsf(gz);
+    const float l1 = ax + ay + az;
+    const float vA = fmaf(PHI, az, ay), vB = fmaf(PHI, ay, ax), vC = fmaf(PHI, ax, az);
+    const float best = fmaxf(vA, fmaxf(vB, vC));
+    const float m = 1.0e-5f * 2.7f * l1;
+    // candidate vertex slots: construction index 6*a + 3*b + group, a/b = 1 for the + sign
+    unsigned slots = 0;
+    auto add_group = [&](float v, int grp, float ca, float cb, float wa, float wb) {
+        // ca / cb: the g components paired with the +-1 and +-phi coordinates, wa / wb their weights
+        if (v < best - m) return;
+        const int sa = ca > 0.f, sb = cb > 0.f;
+        const bool fa = 2.f * wa * fabsf(ca) <= m, fb = 2.f * wb * fabsf(cb) <= m;
+        slots |= 1u << (6 * sa + 3 * sb + grp);
+        if (fa) slots |= 1u << (6 * (1 - sa) + 3 * sb + grp);
+        if (fb) slots |= 1u << (6 * sa + 3 * (1 - sb) + grp);
+        if (fa && fb) slots |= 1u << (6 * (1 - sa) + 3 * (1 - sb) + grp);
+    };
+    add_group(vA, 0, gy, gz, 1.f, PHI);  // (0, a, b)
+    add_group(vB, 1, gx, gy, 1.f, PHI);  // (a, b, 0)
+    add_group(vC, 2, gz, gx, 1.f, PHI);  // (b, 0, a)
+    float b1 = -INFINITY, b2 = -INFINITY;
+    int i1 = 1 << 30;
+    for (unsigned t = slots; t; t &= t - 1) {
+        const int v = __ffs(t) - 1;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+            const float4 dd = ic.cd[6 * v + c];
+            const int k = ic.ci[6 * v + c];
+            const float d = fmaf(gz, dd.z, fmaf(gy, dd.y, gx * dd.x));
+            if (k != i1) {
+                if (d > b1 || (d == b1 && k < i1)) {
+                    b2 = fmaxf(b2, b1);
+                    b1 = d;
+                    i1 = k;
+                } else {
+                    b2 = fmaxf(b2, d);
+                }
+            }
+        }
+    }
+    const float sep = 2.0e-6f * l1;
+    if (b1 - b2 > sep) return i1;
+    // near tie: exact fp64 dots over every candidate within the separation window
+    double x64, y64, z64;
+    grad64(nb, x64, y64, z64);
+    return nearest_dir_ico_exact(dirs, ic, slots, gx, gy, gz, b1 - sep, x64, y64, z64);
+}
+
+// Fast vote of one ball voxel: fp32 magnitude x fp32 window (relative error
+// <= kVoteRel against the reference vote) into the exactly determined nearest
+// direction.  Returns -1 for zero gradients (mag == 0 exactly in the reference).
+VK_D int ori_vote_fast(const Nb6& n, const float* __restrict__ win32, int d2, const double* dirs, const IcoSh* ic,
+                       int K, float& vote) {
     float gx, gy, gz;
     grad32(n, gx, gy, gz);
-    if (gx == 0.f && gy == 0.f && gz == 0.f) return -1;  // exact: mag == 0 in the reference
-    vote = fmul(norm3_f32(gx, gy, gz), (float)__ldg(win + (ox * ox + oy * oy + oz * oz)));
+    if (gx == 0.f && gy == 0.f && gz == 0.f) return -1;
+    vote = fmul(norm3_f32(gx, gy, gz), __ldg(win32 + d2));
+    if (ic) return nearest_dir_ico(dirs, *ic, gx, gy, gz, n);
     double x64, y64, z64;
     grad64(n, x64, y64, z64);
-    if (ico.valid) return nearest_dir_ico(dirs, vdir, ico, gx, gy, gz, x64, y64, z64);
     return nearest_dir(dirs, K, x64, y64, z64);
 }
 
@@ -157,10 +208,16 @@ VK_D void sort_desc(const double* w, int K, int* order) {
 
 // Are all decisions of frames_from() the same for every weight vector within
 // +-eps of w?  (adjacent-order separation + threshold margins)
-VK_D bool frames_certain(const double* w, const int* order, int K, double epsrel, double epsabs, double ratio) {
+// Only the top of the order matters: primaries are the first max_frames bins
+// above the threshold and each secondary is the first usable bin of the
+// order, so positions 0..m (m = max_frames + 2) and the gap below them decide
+// every frame.
+VK_D bool frames_certain(const double* w, const int* order, int K, double epsrel, double epsabs, double ratio,
+                         int max_frames) {
     auto lo = [&](double v) { return v == 0.0 ? 0.0 : dsub(v, v * epsrel + epsabs); };
     auto hi = [&](double v) { return v == 0.0 ? 0.0 : dadd(v, v * epsrel + epsabs); };
-    for (int r = 0; r + 1 < K; ++r) {
+    const int m = min(K - 1, max_frames + 2);
+    for (int r = 0; r < m; ++r) {
         const double a = w[order[r]], b = w[order[r + 1]];
         if (b == 0.0) continue;  // exact zero (no votes) ties are order-independent
         if (!(lo(a) > hi(b))) return false;
@@ -169,8 +226,8 @@ VK_D bool frames_certain(const double* w, const int* order, int K, double epsrel
     if (!(top > 0.0)) return true;
     const double thr_lo = dmul(ratio, lo(top));
     const double thr_hi = dmul(ratio, hi(top));
-    for (int k = 0; k < K; ++k) {
-        const double v = w[k];
+    for (int r = 0; r <= m; ++r) {
+        const double v = w[order[r]];
         const bool yes = lo(v) >= thr_hi;
         const bool no = hi(v) < thr_lo;
         if (!yes && !no) return false;
@@ -178,22 +235,28 @@ VK_D bool frames_certain(const double* w, const int* order, int K, double epsrel
     return true;
 }
 
-__global__ void __launch_bounds__(kOriThreads)
+__global__ void __launch_bounds__(kOriThreads, 4)
 orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, int n_kp_max,
               const vk_level* __restrict__ levels, const vk_ball* __restrict__ balls,
-              const int* __restrict__ ball_offsets, const double* __restrict__ windows, const double* __restrict__ dirs_g,
-              int K, const uint8_t* __restrict__ pair_ok, double ratio, int max_frames, double* __restrict__ weights,
+              const int* __restrict__ ball_offsets, const double* __restrict__ windows,
+              const float* __restrict__ windows32, const double* __restrict__ dirs_g, int K,
+              const uint8_t* __restrict__ pair_ok, double ratio, int max_frames, double* __restrict__ weights,
               int* __restrict__ nframes, int* __restrict__ prim, int* __restrict__ sec, int* __restrict__ status,
               int exact_only, IcoT ico) {
-    extern __shared__ double dyn[];
     __shared__ OriShared sh;
-    __shared__ float vdir[36];
-    double* part = dyn;  // [K][kOriThreads] private partial sums
+    __shared__ IcoSh ic;
+    __shared__ double hist[kOriWarps * VK_MAX_DIRS];
     const int tid = threadIdx.x;
     for (int i = tid; i < 3 * K; i += kOriThreads) sh.dirs[i] = dirs_g[i];
-    if (ico.valid && tid < 36) vdir[tid] = (float)dirs_g[3 * ico.vert[tid / 3] + tid % 3];
+    if (ico.valid && tid < 72) {
+        const int v = tid / 6, c = tid % 6;
+        const int k = c == 0 ? ico.vert[v] : ico.adj[v][c - 1];
+        ic.ci[tid] = k;
+        ic.cd[tid] = make_float4((float)dirs_g[3 * k], (float)dirs_g[3 * k + 1], (float)dirs_g[3 * k + 2], 0.f);
+    }
     for (int i = tid; i < K * K; i += kOriThreads) sh.ok[i] = pair_ok[i];
     const int n_kp = n_kp_dev ? min(*n_kp_dev, n_kp_max) : n_kp_max;
+    const IcoSh* icp = ico.valid ? &ic : nullptr;
     __syncthreads();
 
     for (int item = blockIdx.x; item < n_kp; item += gridDim.x) {
@@ -202,19 +265,29 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         const float* data = L.base + (long long)kp.vol * L.vol_stride;
         const vk_ball ball = balls[kp.ball];
         const double* win = windows + ball.window_start;
-        for (int b = 0; b < K; ++b) part[b * kOriThreads + tid] = 0.0;
+        const float* win32 = windows32 + ball.window_start;
+        for (int i = tid; i < kOriWarps * K; i += kOriThreads) hist[i] = 0.0;
         if (tid == 0) { sh.n_inside = 0; sh.exact = exact_only; }
         __syncthreads();
         int inside_cnt = 0;
         if (!exact_only) {
-            for (int j = tid; j < ball.count; j += kOriThreads) {
-                float vote;
-                bool inside;
-                const int bin = ori_vote_fast(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz,
-                                              __ldg(ball_offsets + ball.start + j), win, sh.dirs, vdir, ico, K, vote,
-                                              inside);
-                inside_cnt += inside;
-                if (bin >= 0) part[bin * kOriThreads + tid] = dadd(part[bin * kOriThreads + tid], (double)vote);
+            // z-major ball walk: consecutive lanes take consecutive x -> coalesced gathers
+            double* wh = hist + (tid >> 5) * K;
+            for (int base = 0; base < ball.count; base += kOriThreads) {
+                const int j = base + tid;
+                int bin = -1;
+                float vote = 0.f;
+                if (j < ball.count) {
+                    const int p = __ldg(ball_offsets + ball.zstart + j);
+                    const int ox = unpack_off(p, 0), oy = unpack_off(p, 1), oz = unpack_off(p, 2);
+                    const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
+                    if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
+                        ++inside_cnt;
+                        bin = ori_vote_fast(load_nb6(data, L.nx, L.ny, L.nz, x, y, z), win32,
+                                            ox * ox + oy * oy + oz * oz, sh.dirs, icp, K, vote);
+                    }
+                }
+                warp_accum(wh, bin, vote);
             }
         } else {
             for (int j = tid; j < ball.count; j += kOriThreads) {
@@ -234,42 +307,54 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
             __syncthreads();
             continue;
         }
-        if (!exact_only) {
+        if (!sh.exact) {
             for (int b = tid; b < K; b += kOriThreads) {
-                double s = 0.0;
-                for (int t = 0; t < kOriThreads; ++t) s = dadd(s, part[b * kOriThreads + t]);
-                sh.w[b] = s;
+                double sacc = 0.0;
+                for (int w = 0; w < kOriWarps; ++w) sacc = dadd(sacc, hist[w * K + b]);
+                sh.w[b] = sacc;
             }
             __syncthreads();
             sort_desc(sh.w, K, sh.order);
             __syncthreads();
             if (tid == 0) {
-                const double per = (double)((ball.count + kOriThreads - 1) / kOriThreads) + kOriThreads;
-                const double epsrel = 2.0 * (kVoteRel + gamma_k((double)sh.n_inside) + gamma_k(per));
+                // each vote passes through <= n_inside run/scan/merge additions
+                const double epsrel = 2.0 * (kVoteRel + kRunRel + gamma_k((double)sh.n_inside + 64.0));
                 const double epsabs = kVoteAbs * sh.n_inside;
-                if (!frames_certain(sh.w, sh.order, K, epsrel, epsabs, ratio)) sh.exact = 1;
+                if (!frames_certain(sh.w, sh.order, K, epsrel, epsabs, ratio, max_frames)) {
+                    sh.exact = 1;
+                    atomicAdd(status + 1, 1);  // fallback counter (diagnostics)
+                }
             }
             __syncthreads();
         }
         if (sh.exact) {
-            // Exact reference order: votes in ball order, each bin summed sequentially.
-            if (tid < 32) {
-                double acc0 = 0.0, acc1 = 0.0;
-                for (int base = 0; base < ball.count; base += 32) {
-                    const int j = base + tid;
-                    double vote = 0.0;
-                    bool inside;
-                    int bin = -1;
-                    if (j < ball.count)
-                        bin = ori_vote(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz, __ldg(ball_offsets + ball.start + j),
-                                       win, sh.dirs, K, vote, inside);
-                    for (int s = 0; s < 32; ++s) {
-                        const int bs = __shfl_sync(0xffffffffu, bin, s);
-                        const double vs = __shfl_sync(0xffffffffu, vote, s);
+            // Exact reference order: all threads compute a chunk of exact votes,
+            // then warp 0 adds them bin by bin in ball order (np.add.at).
+            double acc0 = 0.0, acc1 = 0.0;
+            for (int base = 0; base < ball.count; base += kOriThreads) {
+                const int j = base + tid;
+                double vote = 0.0;
+                bool inside;
+                int bin = -1;
+                if (j < ball.count)
+                    bin = ori_vote(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz, __ldg(ball_offsets + ball.start + j), win,
+                                   sh.dirs, K, vote, inside);
+                sh.xb[tid] = bin;
+                sh.xv[tid] = vote;
+                __syncthreads();
+                if (tid < 32) {
+                    const int m = min(kOriThreads, ball.count - base);
+#pragma unroll 8
+                    for (int q = 0; q < m; ++q) {
+                        const int bs = sh.xb[q];
+                        const double vs = sh.xv[q];
                         if (bs == tid) acc0 = dadd(acc0, vs);
                         else if (bs == tid + 32) acc1 = dadd(acc1, vs);
                     }
                 }
+                __syncthreads();
+            }
+            if (tid < 32) {
                 if (tid < K) sh.w[tid] = acc0;
                 if (tid + 32 < K) sh.w[tid + 32] = acc1;
             }
@@ -398,23 +483,17 @@ __global__ void frame_write_kernel(const int* __restrict__ nframes, const int* _
 using namespace vk;
 
 extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_level* levels,
-                         const vk_ball* balls, const int* ball_offsets, const double* windows, const double* dirs, int K,
-                         const uint8_t* pair_ok, double secondary_ratio, int max_frames, double* weights, int* nframes,
-                         int* prim, int* sec, int* status, int exact_only, const int* ico_host, void* stream) {
-    if (!kps || n_kp_max < 0 || !levels || !balls || !ball_offsets || !windows || !dirs || K < 1 || K > VK_MAX_DIRS ||
-        !pair_ok || !nframes || !prim || !sec || !status || max_frames < 1 || max_frames > VK_MAX_FRAMES ||
-        !(secondary_ratio > 0.0 && secondary_ratio <= 1.0)) {
+                         const vk_ball* balls, const int* ball_offsets, const double* windows, const float* windows32,
+                         const double* dirs, int K, const uint8_t* pair_ok, double secondary_ratio, int max_frames,
+                         double* weights, int* nframes, int* prim, int* sec, int* status, int exact_only,
+                         const int* ico_host, void* stream) {
+    if (!kps || n_kp_max < 0 || !levels || !balls || !ball_offsets || !windows || !windows32 || !dirs || K < 1 ||
+        K > VK_MAX_DIRS || !pair_ok || !nframes || !prim || !sec || !status || max_frames < 1 ||
+        max_frames > VK_MAX_FRAMES || !(secondary_ratio > 0.0 && secondary_ratio <= 1.0)) {
         set_error("vk_orient: bad arguments (K=%d max_frames=%d)", K, max_frames);
         return VK_ERR_PARAMETER;
     }
     if (n_kp_max == 0) return VK_OK;
-    const int smem = K * kOriThreads * (int)sizeof(double);
-    static int configured = 0;
-    if (configured < smem) {
-        cudaError_t e = cudaFuncSetAttribute(orient_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, VK_MAX_DIRS * kOriThreads * 8);
-        if (e != cudaSuccess) return cuda_status(e, "orient attribute");
-        configured = VK_MAX_DIRS * kOriThreads * 8;
-    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -427,9 +506,10 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
             for (int m = 0; m < 5; ++m) ico.adj[v][m] = ico_host[12 + 5 * v + m];
         }
     }
-    orient_kernel<<<grid, kOriThreads, smem, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
-                                                                  windows, dirs, K, pair_ok, secondary_ratio, max_frames,
-                                                                  weights, nframes, prim, sec, status, exact_only, ico);
+    orient_kernel<<<grid, kOriThreads, 0, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
+                                                               windows, windows32, dirs, K, pair_ok, secondary_ratio,
+                                                               max_frames, weights, nframes, prim, sec, status,
+                                                               exact_only, ico);
     count_launch();
     return cuda_status(cudaGetLastError(), "orient launch");
 }

@@ -42,6 +42,11 @@ struct BlurGeom {
     static constexpr int SMEM = (2 * ROWS * XPW + ROWS * XS) * 4;
 };
 
+// Products of two taps at once: packed FMUL2 (two IEEE-rounded products); the
+// sums stay scalar FADDs in tap order.  ptxas never contracts FMUL2 + FADD
+// (it does contract FMUL2 + FADD2 into FFMA2, which would break parity).
+VK_D float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+
 template <int R>
 __global__ void __launch_bounds__(kThreads, 2)
 blur3d_ring_kernel(const float* __restrict__ src, float* __restrict__ dst, float* __restrict__ dog,
@@ -62,13 +67,22 @@ blur3d_ring_kernel(const float* __restrict__ src, float* __restrict__ dst, float
     const float* s = src + b * vol;
     const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
 
+    // Loop-invariant clamped x offsets of this lane's (up to 2) tile columns.
+    constexpr int NCOL = (G::COLS + 31) / 32;
+    int gxo[NCOL];
+#pragma unroll
+    for (int k = 0; k < NCOL; ++k) gxo[k] = clampi(x0 - R + lane + 32 * k, 0, nx - 1);
+
     auto load_plane = [&](int zp, int buf) {
         const float* sp = s + (long long)clampi(zp, 0, nz - 1) * plane;
         float* d = in_s + buf * G::ROWS * G::XPW;
-        for (int i = tid; i < G::ROWS * G::COLS; i += kThreads) {
-            int r = i / G::COLS, c = i - r * G::COLS;
-            int gy = clampi(y0 - R + r, 0, ny - 1), gx = clampi(x0 - R + c, 0, nx - 1);
-            cp_async4(d + r * G::XPW + c, sp + (long long)gy * nx + gx);
+#pragma unroll
+        for (int r = wy; r < G::ROWS; r += kThreads / 32) {
+            const unsigned roff = (unsigned)clampi(y0 - R + r, 0, ny - 1) * (unsigned)nx;
+            float* drow = d + r * G::XPW + lane;
+#pragma unroll
+            for (int k = 0; k < NCOL; ++k)
+                if (lane + 32 * k < G::COLS) cp_async4(drow + 32 * k, sp + (roff + (unsigned)gxo[k]));
         }
         cp_async_commit();
     };
@@ -90,7 +104,7 @@ blur3d_ring_kernel(const float* __restrict__ src, float* __restrict__ dst, float
         else cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
-        // ---- x-pass: 4 threads per tile row, 8 outputs each ----
+        // ---- x-pass: 4 threads per tile row, 8 outputs each (pairs of outputs share FMUL2) ----
         {
             const int r = tid >> 2, sg = tid & 3;
             if (r < G::ROWS) {
@@ -103,11 +117,17 @@ blur3d_ring_kernel(const float* __restrict__ src, float* __restrict__ dst, float
                 }
                 float o[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    float acc = fmul(taps.w[0], v[k]);
+                for (int k = 0; k < 8; k += 2) {
+                    float2 pr = fmul2(make_float2(taps.w[0], taps.w[0]), make_float2(v[k], v[k + 1]));
+                    float a0 = pr.x, a1 = pr.y;
 #pragma unroll
-                    for (int t = 1; t < P; ++t) acc = fadd(acc, fmul(taps.w[t], v[k + t]));
-                    o[k] = acc;
+                    for (int t = 1; t < P; ++t) {
+                        pr = fmul2(make_float2(taps.w[t], taps.w[t]), make_float2(v[k + t], v[k + 1 + t]));
+                        a0 = fadd(a0, pr.x);
+                        a1 = fadd(a1, pr.y);
+                    }
+                    o[k] = a0;
+                    o[k + 1] = a1;
                 }
                 float4* xo = reinterpret_cast<float4*>(x_s + r * G::XS + sg * 8);
                 xo[0] = make_float4(o[0], o[1], o[2], o[3]);
@@ -121,13 +141,22 @@ blur3d_ring_kernel(const float* __restrict__ src, float* __restrict__ dst, float
 #pragma unroll
             for (int i = 0; i < 4 + 2 * R; ++i) col[i] = x_s[(4 * wy + i) * G::XS + lane];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                float acc = fmul(taps.w[0], col[j]);
+            for (int j = 0; j < 4; j += 2) {
+                float2 pr = fmul2(make_float2(taps.w[0], taps.w[0]), make_float2(col[j], col[j + 1]));
+                float a0 = pr.x, a1 = pr.y;
 #pragma unroll
-                for (int t = 1; t < P; ++t) acc = fadd(acc, fmul(taps.w[t], col[j + t]));
+                for (int t = 1; t < P; ++t) {
+                    pr = fmul2(make_float2(taps.w[t], taps.w[t]), make_float2(col[j + t], col[j + 1 + t]));
+                    a0 = fadd(a0, pr.x);
+                    a1 = fadd(a1, pr.y);
+                }
 #pragma unroll
-                for (int t = 0; t < P - 1; ++t) ring[j][t] = ring[j][t + 1];
-                ring[j][P - 1] = acc;
+                for (int t = 0; t < P - 1; ++t) {
+                    ring[j][t] = ring[j][t + 1];
+                    ring[j + 1][t] = ring[j + 1][t + 1];
+                }
+                ring[j][P - 1] = a0;
+                ring[j + 1][P - 1] = a1;
             }
         }
         if (p < 2 * R) continue;
@@ -136,16 +165,31 @@ blur3d_ring_kernel(const float* __restrict__ src, float* __restrict__ dst, float
         const int gx = x0 + lane;
         float out[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            float acc = fmul(taps.w[0], ring[j][0]);
+        for (int j = 0; j < 4; j += 2) {
+            float2 pr = fmul2(make_float2(taps.w[0], taps.w[0]), make_float2(ring[j][0], ring[j + 1][0]));
+            float a0 = pr.x, a1 = pr.y;
 #pragma unroll
-            for (int t = 1; t < P; ++t) acc = fadd(acc, fmul(taps.w[t], ring[j][t]));
-            out[j] = acc;
-            const int gy = y0 + 4 * wy + j;
-            if (gx < nx && gy < ny) {
-                const long long idx = b * vol + (long long)zo * plane + (long long)gy * nx + gx;
-                dst[idx] = acc;
-                if (dog) dog[idx] = __fsub_rn(__ldg(src + idx), acc);
+            for (int t = 1; t < P; ++t) {
+                pr = fmul2(make_float2(taps.w[t], taps.w[t]), make_float2(ring[j][t], ring[j + 1][t]));
+                a0 = fadd(a0, pr.x);
+                a1 = fadd(a1, pr.y);
+            }
+            out[j] = a0;
+            out[j + 1] = a1;
+        }
+        {
+            // 32-bit offsets within the volume (a volume holds < 2^31 voxels)
+            float* dv = dst + b * vol + (long long)zo * plane;
+            float* gv = dog ? dog + b * vol + (long long)zo * plane : nullptr;
+            const float* sv = src + b * vol + (long long)zo * plane;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int gy = y0 + 4 * wy + j;
+                if (gx < nx && gy < ny) {
+                    const unsigned o = (unsigned)gy * (unsigned)nx + (unsigned)gx;
+                    dv[o] = out[j];
+                    if (gv) gv[o] = __fsub_rn(__ldg(sv + o), out[j]);
+                }
             }
         }
         if (half != nullptr && (zo & 1)) {
@@ -281,9 +325,13 @@ static int launch_ring(const float* src, float* dst, float* dog, float* half, in
         configured = true;
     }
     const int tiles = ((nx + kTX - 1) / kTX) * ((ny + kTY - 1) / kTY);
-    // z-chunking: enough CTAs for ~2 waves on 148 SMs, chunk >= 16 planes and even.
+    // z-chunking only when the batch does not fill ~1.5 waves (2 CTAs / SM):
+    // every chunk re-reads and re-blurs 2R halo planes.
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int nzc = 1;
-    while ((long long)tiles * nb * nzc < 296 && (nz + nzc) / (nzc + 1) >= 16) ++nzc;
+    while ((long long)tiles * nb * nzc < 3 * sms && (nz + nzc) / (nzc + 1) >= 16) ++nzc;
     int tz = (nz + nzc - 1) / nzc;
     tz += tz & 1;
     nzc = (nz + tz - 1) / tz;

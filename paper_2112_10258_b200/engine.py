@@ -127,10 +127,12 @@ class DeviceTables:
         self.pair_ok = t.from_numpy(ok.copy()).cuda()
         self.rot_table = t.from_numpy(rot.reshape(-1).copy()).cuda()
         self.ico = np.ascontiguousarray(T.icosphere_structure())
-        balls, off, win = plan.balls.arrays()
+        balls, off, win, planes = plan.balls.arrays()
         self.balls = _lib.to_device_records(balls)
         self.ball_offsets = t.from_numpy(off.copy()).cuda()
         self.windows = t.from_numpy(win.copy()).cuda()
+        self.plane_starts = t.from_numpy(planes.copy()).cuda()
+        self.windows32 = t.from_numpy(win.astype(np.float32)).cuda()
         self.pairs = None
         self.pts = None
         if cfg.descriptor != "siftrank":
@@ -204,7 +206,7 @@ class Extractor:
         self.frame_first = t.zeros(self.kp_cap, dtype=i32, device="cuda")
         self.prim = t.zeros(self.kp_cap * self.maxf, dtype=i32, device="cuda")
         self.sec = t.zeros(self.kp_cap * self.maxf, dtype=i32, device="cuda")
-        self.status = t.zeros(1, dtype=i32, device="cuda")
+        self.status = t.zeros(4, dtype=i32, device="cuda")  # [0] DataError bit, [1] orient fallbacks, [2] sr fallbacks
         self.frames = t.empty(self.frame_cap * 16, dtype=t.uint8, device="cuda")
         self.rot = t.empty(self.frame_cap * 9, dtype=t.float64, device="cuda")
         self.n_frames = t.zeros(1, dtype=i32, device="cuda")
@@ -265,7 +267,8 @@ class Extractor:
         tb, cfg = self.tables, self.cfg
         _memset(self.status, s)
         _lib.call("vk_orient", self.kps.data_ptr(), self.total.data_ptr(), self.kp_cap, self.level_table.data_ptr(),
-                  tb.balls.data_ptr(), tb.ball_offsets.data_ptr(), tb.windows.data_ptr(), tb.dirs.data_ptr(), tb.K,
+                  tb.balls.data_ptr(), tb.ball_offsets.data_ptr(), tb.windows.data_ptr(), tb.windows32.data_ptr(),
+                  tb.dirs.data_ptr(), tb.K,
                   tb.pair_ok.data_ptr(), float(cfg.secondary_ratio), self.maxf, None, self.nframes.data_ptr(),
                   self.prim.data_ptr(), self.sec.data_ptr(), self.status.data_ptr(), self.exact_only,
                   tb.ico.ctypes.data, s)
@@ -278,9 +281,11 @@ class Extractor:
         """describe_all (descriptor.py:266-306)."""
         tb, cfg = self.tables, self.cfg
         if cfg.descriptor == "siftrank":
-            _lib.call("vk_describe_siftrank", self.frames.data_ptr(), self.rot.data_ptr(), self.n_frames.data_ptr(),
-                      self.frame_cap, self.kps.data_ptr(), self.level_table.data_ptr(), tb.balls.data_ptr(),
-                      tb.ball_offsets.data_ptr(), self.desc.data_ptr(), self.exact_only, s)
+            # one work item per keypoint: its frames are contiguous from frame_first[i]
+            _lib.call("vk_describe_siftrank", self.frames.data_ptr(), self.rot.data_ptr(), self.frame_first.data_ptr(),
+                      self.nframes.data_ptr(), self.total.data_ptr(), self.kp_cap, self.maxf, self.kps.data_ptr(),
+                      self.level_table.data_ptr(), tb.balls.data_ptr(), tb.ball_offsets.data_ptr(),
+                      self.desc.data_ptr(), self.exact_only, self.status.data_ptr() + 8, s)
         else:
             code = KIND_CODE[cfg.descriptor]
             _lib.call("vk_describe_patch", code, self.frames.data_ptr(), self.rot.data_ptr(),
@@ -328,8 +333,10 @@ class Extractor:
     def counts(self) -> dict:
         tot = self.total.cpu().numpy()
         nf = int(self.n_frames.cpu().item())
-        st = int(self.status.cpu().item())
+        stv = self.status.cpu().numpy()
+        st = int(stv[0])
         return dict(keypoints=int(tot[0]), cand_overflow=bool(tot[1]), frames=nf, status=st,
+                    orient_fallbacks=int(stv[1]), siftrank_fallbacks=int(stv[2]),
                     dropped=int(self.dropped.cpu().item()), cand=self.cand_count.cpu().numpy())
 
     def check_capacity(self) -> dict:

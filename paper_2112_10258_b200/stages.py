@@ -87,11 +87,12 @@ def run_orientation(pyr, keypoints, radius_factor=4.0, secondary_ratio=0.8, max_
     if n == 0:
         return dict(nframes=np.zeros(0, np.int32), prim=np.zeros((0, mf), np.int32),
                     sec=np.zeros((0, mf), np.int32), weights=np.zeros((0, len(dirs))))
-    b, off, win = balls.arrays()
+    b, off, win, planes = balls.arrays()
     d_kps = _lib.to_device_records(rec)
     d_balls = _lib.to_device_records(b)
     d_off = t.from_numpy(off.copy()).cuda()
     d_win = t.from_numpy(win.copy()).cuda()
+    d_win32 = t.from_numpy(win.astype(np.float32)).cuda()
     d_dirs = t.from_numpy(dirs.copy()).cuda()
     d_ok = t.from_numpy(np.ascontiguousarray(ok).copy()).cuda()
     K = len(dirs)
@@ -99,13 +100,13 @@ def run_orientation(pyr, keypoints, radius_factor=4.0, secondary_ratio=0.8, max_
     nframes = t.zeros(n, dtype=t.int32, device="cuda")
     prim = t.zeros(n * mf, dtype=t.int32, device="cuda")
     sec = t.zeros(n * mf, dtype=t.int32, device="cuda")
-    status = t.zeros(1, dtype=t.int32, device="cuda")
+    status = t.zeros(4, dtype=t.int32, device="cuda")
     ico = np.ascontiguousarray(T.icosphere_structure()) if directions is None else None
     _lib.call("vk_orient", d_kps.data_ptr(), None, n, view.table.data_ptr(), d_balls.data_ptr(), d_off.data_ptr(),
-              d_win.data_ptr(), d_dirs.data_ptr(), K, d_ok.data_ptr(), float(secondary_ratio), mf, _lib.ptr(weights),
+              d_win.data_ptr(), d_win32.data_ptr(), d_dirs.data_ptr(), K, d_ok.data_ptr(), float(secondary_ratio), mf, _lib.ptr(weights),
               nframes.data_ptr(), prim.data_ptr(), sec.data_ptr(), status.data_ptr(), int(bool(exact)),
               None if ico is None else ico.ctypes.data, _lib.stream_ptr())
-    if int(status.item()) & 1:
+    if int(status[0].item()) & 1:
         raise DataError("orientation neighborhood lies entirely outside the volume")
     out = dict(nframes=nframes.cpu().numpy(), prim=prim.cpu().numpy().reshape(n, mf),
                sec=sec.cpu().numpy().reshape(n, mf))
@@ -136,7 +137,7 @@ def run_descriptors(pyr, keypoints, rotations, kind="siftrank", pairs=None, patc
         out = t.empty((max(m, 1), pairs.n), dtype=t.int16, device="cuda")
     if m == 0:
         return out[:0].cpu().numpy()
-    b, off, win = balls.arrays()
+    b, off, win, planes = balls.arrays()
     d_kps = _lib.to_device_records(rec)
     d_fr = _lib.to_device_records(fr)
     d_rot = t.from_numpy(rot.reshape(-1).copy()).cuda()
@@ -144,8 +145,11 @@ def run_descriptors(pyr, keypoints, rotations, kind="siftrank", pairs=None, patc
     if kind == "siftrank":
         d_balls = _lib.to_device_records(b)
         d_off = t.from_numpy(off.copy()).cuda()
-        _lib.call("vk_describe_siftrank", d_fr.data_ptr(), d_rot.data_ptr(), None, m, d_kps.data_ptr(),
-                  view.table.data_ptr(), d_balls.data_ptr(), d_off.data_ptr(), out.data_ptr(), int(bool(exact)), s)
+        first = t.arange(m, dtype=t.int32, device="cuda")
+        count = t.ones(m, dtype=t.int32, device="cuda")
+        _lib.call("vk_describe_siftrank", d_fr.data_ptr(), d_rot.data_ptr(), first.data_ptr(), count.data_ptr(), None,
+                  m, 1, d_kps.data_ptr(), view.table.data_ptr(), d_balls.data_ptr(), d_off.data_ptr(),
+                  out.data_ptr(), int(bool(exact)), None, s)
     else:
         if patch_side < 1 or patch_side % 2 == 0:
             raise ParameterError(f"patch side must be odd and >= 1, got {patch_side}")

@@ -168,43 +168,61 @@ def window_table(radius: float, max_d2: int) -> np.ndarray:
 
 
 class BallTable:
-    """Concatenated balls for a set of radii, as uploaded to the device."""
+    """Concatenated balls for a set of radii, as uploaded to the device.
+
+    Each ball contributes its offsets twice: in the reference's x-major order
+    (exact-order accumulation) and z-major with per-plane start indices (the
+    slab-staged fast path walks the ball plane by plane)."""
 
     def __init__(self):
         self.radii: list[float] = []
         self._index: dict[float, int] = {}
-        self.records: list[tuple[int, int, int, int]] = []
+        self.records: list[tuple] = []
         self._off: list[np.ndarray] = []
         self._win: list[np.ndarray] = []
+        self._planes: list[np.ndarray] = []
         self._noff = 0
         self._nwin = 0
+        self._nplanes = 0
 
     def index(self, radius: float) -> int:
         """Ball id for an orientation / SIFT-Rank radius (radius_factor * sigma_local)."""
         key = float(radius)
         if key in self._index:
             return self._index[key]
-        offs = ball_offsets(int(round(radius * 1024)))
+        rq = int(round(radius * 1024))
+        offs = ball_offsets(rq)
+        r = int(math.floor(rq / 1024.0))
         max_d2 = int(np.max(np.sum(offs * offs, axis=1))) if len(offs) else 0
+        zorder = np.lexsort((offs[:, 0], offs[:, 1], offs[:, 2])) if len(offs) else np.zeros(0, np.int64)
+        zoffs = offs[zorder]
+        counts = np.bincount(zoffs[:, 2] + r, minlength=2 * r + 1) if len(offs) else np.zeros(2 * r + 1, np.int64)
+        planes = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
         self._index[key] = len(self.records)
-        self.records.append((self._noff, len(offs), self._nwin, max_d2))
+        n = len(offs)
+        self.records.append((self._noff, n, self._nwin, max_d2, self._noff + n, self._nplanes, r, 0))
         self._off.append(pack_offsets(offs))
+        self._off.append(pack_offsets(zoffs))
         self._win.append(window_table(radius, max_d2))
-        self._noff += len(offs)
+        self._planes.append(planes)
+        self._noff += 2 * n
         self._nwin += max_d2 + 1
+        self._nplanes += len(planes)
         self.radii.append(key)
         return self._index[key]
 
     def arrays(self):
+        """(ball records, packed offsets, windows, plane starts)."""
         from ._lib import BALL_DTYPE
 
-        rec = np.array(self.records, dtype=np.int32).reshape(-1, 4)
+        rec = np.array(self.records, dtype=np.int32).reshape(-1, len(BALL_DTYPE.names))
         balls = np.zeros(len(rec), dtype=BALL_DTYPE)
         for i, name in enumerate(BALL_DTYPE.names):
             balls[name] = rec[:, i] if len(rec) else 0
         off = np.concatenate(self._off) if self._off else np.zeros(1, np.int32)
         win = np.concatenate(self._win) if self._win else np.zeros(1, np.float64)
-        return balls, off, win
+        planes = np.concatenate(self._planes) if self._planes else np.zeros(1, np.int32)
+        return balls, off, win, planes
 
 
 # ------------------------------------------------------------ patch & pairs

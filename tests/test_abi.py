@@ -37,7 +37,7 @@ def test_library_loads_and_exports_every_declared_symbol():
 def test_record_layouts_match_header():
     src = open(os.path.join(REPO, "include", "volkey_b200.h")).read()
     assert _lib.LEVEL_DTYPE.itemsize == 32 and _lib.KP_DTYPE.itemsize == 32
-    assert _lib.BALL_DTYPE.itemsize == 16 and _lib.FRAME_DTYPE.itemsize == 16
+    assert _lib.BALL_DTYPE.itemsize == 32 and _lib.FRAME_DTYPE.itemsize == 16
     for struct, dt in (("vk_kp", _lib.KP_DTYPE), ("vk_ball", _lib.BALL_DTYPE), ("vk_frame", _lib.FRAME_DTYPE)):
         body = re.search(r"typedef struct %s \{(.*?)\}" % struct, src, re.S).group(1)
         fields = re.findall(r"int\s+([\w, ]+);", body)

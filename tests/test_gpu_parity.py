@@ -278,10 +278,11 @@ def test_fast_path_adversarial(kind):
 
     rng = np.random.default_rng(11)
     smooth = synthetic.random_blob_phantom((36, 38, 34), rng, n_blobs=14, margin=4)
-    vols = [np.round(smooth * 8.0).astype(np.float32) / 8.0,                       # plateaus + ties
-            rng.integers(0, 3, size=(30, 32, 28)).astype(np.float32),              # integer noise
+    vols = [np.round(smooth * 256.0).astype(np.float32) / 256.0,                   # plateaus + ties
+            rng.integers(0, 9, size=(30, 32, 28)).astype(np.float32),              # integer noise
             np.where(smooth > 0.05, 1.0, 0.0).astype(np.float32) + smooth * 1e-3]  # near-binary
     cfg = PipelineConfig(descriptor=kind, num_octaves=2)
+    n_desc = []
     for vol in vols:
         outs = []
         for exact in (False, True):
@@ -294,4 +295,8 @@ def test_fast_path_adversarial(kind):
         assert np.array_equal(a["desc"], b["desc"])
         want = O.extract(vol, descriptor=kind, num_octaves=2)
         assert a["n_keypoints"] == len(want["keypoints"])
-        assert np.array_equal(a["desc"].astype(np.int64), O.desc_array(want["records"], kind).astype(np.int64))
+        assert len(a["desc"]) == len(want["records"])
+        if len(want["records"]):
+            assert np.array_equal(a["desc"].astype(np.int64), O.desc_array(want["records"], kind).astype(np.int64))
+        n_desc.append(len(want["records"]))
+    assert sum(n_desc) > 20

@@ -50,7 +50,7 @@ def test_ball_table_and_windows():
     bt = T.BallTable()
     i0 = bt.index(4.0 * 1.6)
     assert bt.index(4.0 * 1.6) == i0
-    balls, off, win = bt.arrays()
+    balls, off, win, planes = bt.arrays()
     n = balls[i0]["count"]
     offs = T.ball_offsets(int(round(4.0 * 1.6 * 1024)))
     assert n == len(offs)
@@ -59,3 +59,12 @@ def test_ball_table_and_windows():
     sd = 4.0 * 1.6 / 2.0
     d2 = np.sum(offs * offs, axis=1).astype(np.float64)
     assert np.array_equal(win[balls[i0]["window_start"] + d2.astype(int)], np.exp(-d2 / (2.0 * sd * sd)))
+    # z-major copy: same point set, sorted by (oz, oy, ox), with per-plane starts
+    z0 = balls[i0]["zstart"]
+    zo = np.stack([((off[z0:z0 + n] >> s) & 1023) - 512 for s in (20, 10, 0)], axis=1)
+    assert sorted(map(tuple, zo)) == sorted(map(tuple, offs))
+    assert np.all(np.diff(zo[:, 2] * 10**6 + zo[:, 1] * 10**3 + zo[:, 0]) > 0)
+    r = balls[i0]["r"]
+    ps = planes[balls[i0]["pstart"]: balls[i0]["pstart"] + 2 * r + 2]
+    for oz in range(-r, r + 1):
+        assert np.all(zo[ps[oz + r]: ps[oz + r + 1], 2] == oz)
