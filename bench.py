@@ -222,20 +222,22 @@ def run_ours(a):
     launches_per_step = _lib.load().vk_launch_count() - launches0
     # ---- per-stage device times (eager, events on the pipeline stream)
     st = torch.cuda.current_stream()
-    stage_ms = {k: [] for k in ("pyramid", "detect", "orient", "describe")}
+    stage_ms = {k: [] for k in ("pyramid", "detect", "gradients", "orient", "describe")}
     for _ in range(3):
         ex = exs[0]
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         s = st.cuda_stream
         ev[0].record(st)
         ex.enqueue_pyramid(s)
         ev[1].record(st)
         ex.enqueue_detect(s)
         ev[2].record(st)
-        ex.enqueue_orient(s)
+        ex.enqueue_gradients(s)
         ev[3].record(st)
-        ex.enqueue_describe(s)
+        ex.enqueue_orient(s)
         ev[4].record(st)
+        ex.enqueue_describe(s)
+        ev[5].record(st)
         torch.cuda.synchronize()
         for k, (e0, e1) in zip(stage_ms, zip(ev[:-1], ev[1:])):
             stage_ms[k].append(e0.elapsed_time(e1))

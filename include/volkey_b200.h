@@ -52,6 +52,17 @@ typedef struct vk_level {
     int pad_;
 } vk_level;
 
+/* Precomputed per-voxel gradient data of one pyramid level (batch strided):
+ * g4[v] = (gx, gy, gz, |g|) in fp32 (|g| from fp64), bin[v] = nearest of the
+ * 42 icosphere directions (exact np.argmax semantics) or 255 for g == 0. */
+typedef struct vk_gradlevel {
+    const void* g4;
+    const uint8_t* bin;
+    long long vol_stride;
+    int nx, ny, nz;
+    int pad_;
+} vk_gradlevel;
+
 /* One keypoint (device record). */
 typedef struct vk_kp {
     int vol;      /* volume index within the batch */
@@ -159,18 +170,26 @@ int vk_order_keypoints(const unsigned long long* cand_keys, const int* cand_coun
  * only): 12 icosahedron-vertex indices into dirs followed by 12x5 indices of
  * the edge midpoints around each vertex, enabling the screened argmax.
  * exact_only != 0 forces the reference accumulation order and the brute-force
- * argmax for every keypoint (weights then bit-identical to the reference). */
+ * argmax for every keypoint (weights then bit-identical to the reference).
+ * grads (nullable, indexed like levels): precomputed gradient volumes
+ * (vk_gradient_volume); levels without one use direct gathers. */
 int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_level* levels,
               const vk_ball* balls, const int* ball_offsets, const double* windows,
               const float* windows32, const double* dirs, int K, const uint8_t* pair_ok,
               double secondary_ratio, int max_frames,
               double* weights, int* nframes, int* prim, int* sec, int* status,
-              int exact_only, const int* ico_host, void* stream);
+              int exact_only, const int* ico_host, const vk_gradlevel* grads, void* stream);
 
 /* dominant_orientations (orient.py:310-350) on n caller-supplied K-bin
  * weight vectors (exact comparisons). */
 int vk_frames_from_weights(const double* weights, int n, int K, const uint8_t* pair_ok, double secondary_ratio,
                            int max_frames, int* nframes, int* prim, int* sec, void* stream);
+
+/* Dense gradient volume of a batched level for the orientation / SIFT-Rank
+ * fast paths (volume.py:244-264 gradients, orient.py:305 nearest direction
+ * with the default icosphere; ico_host as in vk_orient). */
+int vk_gradient_volume(const float* level, void* g4, uint8_t* bin, int nb, int nx, int ny, int nz,
+                       const double* dirs, const int* ico_host, void* stream);
 
 /* Expand per-keypoint frames into the ordered frame list (pipeline.py:55-67:
  * keypoints with zero frames are dropped).  rot_table: K*K*9 fp64 rotations
@@ -193,7 +212,7 @@ int vk_describe_siftrank(const vk_frame* frames, const double* rot, const int* i
                          const int* item_count, const int* n_items_dev, int n_items_max, int max_f,
                          const vk_kp* kps, const vk_level* levels, const vk_ball* balls,
                          const int* ball_offsets, uint8_t* ranks_out,
-                         int exact_only, int* stats, void* stream);
+                         int exact_only, int* stats, const vk_gradlevel* grads, void* stream);
 
 /* extract_patch + preblur_patch + brief/rrief (descriptor.py:96-111,
  * 196-224).  kind 1 = BRIEF (packed big-endian bits, ceil(n/8) bytes per

@@ -41,10 +41,11 @@ SIGNATURES = {
     "vk_detect_octave": [P, I, I, I, I, I, I, I, F, P, P, I, P],
     "vk_extrema_from_map": [P, P, I, I, I, I, I, F, P, P, I, P],
     "vk_order_keypoints": [P, P, I, I, P, P, I, P, P, P, P, P, P, P, P, I, P],
-    "vk_orient": [P, P, I, P, P, P, P, P, P, I, P, D, I, P, P, P, P, P, I, P, P],
+    "vk_orient": [P, P, I, P, P, P, P, P, P, I, P, D, I, P, P, P, P, P, I, P, P, P],
     "vk_frames_from_weights": [P, I, I, P, D, I, P, P, P, P],
     "vk_expand_frames": [P, P, P, P, I, I, P, I, P, P, P, P, I, P, P],
-    "vk_describe_siftrank": [P, P, P, P, P, I, I, P, P, P, P, P, I, P, P],
+    "vk_describe_siftrank": [P, P, P, P, P, I, I, P, P, P, P, P, I, P, P, P],
+    "vk_gradient_volume": [P, P, P, I, I, I, I, P, P, P],
     "vk_describe_patch": [I, P, P, P, I, P, P, P, P, I, P, P, I, P, I, P, P, P],
     "vk_match": [I, P, I, P, I, I, D, P, P, P, P, P],
 }
@@ -55,6 +56,8 @@ LEVEL_DTYPE = np.dtype([("base", "<u8"), ("vol_stride", "<i8"), ("nx", "<i4"), (
                         ("pad", "<i4")])
 KP_DTYPE = np.dtype([(n, "<i4") for n in ("vol", "lvl", "ix", "iy", "iz", "ball", "octave", "level")])
 BALL_DTYPE = np.dtype([(n, "<i4") for n in ("start", "count", "window_start", "max_d2", "zstart", "pstart", "r", "pad")])
+GRADLEVEL_DTYPE = np.dtype([("g4", "<u8"), ("bin", "<u8"), ("vol_stride", "<i8"), ("nx", "<i4"), ("ny", "<i4"),
+                            ("nz", "<i4"), ("pad", "<i4")])
 FRAME_DTYPE = np.dtype([(n, "<i4") for n in ("kp", "prim", "sec", "pad")])
 
 _lock = threading.Lock()

@@ -67,11 +67,20 @@ __device__ __noinline__ int sr_bin_exact(int ox, int oy, int oz, double x64, dou
     return 8 * ((r0 > 0.0) + 2 * (r1 > 0.0) + 4 * (r2 > 0.0)) + (g0 > 0.0) + 2 * (g1 > 0.0) + 4 * (g2 > 0.0);
 }
 
+// Rare path when only the fp32 gradient is at hand: reload the neighbours.
+__device__ __noinline__ int sr_bin_exact_reload(int ox, int oy, int oz, const float* data, int nx, int ny, int nz,
+                                                int x, int y, int z, const double* R) {
+    const Nb6 n = load_nb6(data, nx, ny, nz, x, y, z);
+    double x64, y64, z64;
+    grad64(n, x64, y64, z64);
+    return sr_bin_exact(ox, oy, oz, x64, y64, z64, R);
+}
+
 // Fast SIFT-Rank bin of one voxel for one frame: octant bits decided in fp32
 // whenever each rotated component clears its error bound (<= ~5 u32 of the L1
 // norm; bound 1e-6), otherwise recomputed with the reference's fp64 FMA chain.
-VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const Nb6& n, const double* R,
-                     const float* Rf) {
+VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const double* R, const float* Rf,
+                     const float* data, int nx, int ny, int nz, int x, int y, int z) {
     const float fx = (float)ox, fy = (float)oy, fz = (float)oz;
     const float eo = 1.0e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
     const float eg = 1.0e-6f * (fabsf(gx) + fabsf(gy) + fabsf(gz)) + 1.0e-40f;
@@ -87,47 +96,56 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
     if (sure)
         return 8 * ((r[0] > 0.f) + 2 * (r[1] > 0.f) + 4 * (r[2] > 0.f)) + (g[0] > 0.f) + 2 * (g[1] > 0.f) +
                4 * (g[2] > 0.f);
-    double x64, y64, z64;
-    grad64(n, x64, y64, z64);
-    return sr_bin_exact(ox, oy, oz, x64, y64, z64, R);
+    return sr_bin_exact_reload(ox, oy, oz, data, nx, ny, nz, x, y, z, R);
 }
 
 // Fast walk of one keypoint's ball for NF frames (rotations in registers);
-// returns the number of in-volume ball voxels seen by this thread.
+// returns the number of in-volume ball voxels seen by this thread.  With a
+// precomputed gradient volume (g4 != null) each visit is one float4 load.
 template <int NF>
-VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
+VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const float4* g4, const vk_ball& ball,
                  const int* __restrict__ ball_offsets, const double* Rs, const float* Rfs, double* hist, int F) {
-    float Rf[NF][9];
-#pragma unroll
-    for (int f = 0; f < NF; ++f)
-#pragma unroll
-        for (int e = 0; e < 9; ++e) Rf[f][e] = Rfs[9 * f + e];
     const int tid = threadIdx.x, wid = tid >> 5;
+    const int step = blockDim.x;
     int cnt = 0;
-    for (int base = 0; base < ball.count; base += blockDim.x) {
+    int pn = tid < ball.count ? __ldg(ball_offsets + ball.zstart + tid) : 0;
+    for (int base = 0; base < ball.count; base += step) {
         const int j = base + tid;
+        const int p = pn;
+        if (j + step < ball.count) pn = __ldg(ball_offsets + ball.zstart + j + step);
         bool has = false;
-        int ox = 0, oy = 0, oz = 0;
+        int ox = 0, oy = 0, oz = 0, x = 0, y = 0, z = 0;
         float gx = 0.f, gy = 0.f, gz = 0.f, mag = 0.f;
-        Nb6 nb{};
         if (j < ball.count) {
-            const int p = __ldg(ball_offsets + ball.zstart + j);
             ox = unpack_off(p, 0);
             oy = unpack_off(p, 1);
             oz = unpack_off(p, 2);
-            const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
+            x = kp.ix + ox;
+            y = kp.iy + oy;
+            z = kp.iz + oz;
             if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
                 ++cnt;
-                nb = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
-                grad32(nb, gx, gy, gz);
-                has = !(gx == 0.f && gy == 0.f && gz == 0.f);  // zero vote: no bin changes
-                if (has) mag = norm3_f32(gx, gy, gz);
+                if (g4) {
+                    const float4 q = __ldg(g4 + (((unsigned)z * (unsigned)L.ny + (unsigned)y) * (unsigned)L.nx + (unsigned)x));
+                    gx = q.x;
+                    gy = q.y;
+                    gz = q.z;
+                    mag = q.w;
+                    has = mag > 0.f;  // |g| > 0 exactly when g != 0 (fp64 norm, never underflows in fp32)
+                } else {
+                    const Nb6 nb = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
+                    grad32(nb, gx, gy, gz);
+                    has = !(gx == 0.f && gy == 0.f && gz == 0.f);  // zero vote: no bin changes
+                    if (has) mag = norm3_f32(gx, gy, gz);
+                }
             }
         }
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             if (f >= F) break;
-            const int bin = has ? sr_bin_fast(ox, oy, oz, gx, gy, gz, nb, Rs + 9 * f, Rf[f]) : -1;
+            const int bin = has ? sr_bin_fast(ox, oy, oz, gx, gy, gz, Rs + 9 * f, Rfs + 9 * f, data, L.nx, L.ny, L.nz, x,
+                                              y, z)
+                                : -1;
             warp_accum(hist + (f * (blockDim.x >> 5) + wid) * 64, bin, mag);
         }
     }
@@ -145,13 +163,14 @@ VK_D int stable_rank(const double* w, int n, int b) {
 // One CTA per work item = one keypoint and its F frames (contiguous in the
 // frame list).  The ball is walked in z-major order (coalesced gathers);
 // each voxel's gradient is computed once and voted into all F frames.
-__global__ void __launch_bounds__(kSrThreads, 3)
+__global__ void __launch_bounds__(kSrThreads, 2)
 siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ rot,
                 const int* __restrict__ item_first, const int* __restrict__ item_count,
                 const int* __restrict__ n_items_dev, int n_items_max, const vk_kp* __restrict__ kps,
                 const vk_level* __restrict__ levels, const vk_ball* __restrict__ balls,
                 const int* __restrict__ ball_offsets, int max_f,
-                uint8_t* __restrict__ out, int exact_only, int* __restrict__ stats) {
+                uint8_t* __restrict__ out, int exact_only, int* __restrict__ stats,
+                const vk_gradlevel* __restrict__ grads) {
     extern __shared__ double hist[];  // [max_f][kSrWarps][64]
     __shared__ double w[kSrBins];
     __shared__ int order[kSrBins];
@@ -159,7 +178,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
     __shared__ float Rfs[VK_MAX_FRAMES * 9];
     __shared__ int xb[kSrThreads];
     __shared__ double xv[kSrThreads];
-    __shared__ int n_inside, exact;
+    __shared__ int n_inside;
     const int tid = threadIdx.x;
     const int n = n_items_dev ? min(*n_items_dev, n_items_max) : n_items_max;
     for (int item = blockIdx.x; item < n; item += gridDim.x) {
@@ -182,14 +201,20 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
         const bool fast = !exact_only;
         if (fast) {
             // z-major ball walk: consecutive lanes take consecutive x -> coalesced gathers
+            const float4* g4 = nullptr;
+            if (grads) {
+                const vk_gradlevel GL = grads[kp.lvl];
+                if (GL.g4) g4 = reinterpret_cast<const float4*>(GL.g4) + (long long)kp.vol * GL.vol_stride;
+            }
             switch (F) {
-                case 1: cnt = sr_walk<1>(kp, L, data, ball, ball_offsets, Rs, Rfs, hist, F); break;
-                case 2: cnt = sr_walk<2>(kp, L, data, ball, ball_offsets, Rs, Rfs, hist, F); break;
-                case 3: cnt = sr_walk<3>(kp, L, data, ball, ball_offsets, Rs, Rfs, hist, F); break;
-                case 4: cnt = sr_walk<4>(kp, L, data, ball, ball_offsets, Rs, Rfs, hist, F); break;
-                default:  // > 4 frames: two passes of up to 4 frames (gradients recomputed)
-                    cnt = sr_walk<4>(kp, L, data, ball, ball_offsets, Rs, Rfs, hist, 4);
-                    sr_walk<4>(kp, L, data, ball, ball_offsets, Rs + 36, Rfs + 36, hist + 4 * kSrWarps * kSrBins, F - 4);
+                case 1: cnt = sr_walk<1>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, F); break;
+                case 2: cnt = sr_walk<2>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, F); break;
+                case 3: cnt = sr_walk<3>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, F); break;
+                case 4: cnt = sr_walk<4>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, F); break;
+                default:  // > 4 frames: two passes of up to 4 frames
+                    cnt = sr_walk<4>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, 4);
+                    sr_walk<4>(kp, L, data, g4, ball, ball_offsets, Rs + 36, Rfs + 36, hist + 4 * kSrWarps * kSrBins,
+                               F - 4);
                     break;
             }
         } else {
@@ -202,34 +227,37 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
         if (cnt) atomicAdd(&n_inside, cnt);
         __syncthreads();
         for (int f = 0; f < F; ++f) {
-            if (tid == 0) exact = fast ? 0 : 1;
             if (fast && tid < kSrBins) {
                 double sacc = 0.0;
                 for (int wi = 0; wi < kSrWarps; ++wi) sacc = dadd(sacc, hist[(f * kSrWarps + wi) * kSrBins + tid]);
                 w[tid] = sacc;
             }
             __syncthreads();
+            int myrank = 0;
+            if (tid < kSrBins) {
+                myrank = stable_rank(w, kSrBins, tid);
+                order[myrank] = tid;
+            }
+            __syncthreads();
+            int go_exact = 1;
             if (fast) {
-                if (tid < kSrBins) order[stable_rank(w, kSrBins, tid)] = tid;
-                __syncthreads();
-                if (tid == 0) {
-                    const double epsrel = 2.0 * (kVoteRel + kRunRel + gamma_k((double)n_inside + 64.0));
-                    const double epsabs = kVoteAbs * n_inside;
-                    for (int q = 0; q + 1 < kSrBins; ++q) {
-                        const double a = w[order[q]], b = w[order[q + 1]];
-                        if (a == 0.0 && b == 0.0) continue;  // exact empty-bin ties
+                // every adjacent pair of the sorted bins must be separated by more than
+                // the bound between our summation and the reference's sequential one
+                const double epsrel = 2.0 * (kVoteRel + kRunRel + gamma_k((double)n_inside + 64.0));
+                const double epsabs = kVoteAbs * n_inside;
+                int bad = 0;
+                if (tid + 1 < kSrBins) {
+                    const double a = w[order[tid]], b = w[order[tid + 1]];
+                    if (!(a == 0.0 && b == 0.0)) {  // exact empty-bin ties are order-independent
                         const double ahi = a == 0.0 ? 0.0 : dadd(a, a * epsrel + epsabs);
                         const double blo = dsub(b, b * epsrel + epsabs);
-                        if (!(ahi < blo)) {
-                            exact = 1;
-                            if (stats) atomicAdd(stats, 1);  // fallback counter (diagnostics)
-                            break;
-                        }
+                        bad = !(ahi < blo);
                     }
                 }
-                __syncthreads();
+                go_exact = __syncthreads_or(bad);
+                if (go_exact && tid == 0 && stats) atomicAdd(stats, 1);  // fallback counter (diagnostics)
             }
-            if (exact) {
+            if (go_exact) {
                 // Exact reference order: chunked exact votes, warp 0 adds in ball order.
                 double R[9];
 #pragma unroll
@@ -263,9 +291,10 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                     w[tid + 32] = acc1;
                 }
                 __syncthreads();
+                if (tid < kSrBins) myrank = stable_rank(w, kSrBins, tid);
+                __syncthreads();
             }
-            if (tid < kSrBins) out[(long long)(first + f) * kSrBins + tid] = (uint8_t)stable_rank(w, kSrBins, tid);
-            __syncthreads();
+            if (tid < kSrBins) out[(long long)(first + f) * kSrBins + tid] = (uint8_t)myrank;
         }
     }
 }
@@ -374,7 +403,7 @@ extern "C" int vk_describe_siftrank(const vk_frame* frames, const double* rot, c
                                     const int* item_count, const int* n_items_dev, int n_items_max, int max_f,
                                     const vk_kp* kps, const vk_level* levels, const vk_ball* balls,
                                     const int* ball_offsets, uint8_t* ranks_out,
-                                    int exact_only, int* stats, void* stream) {
+                                    int exact_only, int* stats, const vk_gradlevel* grads, void* stream) {
     if (!frames || !rot || !item_first || !item_count || n_items_max < 0 || max_f < 1 || max_f > VK_MAX_FRAMES ||
         !kps || !levels || !balls || !ball_offsets || !ranks_out) {
         set_error("vk_describe_siftrank: bad arguments");
@@ -391,7 +420,7 @@ extern "C" int vk_describe_siftrank(const vk_frame* frames, const double* rot, c
     }
     siftrank_kernel<<<grid_for(n_items_max, 4), kSrThreads, smem, as_stream(stream)>>>(
         frames, rot, item_first, item_count, n_items_dev, n_items_max, kps, levels, balls, ball_offsets, max_f,
-        ranks_out, exact_only, stats);
+        ranks_out, exact_only, stats, grads);
     count_launch();
     return cuda_status(cudaGetLastError(), "siftrank launch");
 }

@@ -98,6 +98,50 @@ VK_D void warp_accum(double* hist, int bin, float v) {
     }
 }
 
+// Register-resident variant: this warp's histogram lives in registers, lane L
+// owning bins L (acc0) and L + 32 (acc1).  Uniform warps butterfly-sum and the
+// owner adds; otherwise runs of equal bins are scan-reduced and each run's
+// (bin, sum) is broadcast from its last lane to the owner.  Same error model
+// as warp_accum (depth-5 fp32 tree per vote, then fp64).
+VK_D void warp_accum_reg(double& acc0, double& acc1, int bin, float v) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned act = __ballot_sync(FULL, bin >= 0);
+    if (act == 0) return;
+    const int b0 = __shfl_sync(FULL, bin, __ffs(act) - 1);
+    if (__all_sync(FULL, bin < 0 || bin == b0)) {
+        float s = bin >= 0 ? v : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s = fadd(s, __shfl_xor_sync(FULL, s, o));
+        if ((b0 & 31) == lane) {
+            if (b0 < 32) acc0 = dadd(acc0, (double)s);
+            else acc1 = dadd(acc1, (double)s);
+        }
+        return;
+    }
+    const int prev = __shfl_up_sync(FULL, bin, 1);
+    const unsigned heads = __ballot_sync(FULL, lane == 0 || prev != bin);
+    const int start = 31 - __clz(heads & (FULL >> (31 - lane)));
+    float s = bin >= 0 ? v : 0.f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float t = __shfl_up_sync(FULL, s, o);
+        if (lane - o >= start) s = fadd(s, t);
+    }
+    // tails: last lane of every run that votes
+    unsigned tails = __ballot_sync(FULL, bin >= 0 && (lane == 31 || ((heads >> (lane + 1)) & 1u)));
+    while (tails) {
+        const int t = __ffs(tails) - 1;
+        tails &= tails - 1;
+        const int bt = __shfl_sync(FULL, bin, t);
+        const float st = __shfl_sync(FULL, s, t);
+        if ((bt & 31) == lane) {
+            if (bt < 32) acc0 = dadd(acc0, (double)st);
+            else acc1 = dadd(acc1, (double)st);
+        }
+    }
+}
+
 // Ball plane range [oz0, oz0 + nT) -> z-major point index range.
 VK_D void plane_range(const int* __restrict__ plane_starts, const vk_ball& ball, int oz0, int nT, int& ps, int& pe) {
     ps = __ldg(plane_starts + ball.pstart + oz0 + ball.r);

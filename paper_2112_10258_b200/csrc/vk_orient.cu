@@ -170,6 +170,48 @@ VK_D int ori_vote_fast(const Nb6& n, const float* __restrict__ win32, int d2, co
     return nearest_dir(dirs, K, x64, y64, z64);
 }
 
+// Dense per-voxel gradient data for a batched level: (gx, gy, gz, |g|) with
+// |g| evaluated in fp64 (no fp32 underflow for tiny nonzero gradients) and
+// rounded once, plus the exact nearest icosphere direction (255 for g == 0).
+__global__ void __launch_bounds__(256)
+gradient_volume_kernel(const float* __restrict__ level, float4* __restrict__ g4, uint8_t* __restrict__ bins, int nx,
+                       int ny, int nz, long long total, const double* __restrict__ dirs_g, IcoT ico) {
+    __shared__ double dirs[42 * 3];
+    __shared__ IcoSh ic;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < 42 * 3; i += blockDim.x) dirs[i] = dirs_g[i];
+    if (tid < 72) {
+        const int v = tid / 6, c = tid % 6;
+        const int k = c == 0 ? ico.vert[v] : ico.adj[v][c - 1];
+        ic.ci[tid] = k;
+        ic.cd[tid] = make_float4((float)dirs_g[3 * k], (float)dirs_g[3 * k + 1], (float)dirs_g[3 * k + 2], 0.f);
+    }
+    __syncthreads();
+    const long long vol = (long long)nx * ny * nz;
+    for (long long i = (long long)blockIdx.x * blockDim.x + tid; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const long long b = i / vol;
+        const unsigned r = (unsigned)(i - b * vol);
+        const unsigned plane = (unsigned)nx * (unsigned)ny;
+        const int z = (int)(r / plane);
+        const unsigned rem = r - (unsigned)z * plane;
+        const int y = (int)(rem / (unsigned)nx);
+        const int x = (int)(rem - (unsigned)y * (unsigned)nx);
+        const Nb6 n = load_nb6(level + b * vol, nx, ny, nz, x, y, z);
+        float gx, gy, gz;
+        grad32(n, gx, gy, gz);
+        float4 o = make_float4(gx, gy, gz, 0.f);
+        int bin = 255;
+        if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {
+            double x64, y64, z64;
+            grad64(n, x64, y64, z64);
+            o.w = (float)norm3_numpy(x64, y64, z64);
+            bin = nearest_dir_ico(dirs, ic, gx, gy, gz, n);
+        }
+        g4[i] = o;
+        bins[i] = (uint8_t)bin;
+    }
+}
+
 // Frames from a weight vector whose comparisons are exact (dominant_orientations).
 // order[] must hold the bins sorted by (-w, index).
 VK_D int frames_from(const double* w, const int* order, int K, const uint8_t* ok, double ratio, int max_frames,
@@ -242,7 +284,7 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
               const float* __restrict__ windows32, const double* __restrict__ dirs_g, int K,
               const uint8_t* __restrict__ pair_ok, double ratio, int max_frames, double* __restrict__ weights,
               int* __restrict__ nframes, int* __restrict__ prim, int* __restrict__ sec, int* __restrict__ status,
-              int exact_only, IcoT ico) {
+              int exact_only, IcoT ico, const vk_gradlevel* __restrict__ grads) {
     __shared__ OriShared sh;
     __shared__ IcoSh ic;
     __shared__ double hist[kOriWarps * VK_MAX_DIRS];
@@ -270,15 +312,45 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         if (tid == 0) { sh.n_inside = 0; sh.exact = exact_only; }
         __syncthreads();
         int inside_cnt = 0;
-        if (!exact_only) {
-            // z-major ball walk: consecutive lanes take consecutive x -> coalesced gathers
+        const vk_gradlevel GL = grads ? grads[kp.lvl] : vk_gradlevel{};
+        if (!exact_only && GL.bin != nullptr) {
+            // precomputed gradient volume: one coalesced (bin, |g|) pair per visit
+            const uint8_t* bl = GL.bin + (long long)kp.vol * GL.vol_stride;
+            const float4* gl = reinterpret_cast<const float4*>(GL.g4) + (long long)kp.vol * GL.vol_stride;
             double* wh = hist + (tid >> 5) * K;
+            int pn = tid < ball.count ? __ldg(ball_offsets + ball.zstart + tid) : 0;
             for (int base = 0; base < ball.count; base += kOriThreads) {
                 const int j = base + tid;
+                const int p = pn;
+                if (j + kOriThreads < ball.count) pn = __ldg(ball_offsets + ball.zstart + j + kOriThreads);
                 int bin = -1;
                 float vote = 0.f;
                 if (j < ball.count) {
-                    const int p = __ldg(ball_offsets + ball.zstart + j);
+                    const int ox = unpack_off(p, 0), oy = unpack_off(p, 1), oz = unpack_off(p, 2);
+                    const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
+                    if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
+                        ++inside_cnt;
+                        const unsigned idx = ((unsigned)z * (unsigned)L.ny + (unsigned)y) * (unsigned)L.nx + (unsigned)x;
+                        const int b = __ldg(bl + idx);
+                        if (b != 255) {
+                            bin = b;
+                            vote = fmul(__ldg(&gl[idx].w), __ldg(win32 + (ox * ox + oy * oy + oz * oz)));
+                        }
+                    }
+                }
+                warp_accum(wh, bin, vote);
+            }
+        } else if (!exact_only) {
+            // z-major ball walk: consecutive lanes take consecutive x -> coalesced gathers
+            double* wh = hist + (tid >> 5) * K;
+            int pn = tid < ball.count ? __ldg(ball_offsets + ball.zstart + tid) : 0;
+            for (int base = 0; base < ball.count; base += kOriThreads) {
+                const int j = base + tid;
+                const int p = pn;
+                if (j + kOriThreads < ball.count) pn = __ldg(ball_offsets + ball.zstart + j + kOriThreads);
+                int bin = -1;
+                float vote = 0.f;
+                if (j < ball.count) {
                     const int ox = unpack_off(p, 0), oy = unpack_off(p, 1), oz = unpack_off(p, 2);
                     const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
                     if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
@@ -486,7 +558,7 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
                          const vk_ball* balls, const int* ball_offsets, const double* windows, const float* windows32,
                          const double* dirs, int K, const uint8_t* pair_ok, double secondary_ratio, int max_frames,
                          double* weights, int* nframes, int* prim, int* sec, int* status, int exact_only,
-                         const int* ico_host, void* stream) {
+                         const int* ico_host, const vk_gradlevel* grads, void* stream) {
     if (!kps || n_kp_max < 0 || !levels || !balls || !ball_offsets || !windows || !windows32 || !dirs || K < 1 ||
         K > VK_MAX_DIRS || !pair_ok || !nframes || !prim || !sec || !status || max_frames < 1 ||
         max_frames > VK_MAX_FRAMES || !(secondary_ratio > 0.0 && secondary_ratio <= 1.0)) {
@@ -509,7 +581,7 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
     orient_kernel<<<grid, kOriThreads, 0, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
                                                                windows, windows32, dirs, K, pair_ok, secondary_ratio,
                                                                max_frames, weights, nframes, prim, sec, status,
-                                                               exact_only, ico);
+                                                               exact_only, ico, grads);
     count_launch();
     return cuda_status(cudaGetLastError(), "orient launch");
 }
@@ -549,4 +621,26 @@ extern "C" int vk_expand_frames(const int* nframes, const int* prim, const int* 
         count_launch();
     }
     return cuda_status(cudaGetLastError(), "expand launch");
+}
+
+extern "C" int vk_gradient_volume(const float* level, void* g4, uint8_t* bin, int nb, int nx, int ny, int nz,
+                                  const double* dirs, const int* ico_host, void* stream) {
+    if (!level || !g4 || !bin || nb < 0 || nx < 1 || ny < 1 || nz < 1 || !dirs || !ico_host) {
+        set_error("vk_gradient_volume: bad arguments");
+        return VK_ERR_PARAMETER;
+    }
+    const long long total = (long long)nb * nx * ny * nz;
+    if (total == 0) return VK_OK;
+    IcoT ico{};
+    ico.valid = 1;
+    for (int v = 0; v < 12; ++v) {
+        ico.vert[v] = ico_host[v];
+        for (int m = 0; m < 5; ++m) ico.adj[v][m] = ico_host[12 + 5 * v + m];
+    }
+    long long blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    gradient_volume_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(level, static_cast<float4*>(g4), bin, nx, ny,
+                                                                            nz, total, dirs, ico);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "gradient volume launch");
 }

@@ -153,7 +153,7 @@ class Extractor:
     """Device buffers + launch sequence for B volumes of one shape and config."""
 
     def __init__(self, dims, cfg: PipelineConfig | None = None, batch: int = 1, kp_cap: int | None = None,
-                 frame_cap: int | None = None, exact_only: bool = False, input=None):
+                 frame_cap: int | None = None, exact_only: bool = False, input=None, gradient_volumes: bool = False):
         t = _lib.torch()
         self.cfg = cfg or PipelineConfig()
         self.plan = Plan.build(dims, self.cfg)
@@ -190,6 +190,17 @@ class Extractor:
                 if i < L - 1:
                     dog_t[o * L + i] = self.dogs[o][i]
         self.level_table = _lib.to_device_records(level_records(lvl_t, dims_l))
+        # dense gradient volumes of the keypoint levels (orientation / SIFT-Rank fast paths)
+        self.grad_levels = []  # (octave, level, g4 tensor, bin tensor)
+        grec = np.zeros(nseg, dtype=_lib.GRADLEVEL_DTYPE)
+        if gradient_volumes:
+            for o, (ox, oy, oz) in enumerate(self.plan.octave_dims):
+                for i in range(1, L - 2):
+                    g4 = t.empty((B, oz, oy, ox, 4), dtype=f32, device="cuda")
+                    bn = t.empty((B, oz, oy, ox), dtype=t.uint8, device="cuda")
+                    self.grad_levels.append((o, i, g4, bn))
+                    grec[o * L + i] = (g4.data_ptr(), bn.data_ptr(), ox * oy * oz, ox, oy, oz, 0)
+        self.grad_table = _lib.to_device_records(grec)
         self.dog_table = _lib.to_device_records(level_records(dog_t, dims_l))
         self.source_table = _lib.to_device_records(level_records([self.input], [self.plan.dims]))
         i32 = t.int32
@@ -262,6 +273,14 @@ class Extractor:
                   self.kps.data_ptr(), self.pos.data_ptr(), self.sigma.data_ptr(), self.dogv.data_ptr(),
                   self.sign.data_ptr(), self.vol_offset.data_ptr(), self.total.data_ptr(), self.kp_cap, s)
 
+    def enqueue_gradients(self, s: int) -> None:
+        """Dense gradient / nearest-direction volumes of the keypoint levels."""
+        tb = self.tables
+        for o, i, g4, bn in self.grad_levels:
+            nx, ny, nz = self.plan.octave_dims[o]
+            _lib.call("vk_gradient_volume", self.levels[o][i].data_ptr(), g4.data_ptr(), bn.data_ptr(), self.B, nx, ny,
+                      nz, tb.dirs.data_ptr(), tb.ico.ctypes.data, s)
+
     def enqueue_orient(self, s: int) -> None:
         """assign_orientations (pipeline.py:41-67)."""
         tb, cfg = self.tables, self.cfg
@@ -271,7 +290,7 @@ class Extractor:
                   tb.dirs.data_ptr(), tb.K,
                   tb.pair_ok.data_ptr(), float(cfg.secondary_ratio), self.maxf, None, self.nframes.data_ptr(),
                   self.prim.data_ptr(), self.sec.data_ptr(), self.status.data_ptr(), self.exact_only,
-                  tb.ico.ctypes.data, s)
+                  tb.ico.ctypes.data, self.grad_table.data_ptr(), s)
         _lib.call("vk_expand_frames", self.nframes.data_ptr(), self.prim.data_ptr(), self.sec.data_ptr(),
                   self.total.data_ptr(), self.kp_cap, self.maxf, tb.rot_table.data_ptr(), tb.K,
                   self.frames.data_ptr(), self.rot.data_ptr(), self.n_frames.data_ptr(), self.dropped.data_ptr(),
@@ -285,7 +304,8 @@ class Extractor:
             _lib.call("vk_describe_siftrank", self.frames.data_ptr(), self.rot.data_ptr(), self.frame_first.data_ptr(),
                       self.nframes.data_ptr(), self.total.data_ptr(), self.kp_cap, self.maxf, self.kps.data_ptr(),
                       self.level_table.data_ptr(), tb.balls.data_ptr(), tb.ball_offsets.data_ptr(),
-                      self.desc.data_ptr(), self.exact_only, self.status.data_ptr() + 8, s)
+                      self.desc.data_ptr(), self.exact_only, self.status.data_ptr() + 8,
+                      self.grad_table.data_ptr(), s)
         else:
             code = KIND_CODE[cfg.descriptor]
             _lib.call("vk_describe_patch", code, self.frames.data_ptr(), self.rot.data_ptr(),
@@ -299,6 +319,8 @@ class Extractor:
         rec = rec or _no_stage
         self.enqueue_pyramid(s, rec=rec)
         self.enqueue_detect(s, rec=rec)
+        with rec("gradients", -1, -1):
+            self.enqueue_gradients(s)
         with rec("orient", -1, -1):
             self.enqueue_orient(s)
         with rec("descriptor", -1, -1):

@@ -24,11 +24,12 @@ for exact in (False, True):
     ex = Extractor(dims, vk.PipelineConfig(descriptor=a.descriptor), batch=a.batch, input=dev, exact_only=exact)
     st = torch.cuda.current_stream()
     s = st.cuda_stream
-    times = {k: [] for k in ("pyramid", "detect", "orient", "describe")}
+    times = {k: [] for k in ("pyramid", "detect", "gradients", "orient", "describe")}
     for _ in range(a.reps):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         ev[0].record(st); ex.enqueue_pyramid(s); ev[1].record(st); ex.enqueue_detect(s); ev[2].record(st)
-        ex.enqueue_orient(s); ev[3].record(st); ex.enqueue_describe(s); ev[4].record(st)
+        ex.enqueue_gradients(s); ev[3].record(st)
+        ex.enqueue_orient(s); ev[4].record(st); ex.enqueue_describe(s); ev[5].record(st)
         torch.cuda.synchronize()
         for k, e0, e1 in zip(times, ev[:-1], ev[1:]):
             times[k].append(e0.elapsed_time(e1))
