@@ -236,6 +236,13 @@ int vk_describe_patch(int kind, const vk_frame* frames, const double* rot, const
 int vk_match(int metric, const void* a, int na, const void* b, int nb_rows, int dim,
              double ratio_max, int* best, double* d1, double* d2, uint8_t* keep, void* stream);
 
+/* Database matching (SURVEY.md §8(d) configs[4]): as vk_match against the
+ * reference rows with [ex_lo, ex_hi) removed (the query subject's own rows);
+ * reported indices are into the remaining rows (concat of the other subjects). */
+int vk_match_excluding(int metric, const void* a, int na, const void* b, int nb_rows, int dim,
+                       double ratio_max, int ex_lo, int ex_hi, int* best, double* d1, double* d2,
+                       uint8_t* keep, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

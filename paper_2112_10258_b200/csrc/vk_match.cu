@@ -44,7 +44,7 @@ VK_D void consider(Best& b, long long d, int j) {
 template <int METRIC>
 __global__ void __launch_bounds__(kMatchThreads)
 match_int_kernel(const uint8_t* __restrict__ a, int na, const uint8_t* __restrict__ b, int nbr, int dim, int slice,
-                 long long* __restrict__ pm1, long long* __restrict__ pm2, int* __restrict__ pi1) {
+                 long long* __restrict__ pm1, long long* __restrict__ pm2, int* __restrict__ pi1, int ex_lo, int ex_hi) {
     extern __shared__ uint4 tile4[];
     uint8_t* tile = reinterpret_cast<uint8_t*>(tile4);
     __shared__ long long nrm[kTileRows];
@@ -89,7 +89,9 @@ match_int_kernel(const uint8_t* __restrict__ a, int na, const uint8_t* __restric
                     for (int w = 0; w < words; ++w) dot = __dp4a((int)__ldg(arow + w), (int)brow[w], dot);
                     d = na2 + nrm[r] - 2ll * dot;
                 }
-                consider(best, d, t + r);
+                const int jj = t + r;
+                if (jj < ex_lo) consider(best, d, jj);
+                else if (jj >= ex_hi) consider(best, d, jj - (ex_hi - ex_lo));
             }
         }
     }
@@ -104,7 +106,7 @@ match_int_kernel(const uint8_t* __restrict__ a, int na, const uint8_t* __restric
 // fp64 descriptors: d2 = |a|^2 + |b|^2 - 2 a.b evaluated in fp64.
 __global__ void __launch_bounds__(kMatchThreads)
 match_f64_kernel(const double* __restrict__ a, int na, const double* __restrict__ b, int nbr, int dim, int slice,
-                 double* __restrict__ pm1, double* __restrict__ pm2, int* __restrict__ pi1) {
+                 double* __restrict__ pm1, double* __restrict__ pm2, int* __restrict__ pi1, int ex_lo, int ex_hi) {
     const int q = blockIdx.x * kMatchThreads + threadIdx.x;
     if (q >= na) return;
     const int j0 = blockIdx.y * slice, j1 = min(nbr, j0 + slice);
@@ -114,6 +116,7 @@ match_f64_kernel(const double* __restrict__ a, int na, const double* __restrict_
     double m1 = INFINITY, m2 = INFINITY;
     int i1 = -1;
     for (int j = j0; j < j1; ++j) {
+        if (j >= ex_lo && j < ex_hi) continue;
         const double* br = b + (long long)j * dim;
         double nb2 = 0.0, dot = 0.0;
         for (int k = 0; k < dim; ++k) {
@@ -121,7 +124,8 @@ match_f64_kernel(const double* __restrict__ a, int na, const double* __restrict_
             dot = dadd(dot, dmul(ar[k], br[k]));
         }
         const double d2 = fmax(dsub(dadd(na2, nb2), dmul(2.0, dot)), 0.0);
-        if (d2 < m1) { m2 = m1; m1 = d2; i1 = j; }
+        const int jo = j < ex_lo ? j : j - (ex_hi - ex_lo);
+        if (d2 < m1) { m2 = m1; m1 = d2; i1 = jo; }
         else if (d2 < m2) m2 = d2;
     }
     const long long o = (long long)blockIdx.y * na + q;
@@ -168,10 +172,13 @@ __global__ void match_merge_kernel(const T* __restrict__ pm1, const T* __restric
 
 using namespace vk;
 
-extern "C" int vk_match(int metric, const void* a, int na, const void* b, int nb_rows, int dim, double ratio_max,
-                        int* best, double* d1, double* d2, uint8_t* keep, void* stream) {
-    if (metric < 0 || metric > 2 || !a || !b || na < 0 || nb_rows < 2 || dim < 1 || !best || !d1 || !d2 || !keep ||
-        !(ratio_max > 0.0 && ratio_max <= 1.0) || (metric == 0 && dim % 8) || (metric == 1 && dim % 4)) {
+extern "C" int vk_match_excluding(int metric, const void* a, int na, const void* b, int nb_rows, int dim,
+                                  double ratio_max, int ex_lo, int ex_hi, int* best, double* d1, double* d2,
+                                  uint8_t* keep, void* stream) {
+    if (ex_lo < 0 || ex_hi < ex_lo || ex_hi > nb_rows) ex_lo = ex_hi = 0;
+    if (metric < 0 || metric > 2 || !a || !b || na < 0 || nb_rows - (ex_hi - ex_lo) < 2 || dim < 1 || !best || !d1 ||
+        !d2 || !keep || !(ratio_max > 0.0 && ratio_max <= 1.0) || (metric == 0 && dim % 8) ||
+        (metric == 1 && dim % 4)) {
         set_error("vk_match: bad arguments (metric=%d na=%d nb=%d dim=%d)", metric, na, nb_rows, dim);
         return VK_ERR_PARAMETER;
     }
@@ -200,7 +207,7 @@ extern "C" int vk_match(int metric, const void* a, int na, const void* b, int nb
         double* pm2 = pm1 + part;
         int* pi1 = reinterpret_cast<int*>(pm2 + part);
         match_f64_kernel<<<grid, kMatchThreads, 0, st>>>(static_cast<const double*>(a), na, static_cast<const double*>(b),
-                                                         nb_rows, dim, slice, pm1, pm2, pi1);
+                                                         nb_rows, dim, slice, pm1, pm2, pi1, ex_lo, ex_hi);
         count_launch();
         match_merge_kernel<double><<<(na + 255) / 256, 256, 0, st>>>(pm1, pm2, pi1, na, slices, metric, ratio_max, best,
                                                                      d1, d2, keep);
@@ -213,11 +220,11 @@ extern "C" int vk_match(int metric, const void* a, int na, const void* b, int nb
         if (metric == 0)
             match_int_kernel<0><<<grid, kMatchThreads, smem, st>>>(static_cast<const uint8_t*>(a), na,
                                                                    static_cast<const uint8_t*>(b), nb_rows, dim, slice,
-                                                                   pm1, pm2, pi1);
+                                                                   pm1, pm2, pi1, ex_lo, ex_hi);
         else
             match_int_kernel<1><<<grid, kMatchThreads, smem, st>>>(static_cast<const uint8_t*>(a), na,
                                                                    static_cast<const uint8_t*>(b), nb_rows, dim, slice,
-                                                                   pm1, pm2, pi1);
+                                                                   pm1, pm2, pi1, ex_lo, ex_hi);
         count_launch();
         match_merge_kernel<long long><<<(na + 255) / 256, 256, 0, st>>>(pm1, pm2, pi1, na, slices, metric, ratio_max,
                                                                         best, d1, d2, keep);
@@ -225,4 +232,9 @@ extern "C" int vk_match(int metric, const void* a, int na, const void* b, int nb
     }
     cudaFreeAsync(scratch, st);
     return cuda_status(cudaGetLastError(), "match launch");
+}
+
+extern "C" int vk_match(int metric, const void* a, int na, const void* b, int nb_rows, int dim, double ratio_max,
+                        int* best, double* d1, double* d2, uint8_t* keep, void* stream) {
+    return vk_match_excluding(metric, a, na, b, nb_rows, dim, ratio_max, 0, 0, best, d1, d2, keep, stream);
 }

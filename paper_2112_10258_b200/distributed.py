@@ -1,0 +1,105 @@
+"""Multi-GPU plumbing: one process per GPU over torch.distributed.
+
+Detect + describe needs no exchange (independent volumes):
+ranks take contiguous shards of the volume / subject list (`shard_range`).
+Database matching (configs[4]) has exactly one exchange: the descriptor
+tables of all ranks are all-gathered (NCCL over NVLink on GPUs, gloo in the CPU
+tests) into one database, then every rank matches its own subjects against
+it, excluding each query subject's own rows -- the composition
+``nearest_neighbor_matches(desc_i, concat_{j != i} desc_j)`` of the reference
+API (match.py:81-121) for every subject i.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .errors import ParameterError
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous shard [lo, hi) of range(n) for `rank` (sizes differ by <= 1)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ParameterError(f"bad rank {rank} / world {world}")
+    return n * rank // world, n * (rank + 1) // world
+
+
+def gather_rows(local, group=None):
+    """All-gather a (n_local, ...) tensor with per-rank n_local; returns the
+    concatenation in rank order (same tensor on every rank) and the counts."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    n = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    counts = [int(s.item()) for s in sizes]
+    m = max(counts) if counts else 0
+    pad = torch.zeros((m,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)]), counts
+
+
+def gather_database(desc, subjects, group=None):
+    """All-gather descriptor rows and their subject ids.  Each rank must hold
+    whole subjects, sorted by id, and ranks must hold increasing id ranges, so
+    the database is in subject-id order.  Returns (db, subject_of_row,
+    {subject: (lo, hi)})."""
+    db, _ = gather_rows(desc, group)
+    subj, _ = gather_rows(subjects.to(desc.device) if hasattr(subjects, "to") else subjects, group)
+    s = subj.cpu().numpy()
+    if len(s) and np.any(np.diff(s) < 0):
+        raise ParameterError("database rows are not grouped by increasing subject id across ranks")
+    ranges = {}
+    if len(s):
+        cuts = np.flatnonzero(np.diff(s)) + 1
+        starts = np.concatenate([[0], cuts])
+        ends = np.concatenate([cuts, [len(s)]])
+        for a, b in zip(starts, ends):
+            ranges[int(s[a])] = (int(a), int(b))
+    return db, subj, ranges
+
+
+def match_database(local: dict, ratio_max: float = 0.9, metric: str = "euclidean", group=None) -> dict:
+    """{subject: descriptor array} for this rank's subjects -> {subject:
+    (best_index, d1, d2, keep)} against all other subjects' descriptors (indices
+    into concat of the other subjects in id order).  Rank descriptors (int,
+    values in [-128, 127]) travel as int8; packed BRIEF bits as uint8."""
+    t = _lib.torch()
+    ids = sorted(local)
+    if metric not in ("hamming", "euclidean"):
+        raise ParameterError(f"unknown metric {metric!r}")
+    arrs = [np.asarray(local[i]) for i in ids]
+    if metric == "hamming":
+        rows = np.concatenate([a.astype(np.uint8) for a in arrs]) if arrs else np.zeros((0, 8), np.uint8)
+        pad = (-rows.shape[1]) % 8
+        code = 0
+    else:
+        rows = np.concatenate([a.astype(np.int8) for a in arrs]) if arrs else np.zeros((0, 64), np.int8)
+        pad = (-rows.shape[1]) % 4
+        code = 1
+    rows = np.pad(rows, ((0, 0), (0, pad)))
+    subj = np.concatenate([np.full(len(a), i, np.int32) for i, a in zip(ids, arrs)]) if arrs else np.zeros(0, np.int32)
+    d_rows = t.from_numpy(np.ascontiguousarray(rows)).cuda()
+    db, _, ranges = gather_database(d_rows, t.from_numpy(subj).cuda(), group)
+    out = {}
+    off = 0
+    for i, a in zip(ids, arrs):
+        q = d_rows[off: off + len(a)]
+        off += len(a)
+        lo, hi = ranges[i]
+        n = len(a)
+        best = t.empty(max(n, 1), dtype=t.int32, device="cuda")
+        d1 = t.empty(max(n, 1), dtype=t.float64, device="cuda")
+        d2 = t.empty(max(n, 1), dtype=t.float64, device="cuda")
+        keep = t.empty(max(n, 1), dtype=t.uint8, device="cuda")
+        if n:
+            _lib.call("vk_match_excluding", code, q.data_ptr(), n, db.data_ptr(), db.shape[0], db.shape[1],
+                      float(ratio_max), lo, hi, best.data_ptr(), d1.data_ptr(), d2.data_ptr(), keep.data_ptr(),
+                      _lib.stream_ptr())
+        out[i] = (best[:n].cpu().numpy(), d1[:n].cpu().numpy(), d2[:n].cpu().numpy(), keep[:n].cpu().numpy())
+    return out

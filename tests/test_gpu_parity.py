@@ -300,3 +300,35 @@ def test_fast_path_adversarial(kind):
             assert np.array_equal(a["desc"].astype(np.int64), O.desc_array(want["records"], kind).astype(np.int64))
         n_desc.append(len(want["records"]))
     assert sum(n_desc) > 20
+
+
+def test_database_matching_single_rank():
+    """configs[4] composition on one rank: match_database == per-subject
+    nearest_neighbor_matches(desc_i, concat_{j != i} desc_j) of the oracle."""
+    import torch.distributed as dist
+
+    from oracle import volkey_oracle as O
+    from paper_2112_10258_b200.distributed import match_database
+
+    rng = np.random.default_rng(5)
+    subjects = {i: np.stack([rng.permutation(64) for _ in range(int(rng.integers(20, 60)))]) for i in range(5)}
+    if not dist.is_initialized():
+        import os
+        import socket
+
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        got = match_database(subjects, 0.9, "euclidean")
+    finally:
+        dist.destroy_process_group()
+    for i, a in subjects.items():
+        others = np.concatenate([subjects[j] for j in sorted(subjects) if j != i])
+        ref = O.nn_match(a, others, 0.9, "euclidean")
+        best, d1, d2, keep = got[i]
+        mine = [(q, int(best[q]), float(d1[q]), float(d2[q])) for q in np.flatnonzero(keep)]
+        assert mine == ref, f"subject {i}"
