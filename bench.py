@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=16, help="volumes per GPU per step")
+    ap.add_argument("--batch", type=int, default=24, help="volumes per GPU per step")
+    ap.add_argument("--streams", type=int, default=2, help="parallel sub-batches (streams) per GPU")
     ap.add_argument("--slots", type=int, default=2, help="distinct input batches cycled over steps")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--descriptor", default="siftrank", choices=("siftrank", "brief", "rrief"))
@@ -128,6 +129,31 @@ def pyramid_bytes(plan) -> int:
     return total
 
 
+def ncu_pyramid_traffic(batch: int):
+    """DRAM bytes (read + write) of all blur3d launches of one step, from the
+    committed ncu capture (profiles/*/pyramid_dram.csv, batch noted in its
+    companion log), scaled to `batch` volumes; (bytes, source) or (None, None)."""
+    import csv
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(REPO, "profiles", "r*", "pyramid_dram.csv")))
+    if not paths:
+        return None, None
+    path = paths[-1]
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r]
+    if not hi:
+        return None, None
+    h = rows[hi[0]]
+    ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    tot = 0.0
+    for r in rows[hi[0] + 1:]:
+        if len(r) > vi and "blur3d" in r[ki] and r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(r[vi].replace(",", ""))
+    captured_batch = 16  # scripts/gpu_bench_full.sh profiles profile_step.py --batch 16
+    return tot * batch / captured_batch, os.path.relpath(path, REPO)
+
+
 def detect_bytes(plan) -> int:
     """Detection reads each of the L-1 DoG levels once per octave."""
     L = plan.cfg.levels_per_octave
@@ -201,23 +227,33 @@ def run_ours(a):
     del tmp
     pinned = torch.from_numpy(np.ascontiguousarray(host.transpose(0, 3, 2, 1))).pin_memory()  # x-fastest host copy
     del host
-    # ---- one extractor per slot (its input buffer is the resident slot)
-    exs = []
-    for s in range(S):
-        exs.append(Extractor(DIMS, cfg, batch=B, input=dev_in[s * B:(s + 1) * B]))
+    # ---- one extractor group per slot: G parallel-stream sub-batches reading the resident slot
+    from paper_2112_10258_b200.engine import ExtractorGroup
+
+    G = max(1, min(a.streams, B))
+    subs = [B * g // G for g in range(G + 1)]
+    groups = []
+    for s_ in range(S):
+        members = []
+        for g in range(G):
+            lo, hi = s_ * B + subs[g], s_ * B + subs[g + 1]
+            members.append(Extractor(DIMS, cfg, batch=hi - lo, input=dev_in[lo:hi]))
+        groups.append(ExtractorGroup(members))
     # capacity check on a first eager run, grow buffers if needed
-    for i, ex in enumerate(exs):
-        ex.enqueue()
-        c = ex.check_capacity()
-        if c["overflow"]:
-            ex2 = Extractor(DIMS, cfg, batch=B, kp_cap=2 * c["keypoints"] + 1024, frame_cap=2 * c["frames"] + 1024,
-                            input=ex.input)
-            exs[i] = ex2
-            ex2.enqueue()
+    for grp in groups:
+        for i, ex in enumerate(grp.members):
+            ex.enqueue()
+            c = ex.check_capacity()
+            if c["overflow"]:
+                ex2 = Extractor(DIMS, cfg, batch=ex.B, kp_cap=2 * c["keypoints"] + 1024,
+                                frame_cap=2 * c["frames"] + 1024, input=ex.input)
+                grp.members[i] = ex2
+                ex2.enqueue()
     torch.cuda.synchronize()
-    counts = exs[0].counts()
+    exs = [grp.members[0] for grp in groups]
+    counts = {k: sum(m.counts()[k] for m in groups[0].members) for k in ("keypoints", "frames")}
     launches0 = _lib.load().vk_launch_count()
-    exs[0].enqueue()
+    groups[0].enqueue()
     torch.cuda.synchronize()
     launches_per_step = _lib.load().vk_launch_count() - launches0
     # ---- per-stage device times (eager, events on the pipeline stream)
@@ -245,11 +281,11 @@ def run_ours(a):
     # ---- graphs
     use_graph = not a.no_graph
     if use_graph:
-        for ex in exs:
-            ex.capture()
+        for grp in groups:
+            grp.capture()
     # ---- warmup + timed region
     for w in range(a.warmup):
-        exs[w % S].run()
+        groups[w % S].run()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -260,7 +296,7 @@ def run_ours(a):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for k in range(a.steps):
-        exs[k % S].run()
+        groups[k % S].run()
     e1.record(st)
     torch.cuda.synchronize()
     clk = clocks.stop()
@@ -275,18 +311,18 @@ def run_ours(a):
     # ---- end to end through the public API: pinned host -> HBM -> results -> host
     e2e = None
     if not a.no_e2e:
-        ex = exs[0]
-        res_host = {}
+        grp = groups[0]
         h2d = B * int(np.prod(DIMS)) * 4
         d2h_tot = 0
 
         def one_step(slot):
             nonlocal d2h_tot
-            ex.input.copy_(pinned[slot * B:(slot + 1) * B], non_blocking=True)
-            ex.run()
-            r = ex.results()   # reads counts, then copies exactly the produced SoA
-            d2h_tot += 16 + sum(v.nbytes for v in r.values() if isinstance(v, np.ndarray))
-            res_host["last"] = r
+            for g, m in enumerate(grp.members):   # H2D of this step's volumes into the group's input slot
+                m.input.copy_(pinned[slot * B + subs[g]: slot * B + subs[g + 1]], non_blocking=True)
+            grp.run()
+            for m in grp.members:   # counts, then exactly the produced SoA to host
+                r = m.results()
+                d2h_tot += 16 + sum(v.nbytes for v in r.values() if isinstance(v, np.ndarray))
 
         for w in range(max(1, a.warmup)):
             one_step(w % S)
@@ -305,27 +341,28 @@ def run_ours(a):
             t = torch.tensor([ems], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        # restore the resident slot-0 input for any later use
-        ex.input.copy_(dev_in[:B])
         e2e = {"value": world * B * a.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(d2h_tot / a.steps), "ms_per_step": ems / a.steps,
-               "path": "Extractor.run(pinned x-fastest host batch) + Extractor.results() (SoA to host)"}
+               "path": "ExtractorGroup.run() on a pinned x-fastest host batch copied in + Extractor.results() (SoA to host)"}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
     plan = exs[0].plan
+    Bs = exs[0].B  # stage timings / roofline are measured on one sub-batch
     with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
         peaks = json.load(fh)
-    pbytes = pyramid_bytes(plan) * B
+    pbytes = pyramid_bytes(plan) * Bs
     achieved = pbytes / (stage_ms["pyramid"] / 1e3) / 1e9
+    traffic, tsrc = ncu_pyramid_traffic(Bs)
     roofline = {"bound": "hbm", "kernel": "blur3d_ring_kernel (fused blur + DoG + subsample), all pyramid launches",
                 "achieved": round(achieved, 1), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": round(achieved / peaks["hbm_gbs"], 4) if peaks.get("hbm_gbs") else None,
-                "traffic": None, "algorithmic_bytes_per_step": pbytes,
+                "traffic": round(traffic) if traffic else None, "traffic_source": tsrc,
+                "algorithmic_bytes": pbytes,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"}
-    det_gbs = detect_bytes(plan) * B / (stage_ms["detect"] / 1e3) / 1e9
+    det_gbs = detect_bytes(plan) * Bs / (stage_ms["detect"] / 1e3) / 1e9
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
@@ -335,11 +372,13 @@ def run_ours(a):
                                f"describe ({a.descriptor}), defaults of PipelineConfig",
                    "volume": list(DIMS), "batch_per_gpu": B, "descriptor": a.descriptor,
                    "l2_policy": f"inputs larger than L2: {S} resident input slots x {B} volumes x 14.6 MB cycled",
+                   "streams_per_gpu": G, "stage_timing_subbatch": Bs,
                    "cuda_graph": use_graph, "parallelism": f"dp{world} (independent volumes, no collective)"},
         "roofline": roofline,
         "stages_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
         "detect_gbs": round(det_gbs, 1),
         "keypoints_per_volume": counts["keypoints"] / B, "frames_per_volume": counts["frames"] / B,
+        "roofline_note": "pyramid stage measured eagerly on one sub-batch of stage_timing_subbatch volumes",
         "gpu_launches": int(launches_per_step * a.steps),
         "clocks": clk,
     }

@@ -384,3 +384,50 @@ class Extractor:
             frame_sec=fr["sec"].copy(), rot=self.rot[: 9 * m].cpu().numpy().reshape(m, 3, 3),
             desc=self.desc[:m].cpu().numpy(),
         )
+
+
+class ExtractorGroup:
+    """Several Extractors (sub-batches) whose pipelines run on parallel streams
+    inside one CUDA graph: the tails and the latency-bound small-octave /
+    bookkeeping launches of one sub-batch overlap the bulk work of the others."""
+
+    def __init__(self, extractors: list):
+        if not extractors:
+            raise ParameterError("ExtractorGroup needs at least one Extractor")
+        self.members = list(extractors)
+        self.graph = None
+
+    @property
+    def B(self) -> int:
+        return sum(e.B for e in self.members)
+
+    def enqueue(self, stream=None) -> None:
+        t = _lib.torch()
+        main = stream if stream is not None else t.cuda.current_stream()
+        subs = [t.cuda.Stream() for _ in self.members]
+        for sub, ex in zip(subs, self.members):
+            sub.wait_stream(main)
+            with t.cuda.stream(sub):
+                ex.enqueue(sub)
+        for sub in subs:
+            main.wait_stream(sub)
+
+    def run(self) -> None:
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.enqueue()
+
+    def capture(self) -> None:
+        t = _lib.torch()
+        s = t.cuda.Stream()
+        s.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(s):
+            self.enqueue(s)
+        t.cuda.current_stream().wait_stream(s)
+        t.cuda.synchronize()
+        g = t.cuda.CUDAGraph()
+        with t.cuda.graph(g, stream=s):
+            self.enqueue(s)
+        t.cuda.synchronize()
+        self.graph = g
