@@ -122,6 +122,17 @@ int vk_transpose_xfast_to_zfast(const float* src, float* dst, int nb, int nx, in
 int vk_blur3d(const float* src, float* dst, float* dog_out, float* half_out,
               int nb, int nx, int ny, int nz, const float* taps_host, int radius, void* stream);
 
+/* The tail of the pyramid in one launch (scalespace.py:186-251 for octaves
+ * whose levels hold <= 16384 voxels): one CTA per volume runs every level of
+ * octaves 0..n_oct-1 of this call in shared memory.  dims_host: 3 per octave;
+ * level_ptrs_host / dog_ptrs_host: n_oct*levels batched device pointers
+ * (level 0 of the first octave must already be filled; level 0 of the next
+ * octaves is written by the handoff subsample); radius_host[i] / taps_host
+ * [i*VK_MAX_TAPS ...]: blur of level i (i >= 1). */
+int vk_small_octaves(int n_oct, int levels, int handoff, const int* dims_host, float* const* level_ptrs_host,
+                     float* const* dog_ptrs_host, const int* radius_host, const float* taps_host, int nb,
+                     void* stream);
+
 /* subsample_half (scalespace.py:123-137): floor dims, ordered 8-sum, /8. */
 int vk_subsample_half(const float* src, float* dst, int nb, int nx, int ny, int nz, void* stream);
 

@@ -36,6 +36,7 @@ SIGNATURES = {
     "vk_transpose_xfast_to_zfast": [P, P, I, I, I, I, P],
     "vk_blur3d": [P, P, P, P, I, I, I, I, P, I, P],
     "vk_subsample_half": [P, P, I, I, I, I, P],
+    "vk_small_octaves": [I, I, I, P, P, P, P, P, I, P],
     "vk_difference": [P, P, P, LL, P],
     "vk_sum_of_signs": [P, P, P, P, I, I, I, I, P],
     "vk_detect_octave": [P, I, I, I, I, I, I, I, F, P, P, I, P],

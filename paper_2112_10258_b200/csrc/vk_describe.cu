@@ -67,36 +67,45 @@ __device__ __noinline__ int sr_bin_exact(int ox, int oy, int oz, double x64, dou
     return 8 * ((r0 > 0.0) + 2 * (r1 > 0.0) + 4 * (r2 > 0.0)) + (g0 > 0.0) + 2 * (g1 > 0.0) + 4 * (g2 > 0.0);
 }
 
-// Rare path when only the fp32 gradient is at hand: reload the neighbours.
-__device__ __noinline__ int sr_bin_exact_reload(int ox, int oy, int oz, const float* data, int nx, int ny, int nz,
-                                                int x, int y, int z, const double* R) {
+// Rare path: reference fp64 octant bits of the rotated gradient (reloads the
+// neighbours: only the fp32 gradient is at hand).
+__device__ __noinline__ int sr_gbits_exact(const float* data, int nx, int ny, int nz, int x, int y, int z,
+                                           const double* R) {
     const Nb6 n = load_nb6(data, nx, ny, nz, x, y, z);
     double x64, y64, z64;
     grad64(n, x64, y64, z64);
-    return sr_bin_exact(ox, oy, oz, x64, y64, z64, R);
+    const double g0 = dot3_blas(x64, y64, z64, R[0], R[3], R[6]);
+    const double g1 = dot3_blas(x64, y64, z64, R[1], R[4], R[7]);
+    const double g2 = dot3_blas(x64, y64, z64, R[2], R[5], R[8]);
+    return (g0 > 0.0) + 2 * (g1 > 0.0) + 4 * (g2 > 0.0);
 }
 
-// Fast SIFT-Rank bin of one voxel for one frame: octant bits decided in fp32
-// whenever each rotated component clears its error bound (<= ~5 u32 of the L1
-// norm; bound 1e-6), otherwise recomputed with the reference's fp64 FMA chain.
+// Fast SIFT-Rank bin of one voxel for one frame.  Each octant bit is taken
+// from the fp32 rotated component when it clears its error bound (<= ~5 u32 of
+// the L1 norm; bound 1e-6), otherwise from the reference's fp64 FMA chain:
+// offset components need only the integer offset and R (offsets on lines /
+// planes through the centre give exact zeros for axes with zero coordinates),
+// gradient components need the exact fp64 gradient (rare).
 VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const double* R, const float* Rf,
                      const float* data, int nx, int ny, int nz, int x, int y, int z) {
     const float fx = (float)ox, fy = (float)oy, fz = (float)oz;
     const float eo = 1.0e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
     const float eg = 1.0e-6f * (fabsf(gx) + fabsf(gy) + fabsf(gz)) + 1.0e-40f;
-    float r[3], g[3];
+    int sp = 0, og = 0;
+    bool gsure = true;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        r[j] = fmaf(fz, Rf[6 + j], fmaf(fy, Rf[3 + j], fx * Rf[j]));
-        g[j] = fmaf(gz, Rf[6 + j], fmaf(gy, Rf[3 + j], gx * Rf[j]));
+        const float r = fmaf(fz, Rf[6 + j], fmaf(fy, Rf[3 + j], fx * Rf[j]));
+        const float g = fmaf(gz, Rf[6 + j], fmaf(gy, Rf[3 + j], gx * Rf[j]));
+        bool rb;
+        if (fabsf(r) > eo) rb = r > 0.f;
+        else rb = dot3_blas((double)ox, (double)oy, (double)oz, R[j], R[3 + j], R[6 + j]) > 0.0;
+        sp |= (int)rb << j;
+        og |= (int)(g > 0.f) << j;
+        gsure = gsure && fabsf(g) > eg;
     }
-    const bool zero_off = (ox | oy | oz) == 0;  // rotated zero offset is exactly 0: spatial octant 0
-    const bool sure = (zero_off || (fabsf(r[0]) > eo && fabsf(r[1]) > eo && fabsf(r[2]) > eo)) &&
-                      fabsf(g[0]) > eg && fabsf(g[1]) > eg && fabsf(g[2]) > eg;
-    if (sure)
-        return 8 * ((r[0] > 0.f) + 2 * (r[1] > 0.f) + 4 * (r[2] > 0.f)) + (g[0] > 0.f) + 2 * (g[1] > 0.f) +
-               4 * (g[2] > 0.f);
-    return sr_bin_exact_reload(ox, oy, oz, data, nx, ny, nz, x, y, z, R);
+    if (!gsure) og = sr_gbits_exact(data, nx, ny, nz, x, y, z, R);
+    return 8 * sp + og;
 }
 
 // Fast walk of one keypoint's ball for NF frames (rotations in registers);
@@ -158,6 +167,47 @@ VK_D int stable_rank(const double* w, int n, int b) {
     int r = 0;
     for (int j = 0; j < n; ++j) r += (w[j] < wb) || (w[j] == wb && j < b);
     return r;
+}
+
+// Exact reference order for one frame (out of line: keeps its fp64 register
+// footprint out of the fast loop): chunked exact votes by all threads, then
+// warp 0 adds them bin by bin in ball order (np.add.at).  Writes w[64].
+__device__ __noinline__ void sr_exact_frame(const float* data, const vk_level& L, const vk_kp& kp, const vk_ball& ball,
+                                            const int* __restrict__ ball_offsets, const double* Rsm, double* w,
+                                            int* xb, double* xv) {
+    const int tid = threadIdx.x;
+    double R[9];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) R[e] = Rsm[e];
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int base = 0; base < ball.count; base += blockDim.x) {
+        const int j = base + tid;
+        double mg = 0.0;
+        bool inside;
+        int bin = -1;
+        if (j < ball.count)
+            bin = sr_vote(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz, __ldg(ball_offsets + ball.start + j), R, mg,
+                          inside);
+        xb[tid] = bin;
+        xv[tid] = mg;
+        __syncthreads();
+        if (tid < 32) {
+            const int m = min((int)blockDim.x, ball.count - base);
+#pragma unroll 8
+            for (int q = 0; q < m; ++q) {
+                const int bs = xb[q];
+                const double vs = xv[q];
+                if (bs == tid) acc0 = dadd(acc0, vs);
+                else if (bs == tid + 32) acc1 = dadd(acc1, vs);
+            }
+        }
+        __syncthreads();
+    }
+    if (tid < 32) {
+        w[tid] = acc0;
+        w[tid + 32] = acc1;
+    }
+    __syncthreads();
 }
 
 // One CTA per work item = one keypoint and its F frames (contiguous in the
@@ -258,39 +308,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                 if (go_exact && tid == 0 && stats) atomicAdd(stats, 1);  // fallback counter (diagnostics)
             }
             if (go_exact) {
-                // Exact reference order: chunked exact votes, warp 0 adds in ball order.
-                double R[9];
-#pragma unroll
-                for (int e = 0; e < 9; ++e) R[e] = Rs[9 * f + e];
-                double acc0 = 0.0, acc1 = 0.0;
-                for (int base = 0; base < ball.count; base += kSrThreads) {
-                    const int j = base + tid;
-                    double mg = 0.0;
-                    bool inside;
-                    int bin = -1;
-                    if (j < ball.count)
-                        bin = sr_vote(data, L.nx, L.ny, L.nz, kp.ix, kp.iy, kp.iz, __ldg(ball_offsets + ball.start + j), R,
-                                      mg, inside);
-                    xb[tid] = bin;
-                    xv[tid] = mg;
-                    __syncthreads();
-                    if (tid < 32) {
-                        const int m = min(kSrThreads, ball.count - base);
-#pragma unroll 8
-                        for (int q = 0; q < m; ++q) {
-                            const int bs = xb[q];
-                            const double vs = xv[q];
-                            if (bs == tid) acc0 = dadd(acc0, vs);
-                            else if (bs == tid + 32) acc1 = dadd(acc1, vs);
-                        }
-                    }
-                    __syncthreads();
-                }
-                if (tid < 32) {
-                    w[tid] = acc0;
-                    w[tid + 32] = acc1;
-                }
-                __syncthreads();
+                sr_exact_frame(data, L, kp, ball, ball_offsets, Rs + 9 * f, w, xb, xv);
                 if (tid < kSrBins) myrank = stable_rank(w, kSrBins, tid);
                 __syncthreads();
             }

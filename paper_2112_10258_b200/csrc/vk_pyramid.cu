@@ -226,6 +226,100 @@ blur3d_ring_kernel(const float* __restrict__ src, float* __restrict__ dst, float
 }
 
 // ---------------------------------------------------------------------------
+// Small octaves in one launch.  Once a level fits in shared memory three times
+// over, one CTA per volume runs every remaining octave there: each blur is
+// three out-of-place 1-D passes (same arithmetic as above: fp32 products
+// added in tap order, replicate borders, x then y then z), the DoG and the
+// handoff subsample are written as the levels are produced, and the next
+// octave starts from the subsampled level.  Removes ~5 latency-bound launches
+// per small octave.
+constexpr int kSmallMaxVox = 16384;  // 3 buffers x 64 KB
+constexpr int kSmallMaxOct = 8;
+constexpr int kSmallMaxLev = 12;
+
+struct SmallOctaves {
+    int n_oct, levels, handoff;
+    int dims[kSmallMaxOct][3];
+    float* lv[kSmallMaxOct][kSmallMaxLev];    // batched level tensors
+    float* dog[kSmallMaxOct][kSmallMaxLev];   // batched DoG tensors
+    int radius[kSmallMaxLev];                 // blur radius of level i (i >= 1)
+    float taps[kSmallMaxLev][VK_MAX_TAPS];
+};
+
+VK_D void small_pass(const float* __restrict__ in, float* __restrict__ out, int nx, int ny, int nz, int axis, int R,
+                     const float* w) {
+    const int n = nx * ny * nz;
+    const int st = axis == 0 ? 1 : (axis == 1 ? nx : nx * ny);
+    const int len = axis == 0 ? nx : (axis == 1 ? ny : nz);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int c = axis == 0 ? i % nx : (axis == 1 ? (i / nx) % ny : i / (nx * ny));
+        const float* base = in + (i - c * st);
+        float acc = fmul(w[0], base[clampi(c - R, 0, len - 1) * st]);
+        for (int t = 1; t <= 2 * R; ++t) acc = fadd(acc, fmul(w[t], base[clampi(c - R + t, 0, len - 1) * st]));
+        out[i] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(512)
+small_octaves_kernel(SmallOctaves so) {
+    extern __shared__ float4 sm4[];
+    float* A = reinterpret_cast<float*>(sm4);
+    float* Bf = A + kSmallMaxVox;
+    float* C = Bf + kSmallMaxVox;
+    const int b = blockIdx.x;
+    for (int o = 0; o < so.n_oct; ++o) {
+        const int nx = so.dims[o][0], ny = so.dims[o][1], nz = so.dims[o][2];
+        const int n = nx * ny * nz;
+        const long long vb = (long long)b * n;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) A[i] = so.lv[o][0][vb + i];
+        __syncthreads();
+        float* src = A;
+        float* xb = Bf;
+        float* yb = C;
+        for (int lvi = 1; lvi < so.levels; ++lvi) {
+            const int R = so.radius[lvi];
+            const float* w = so.taps[lvi];
+            small_pass(src, xb, nx, ny, nz, 0, R, w);
+            __syncthreads();
+            small_pass(xb, yb, nx, ny, nz, 1, R, w);
+            __syncthreads();
+            small_pass(yb, xb, nx, ny, nz, 2, R, w);  // xb now holds level lvi
+            __syncthreads();
+            float* lo = so.lv[o][lvi] + vb;
+            float* dg = so.dog[o][lvi - 1] + vb;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                lo[i] = xb[i];
+                dg[i] = __fsub_rn(src[i], xb[i]);
+            }
+            if (lvi == so.handoff && o + 1 < so.n_oct) {
+                const int hx = nx >> 1, hy = ny >> 1, hz = nz >> 1, hn = hx * hy * hz;
+                float* hdst = so.lv[o + 1][0] + (long long)b * hn;
+                for (int i = threadIdx.x; i < hn; i += blockDim.x) {
+                    const int x = i % hx, y = (i / hx) % hy, z = i / (hx * hy);
+                    auto at = [&](int dx, int dy, int dz) {
+                        return xb[((2 * z + dz) * ny + (2 * y + dy)) * nx + (2 * x + dx)];
+                    };
+                    float sm = at(0, 0, 0);
+                    sm = fadd(sm, at(0, 0, 1));
+                    sm = fadd(sm, at(0, 1, 0));
+                    sm = fadd(sm, at(0, 1, 1));
+                    sm = fadd(sm, at(1, 0, 0));
+                    sm = fadd(sm, at(1, 0, 1));
+                    sm = fadd(sm, at(1, 1, 0));
+                    sm = fadd(sm, at(1, 1, 1));
+                    hdst[i] = fmul(sm, 0.125f);
+                }
+            }
+            __syncthreads();
+            float* t = src;  // the new level becomes the source of the next blur
+            src = xb;
+            xb = t;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Generic fallback for radius > 10: three 1-D passes through global scratch.
 __global__ void blur_axis_kernel(const float* __restrict__ src, float* __restrict__ dst, int nx, int ny, int nz,
                                  long long total, int axis, int R, Taps taps) {
@@ -462,4 +556,46 @@ extern "C" int vk_transpose_xfast_to_zfast(const float* src, float* dst, int nb,
     transpose_xz_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(src, dst, nz, ny, nx);
     count_launch();
     return cuda_status(cudaGetLastError(), "transpose launch");
+}
+
+extern "C" int vk_small_octaves(int n_oct, int levels, int handoff, const int* dims_host, float* const* level_ptrs_host,
+                                float* const* dog_ptrs_host, const int* radius_host, const float* taps_host, int nb,
+                                void* stream) {
+    if (n_oct < 1 || n_oct > kSmallMaxOct || levels < 2 || levels > kSmallMaxLev || !dims_host || !level_ptrs_host ||
+        !dog_ptrs_host || !radius_host || !taps_host || nb < 0) {
+        set_error("vk_small_octaves: bad arguments (n_oct=%d levels=%d)", n_oct, levels);
+        return VK_ERR_PARAMETER;
+    }
+    SmallOctaves so{};
+    so.n_oct = n_oct;
+    so.levels = levels;
+    so.handoff = handoff;
+    for (int o = 0; o < n_oct; ++o) {
+        for (int a = 0; a < 3; ++a) so.dims[o][a] = dims_host[3 * o + a];
+        if ((long long)so.dims[o][0] * so.dims[o][1] * so.dims[o][2] > kSmallMaxVox) {
+            set_error("vk_small_octaves: octave %d has more than %d voxels", o, kSmallMaxVox);
+            return VK_ERR_PARAMETER;
+        }
+        for (int i = 0; i < levels; ++i) so.lv[o][i] = level_ptrs_host[o * levels + i];
+        for (int i = 0; i + 1 < levels; ++i) so.dog[o][i] = dog_ptrs_host[o * levels + i];
+    }
+    for (int i = 1; i < levels; ++i) {
+        so.radius[i] = radius_host[i];
+        if (so.radius[i] < 1 || 2 * so.radius[i] + 1 > VK_MAX_TAPS) {
+            set_error("vk_small_octaves: bad radius %d", so.radius[i]);
+            return VK_ERR_PARAMETER;
+        }
+        for (int t = 0; t < 2 * so.radius[i] + 1; ++t) so.taps[i][t] = taps_host[i * VK_MAX_TAPS + t];
+    }
+    if (nb == 0) return VK_OK;
+    const int smem = 3 * kSmallMaxVox * 4;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(small_octaves_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return cuda_status(e, "small octaves attribute");
+        configured = true;
+    }
+    small_octaves_kernel<<<nb, 512, smem, as_stream(stream)>>>(so);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "small octaves launch");
 }

@@ -190,6 +190,12 @@ class Extractor:
                 if i < L - 1:
                     dog_t[o * L + i] = self.dogs[o][i]
         self.level_table = _lib.to_device_records(level_records(lvl_t, dims_l))
+        # octaves from here on are small enough for the fused shared-memory kernel
+        self.small_from = self.plan.n_octaves
+        for o, d in enumerate(self.plan.octave_dims):
+            if o > 0 and int(np.prod(d)) <= 16384 and max(k.radius for k in self.plan.taps[1:]) <= 32:
+                self.small_from = o
+                break
         # dense gradient volumes of the keypoint levels (orientation / SIFT-Rank fast paths)
         self.grad_levels = []  # (octave, level, g4 tensor, bin tensor)
         grec = np.zeros(nseg, dtype=_lib.GRADLEVEL_DTYPE)
@@ -237,7 +243,10 @@ class Extractor:
         L, B, P = self.cfg.levels_per_octave, self.B, self.plan
         rec = rec or _no_stage
         handoff = L - 3
+        small = self.small_from if with_dog else P.n_octaves
         for o, (nx, ny, nz) in enumerate(P.octave_dims):
+            if o >= small:
+                break
             lv, dg = self.levels[o], self.dogs[o]
             if o == 0:
                 k = P.taps[0]
@@ -251,6 +260,22 @@ class Extractor:
                     _lib.call("vk_blur3d", lv[i - 1].data_ptr(), lv[i].data_ptr(),
                               dg[i - 1].data_ptr() if with_dog else None, half, B, nx, ny, nz,
                               k.weights.ctypes.data, k.radius, s)
+        if small < P.n_octaves:
+            import ctypes as C
+
+            n = P.n_octaves - small
+            dims = np.array(P.octave_dims[small:], dtype=np.int32).reshape(-1)
+            lp = (C.c_void_p * (n * L))(*[self.levels[o][i].data_ptr() for o in range(small, P.n_octaves)
+                                          for i in range(L)])
+            dp = (C.c_void_p * (n * L))(*[(self.dogs[o][i].data_ptr() if i < L - 1 else 0)
+                                          for o in range(small, P.n_octaves) for i in range(L)])
+            rad = np.array([0] + [k.radius for k in P.taps[1:]], dtype=np.int32)
+            taps = np.zeros((L, 65), dtype=np.float32)
+            for i in range(1, L):
+                taps[i, : 2 * P.taps[i].radius + 1] = P.taps[i].weights
+            with rec("convolution", small, -1):
+                _lib.call("vk_small_octaves", n, L, handoff, dims.ctypes.data, C.cast(lp, C.c_void_p),
+                          C.cast(dp, C.c_void_p), rad.ctypes.data, taps.ctypes.data, B, s)
 
     def enqueue_detect(self, s: int, rec=None) -> None:
         """detect_keypoints (detect.py:149-182) for the whole batch."""
