@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define VK_ABI_VERSION 1
+#define VK_ABI_VERSION 2
 
 #define VK_OK 0
 #define VK_ERR_PARAMETER 5 /* errors.py:32-36 ParameterError */
@@ -171,6 +171,11 @@ int vk_order_keypoints(const unsigned long long* cand_keys, const int* cand_coun
                        const vk_level* dog_levels, vk_kp* kps, double* pos, double* sigma, float* dog,
                        int8_t* sign, int* vol_offset, int* total, int kp_cap, void* stream);
 
+/* Bytes of device scratch vk_orient / vk_describe_siftrank need on `device`:
+ * one fp64 histogram slot per CTA of their persistent grids, which the fast
+ * paths reduce votes into (fp64 RED, L2-resident).  -1 if no such device. */
+long long vk_accum_work_bytes(int device);
+
 /* ----------------------------------------------------------- orientation */
 /* gradient_histogram + dominant_orientations (orient.py:271-350) for n_kp
  * keypoints (n_kp_dev: device count, read by the kernel; n_kp_max bounds it).
@@ -183,13 +188,15 @@ int vk_order_keypoints(const unsigned long long* cand_keys, const int* cand_coun
  * exact_only != 0 forces the reference accumulation order and the brute-force
  * argmax for every keypoint (weights then bit-identical to the reference).
  * grads (nullable, indexed like levels): precomputed gradient volumes
- * (vk_gradient_volume); levels without one use direct gathers. */
+ * (vk_gradient_volume); levels without one use direct gathers.
+ * work: vk_accum_work_bytes() of device scratch owned by this call while it
+ * runs (one per concurrently running stream). */
 int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_level* levels,
               const vk_ball* balls, const int* ball_offsets, const double* windows,
               const float* windows32, const double* dirs, int K, const uint8_t* pair_ok,
               double secondary_ratio, int max_frames,
               double* weights, int* nframes, int* prim, int* sec, int* status,
-              int exact_only, const int* ico_host, const vk_gradlevel* grads, void* stream);
+              int exact_only, const int* ico_host, const vk_gradlevel* grads, double* work, void* stream);
 
 /* dominant_orientations (orient.py:310-350) on n caller-supplied K-bin
  * weight vectors (exact comparisons). */
@@ -218,12 +225,13 @@ int vk_expand_frames(const int* nframes, const int* prim, const int* sec, const 
  * one item per keypoint so gradients are computed once for all its frames,
  * the stage API one item per frame).  rot: 9 fp64 per frame (row-major 3x3).
  * max_f bounds item_count.  stats (nullable): stats[0] counts frames that fell
- * back to the exact accumulation order.  exact_only forces that order. */
+ * back to the exact accumulation order.  exact_only forces that order.
+ * work: as for vk_orient. */
 int vk_describe_siftrank(const vk_frame* frames, const double* rot, const int* item_first,
                          const int* item_count, const int* n_items_dev, int n_items_max, int max_f,
                          const vk_kp* kps, const vk_level* levels, const vk_ball* balls,
                          const int* ball_offsets, uint8_t* ranks_out,
-                         int exact_only, int* stats, const vk_gradlevel* grads, void* stream);
+                         int exact_only, int* stats, const vk_gradlevel* grads, double* work, void* stream);
 
 /* extract_patch + preblur_patch + brief/rrief (descriptor.py:96-111,
  * 196-224).  kind 1 = BRIEF (packed big-endian bits, ceil(n/8) bytes per

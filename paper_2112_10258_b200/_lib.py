@@ -32,6 +32,7 @@ SIGNATURES = {
     "vk_device_sm_count": [I],
     "vk_memset_async": [P, LL, P],
     "vk_launch_count": [],
+    "vk_accum_work_bytes": [I],
     "vk_transpose_zfast_to_xfast": [P, P, I, I, I, I, P],
     "vk_transpose_xfast_to_zfast": [P, P, I, I, I, I, P],
     "vk_blur3d": [P, P, P, P, I, I, I, I, P, I, P],
@@ -42,16 +43,16 @@ SIGNATURES = {
     "vk_detect_octave": [P, I, I, I, I, I, I, I, F, P, P, I, P],
     "vk_extrema_from_map": [P, P, I, I, I, I, I, F, P, P, I, P],
     "vk_order_keypoints": [P, P, I, I, P, P, I, P, P, P, P, P, P, P, P, I, P],
-    "vk_orient": [P, P, I, P, P, P, P, P, P, I, P, D, I, P, P, P, P, P, I, P, P, P],
+    "vk_orient": [P, P, I, P, P, P, P, P, P, I, P, D, I, P, P, P, P, P, I, P, P, P, P],
     "vk_frames_from_weights": [P, I, I, P, D, I, P, P, P, P],
     "vk_expand_frames": [P, P, P, P, I, I, P, I, P, P, P, P, I, P, P],
-    "vk_describe_siftrank": [P, P, P, P, P, I, I, P, P, P, P, P, I, P, P, P],
+    "vk_describe_siftrank": [P, P, P, P, P, I, I, P, P, P, P, P, I, P, P, P, P],
     "vk_gradient_volume": [P, P, P, I, I, I, I, P, P, P],
     "vk_describe_patch": [I, P, P, P, I, P, P, P, P, I, P, P, I, P, I, P, P, P],
     "vk_match": [I, P, I, P, I, I, D, P, P, P, P, P],
     "vk_match_excluding": [I, P, I, P, I, I, D, I, I, P, P, P, P, P],
 }
-_RESTYPE = {"vk_last_error": C.c_char_p, "vk_launch_count": C.c_longlong}
+_RESTYPE = {"vk_last_error": C.c_char_p, "vk_launch_count": C.c_longlong, "vk_accum_work_bytes": C.c_longlong}
 
 # device record layouts (must match include/volkey_b200.h)
 LEVEL_DTYPE = np.dtype([("base", "<u8"), ("vol_stride", "<i8"), ("nx", "<i4"), ("ny", "<i4"), ("nz", "<i4"),
@@ -104,6 +105,16 @@ def check(rc: int, what: str = "") -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def accum_work():
+    """Device scratch for vk_orient / vk_describe_siftrank (one per stream that
+    runs them concurrently)."""
+    t = torch()
+    n = load().vk_accum_work_bytes(t.cuda.current_device())
+    if n <= 0:
+        raise DeviceError(f"vk_accum_work_bytes: {last_error()}")
+    return t.empty(n // 8, dtype=t.float64, device="cuda")
 
 
 _torch = None

@@ -4,7 +4,7 @@
 #include <atomic>
 #include <stdio.h>
 
-#include "vk_common.cuh"
+#include "vk_hood.cuh"
 
 namespace vk {
 
@@ -47,3 +47,12 @@ extern "C" int vk_memset_async(void* ptr, long long bytes, void* stream) {
 }
 
 extern "C" long long vk_launch_count(void) { return vk::g_launches.load(); }
+
+extern "C" long long vk_accum_work_bytes(int device) {
+    const int sms = vk_device_sm_count(device);
+    if (sms <= 0) {
+        vk::set_error("vk_accum_work_bytes: no device %d", device);
+        return -1;
+    }
+    return (long long)sms * vk::kAccumCtasPerSm * vk::kAccumSlot * (long long)sizeof(double);
+}

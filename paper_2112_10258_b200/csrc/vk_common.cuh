@@ -161,9 +161,6 @@ VK_D float norm3_f32(float x, float y, float z) {
 // (4 u32 for the norm, 1 u32 for the window cast, 1 u32 for the product,
 // rounded up generously), and an absolute allowance for fp32 subnormals.
 constexpr double kVoteRel = 1.0e-6;
-// Relative error of an fp32 run / butterfly sum of <= 32 votes (depth-5
-// addition tree: gamma_5 in fp32 ~ 3e-7, rounded up).
-constexpr double kRunRel = 5.0e-7;
 constexpr double kVoteAbs = 1.0e-43;
 
 // Unit roundoff of fp64 and a rigorous bound factor for recursive summation:

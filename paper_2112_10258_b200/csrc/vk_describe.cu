@@ -114,7 +114,7 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
 template <int NF>
 VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const float4* g4, const vk_ball& ball,
                  const int* __restrict__ ball_offsets, const double* Rs, const float* Rfs, double* hist, int F) {
-    const int tid = threadIdx.x, wid = tid >> 5;
+    const int tid = threadIdx.x;
     const int step = blockDim.x;
     int cnt = 0;
     int pn = tid < ball.count ? __ldg(ball_offsets + ball.zstart + tid) : 0;
@@ -155,7 +155,7 @@ VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const fl
             const int bin = has ? sr_bin_fast(ox, oy, oz, gx, gy, gz, Rs + 9 * f, Rfs + 9 * f, data, L.nx, L.ny, L.nz, x,
                                               y, z)
                                 : -1;
-            warp_accum(hist + (f * (blockDim.x >> 5) + wid) * 64, bin, mag);
+            red_vote(hist + f * kSrBins, bin, mag);
         }
     }
     return cnt;
@@ -220,8 +220,8 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                 const vk_level* __restrict__ levels, const vk_ball* __restrict__ balls,
                 const int* __restrict__ ball_offsets, int max_f,
                 uint8_t* __restrict__ out, int exact_only, int* __restrict__ stats,
-                const vk_gradlevel* __restrict__ grads) {
-    extern __shared__ double hist[];  // [max_f][kSrWarps][64]
+                const vk_gradlevel* __restrict__ grads, double* __restrict__ work) {
+    double* hist = work + (long long)blockIdx.x * kAccumSlot;  // [F][64] fp64, L2-resident
     __shared__ double w[kSrBins];
     __shared__ int order[kSrBins];
     __shared__ double Rs[VK_MAX_FRAMES * 9];
@@ -244,7 +244,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
             Rs[i] = rot[(long long)first * 9 + i];
             Rfs[i] = (float)Rs[i];
         }
-        for (int i = tid; i < F * kSrWarps * kSrBins; i += kSrThreads) hist[i] = 0.0;
+        zero_hist(hist, F * kSrBins);
         if (tid == 0) n_inside = 0;
         __syncthreads();
         int cnt = 0;
@@ -263,7 +263,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                 case 4: cnt = sr_walk<4>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, F); break;
                 default:  // > 4 frames: two passes of up to 4 frames
                     cnt = sr_walk<4>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, 4);
-                    sr_walk<4>(kp, L, data, g4, ball, ball_offsets, Rs + 36, Rfs + 36, hist + 4 * kSrWarps * kSrBins,
+                    sr_walk<4>(kp, L, data, g4, ball, ball_offsets, Rs + 36, Rfs + 36, hist + 4 * kSrBins,
                                F - 4);
                     break;
             }
@@ -278,9 +278,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
         __syncthreads();
         for (int f = 0; f < F; ++f) {
             if (fast && tid < kSrBins) {
-                double sacc = 0.0;
-                for (int wi = 0; wi < kSrWarps; ++wi) sacc = dadd(sacc, hist[(f * kSrWarps + wi) * kSrBins + tid]);
-                w[tid] = sacc;
+                w[tid] = read_hist(hist, f * kSrBins + tid);
             }
             __syncthreads();
             int myrank = 0;
@@ -293,7 +291,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
             if (fast) {
                 // every adjacent pair of the sorted bins must be separated by more than
                 // the bound between our summation and the reference's sequential one
-                const double epsrel = 2.0 * (kVoteRel + kRunRel + gamma_k((double)n_inside + 64.0));
+                const double epsrel = 2.0 * (kVoteRel + gamma_k((double)n_inside + 64.0));
                 const double epsabs = kVoteAbs * n_inside;
                 int bad = 0;
                 if (tid + 1 < kSrBins) {
@@ -421,24 +419,17 @@ extern "C" int vk_describe_siftrank(const vk_frame* frames, const double* rot, c
                                     const int* item_count, const int* n_items_dev, int n_items_max, int max_f,
                                     const vk_kp* kps, const vk_level* levels, const vk_ball* balls,
                                     const int* ball_offsets, uint8_t* ranks_out,
-                                    int exact_only, int* stats, const vk_gradlevel* grads, void* stream) {
+                                    int exact_only, int* stats, const vk_gradlevel* grads, double* work,
+                                    void* stream) {
     if (!frames || !rot || !item_first || !item_count || n_items_max < 0 || max_f < 1 || max_f > VK_MAX_FRAMES ||
-        !kps || !levels || !balls || !ball_offsets || !ranks_out) {
+        !kps || !levels || !balls || !ball_offsets || !ranks_out || !work) {
         set_error("vk_describe_siftrank: bad arguments");
         return VK_ERR_PARAMETER;
     }
     if (n_items_max == 0) return VK_OK;
-    const int smem = max_f * kSrWarps * kSrBins * 8;
-    static int configured = 0;
-    if (smem > 48 * 1024 && configured < smem) {
-        cudaError_t e = cudaFuncSetAttribute(siftrank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             VK_MAX_FRAMES * kSrWarps * kSrBins * 8);
-        if (e != cudaSuccess) return cuda_status(e, "siftrank attribute");
-        configured = VK_MAX_FRAMES * kSrWarps * kSrBins * 8;
-    }
-    siftrank_kernel<<<grid_for(n_items_max, 4), kSrThreads, smem, as_stream(stream)>>>(
+    siftrank_kernel<<<grid_for(n_items_max, kAccumCtasPerSm), kSrThreads, 0, as_stream(stream)>>>(
         frames, rot, item_first, item_count, n_items_dev, n_items_max, kps, levels, balls, ball_offsets, max_f,
-        ranks_out, exact_only, stats, grads);
+        ranks_out, exact_only, stats, grads, work);
     count_launch();
     return cuda_status(cudaGetLastError(), "siftrank launch");
 }

@@ -20,7 +20,6 @@
 namespace vk {
 
 constexpr int kOriThreads = 256;
-constexpr int kOriWarps = kOriThreads / 32;
 
 struct OriShared {
     double xv[kOriThreads];
@@ -284,10 +283,10 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
               const float* __restrict__ windows32, const double* __restrict__ dirs_g, int K,
               const uint8_t* __restrict__ pair_ok, double ratio, int max_frames, double* __restrict__ weights,
               int* __restrict__ nframes, int* __restrict__ prim, int* __restrict__ sec, int* __restrict__ status,
-              int exact_only, IcoT ico, const vk_gradlevel* __restrict__ grads) {
+              int exact_only, IcoT ico, const vk_gradlevel* __restrict__ grads, double* __restrict__ work) {
     __shared__ OriShared sh;
     __shared__ IcoSh ic;
-    __shared__ double hist[kOriWarps * VK_MAX_DIRS];
+    double* hist = work + (long long)blockIdx.x * kAccumSlot;  // [K] fp64, L2-resident
     const int tid = threadIdx.x;
     for (int i = tid; i < 3 * K; i += kOriThreads) sh.dirs[i] = dirs_g[i];
     if (ico.valid && tid < 72) {
@@ -308,7 +307,7 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         const vk_ball ball = balls[kp.ball];
         const double* win = windows + ball.window_start;
         const float* win32 = windows32 + ball.window_start;
-        for (int i = tid; i < kOriWarps * K; i += kOriThreads) hist[i] = 0.0;
+        zero_hist(hist, K);
         if (tid == 0) { sh.n_inside = 0; sh.exact = exact_only; }
         __syncthreads();
         int inside_cnt = 0;
@@ -317,7 +316,6 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
             // precomputed gradient volume: one coalesced (bin, |g|) pair per visit
             const uint8_t* bl = GL.bin + (long long)kp.vol * GL.vol_stride;
             const float4* gl = reinterpret_cast<const float4*>(GL.g4) + (long long)kp.vol * GL.vol_stride;
-            double* wh = hist + (tid >> 5) * K;
             int pn = tid < ball.count ? __ldg(ball_offsets + ball.zstart + tid) : 0;
             for (int base = 0; base < ball.count; base += kOriThreads) {
                 const int j = base + tid;
@@ -338,11 +336,10 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
                         }
                     }
                 }
-                warp_accum(wh, bin, vote);
+                red_vote(hist, bin, vote);
             }
         } else if (!exact_only) {
             // z-major ball walk: consecutive lanes take consecutive x -> coalesced gathers
-            double* wh = hist + (tid >> 5) * K;
             int pn = tid < ball.count ? __ldg(ball_offsets + ball.zstart + tid) : 0;
             for (int base = 0; base < ball.count; base += kOriThreads) {
                 const int j = base + tid;
@@ -359,7 +356,7 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
                                             ox * ox + oy * oy + oz * oz, sh.dirs, icp, K, vote);
                     }
                 }
-                warp_accum(wh, bin, vote);
+                red_vote(hist, bin, vote);
             }
         } else {
             for (int j = tid; j < ball.count; j += kOriThreads) {
@@ -380,17 +377,13 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
             continue;
         }
         if (!sh.exact) {
-            for (int b = tid; b < K; b += kOriThreads) {
-                double sacc = 0.0;
-                for (int w = 0; w < kOriWarps; ++w) sacc = dadd(sacc, hist[w * K + b]);
-                sh.w[b] = sacc;
-            }
+            for (int b = tid; b < K; b += kOriThreads) sh.w[b] = read_hist(hist, b);
             __syncthreads();
             sort_desc(sh.w, K, sh.order);
             __syncthreads();
             if (tid == 0) {
-                // each vote passes through <= n_inside run/scan/merge additions
-                const double epsrel = 2.0 * (kVoteRel + kRunRel + gamma_k((double)sh.n_inside + 64.0));
+                // fp32 votes (kVoteRel) summed in fp64 in some order vs the reference's
+                const double epsrel = 2.0 * (kVoteRel + gamma_k((double)sh.n_inside + 64.0));
                 const double epsabs = kVoteAbs * sh.n_inside;
                 if (!frames_certain(sh.w, sh.order, K, epsrel, epsabs, ratio, max_frames)) {
                     sh.exact = 1;
@@ -558,8 +551,8 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
                          const vk_ball* balls, const int* ball_offsets, const double* windows, const float* windows32,
                          const double* dirs, int K, const uint8_t* pair_ok, double secondary_ratio, int max_frames,
                          double* weights, int* nframes, int* prim, int* sec, int* status, int exact_only,
-                         const int* ico_host, const vk_gradlevel* grads, void* stream) {
-    if (!kps || n_kp_max < 0 || !levels || !balls || !ball_offsets || !windows || !windows32 || !dirs || K < 1 ||
+                         const int* ico_host, const vk_gradlevel* grads, double* work, void* stream) {
+    if (!kps || n_kp_max < 0 || !levels || !balls || !ball_offsets || !windows || !windows32 || !dirs || K < 1 || !work ||
         K > VK_MAX_DIRS || !pair_ok || !nframes || !prim || !sec || !status || max_frames < 1 ||
         max_frames > VK_MAX_FRAMES || !(secondary_ratio > 0.0 && secondary_ratio <= 1.0)) {
         set_error("vk_orient: bad arguments (K=%d max_frames=%d)", K, max_frames);
@@ -569,7 +562,7 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = n_kp_max < sms * 4 ? n_kp_max : sms * 4;
+    const int grid = n_kp_max < sms * kAccumCtasPerSm ? n_kp_max : sms * kAccumCtasPerSm;
     IcoT ico{};
     if (ico_host && K == 42) {
         ico.valid = 1;
@@ -581,7 +574,7 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
     orient_kernel<<<grid, kOriThreads, 0, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
                                                                windows, windows32, dirs, K, pair_ok, secondary_ratio,
                                                                max_frames, weights, nframes, prim, sec, status,
-                                                               exact_only, ico, grads);
+                                                               exact_only, ico, grads, work);
     count_launch();
     return cuda_status(cudaGetLastError(), "orient launch");
 }

@@ -190,6 +190,7 @@ class Extractor:
                 if i < L - 1:
                     dog_t[o * L + i] = self.dogs[o][i]
         self.level_table = _lib.to_device_records(level_records(lvl_t, dims_l))
+        self.accum = _lib.accum_work()  # orientation / SIFT-Rank vote histograms
         # octaves from here on are small enough for the fused shared-memory kernel
         self.small_from = self.plan.n_octaves
         for o, d in enumerate(self.plan.octave_dims):
@@ -315,7 +316,7 @@ class Extractor:
                   tb.dirs.data_ptr(), tb.K,
                   tb.pair_ok.data_ptr(), float(cfg.secondary_ratio), self.maxf, None, self.nframes.data_ptr(),
                   self.prim.data_ptr(), self.sec.data_ptr(), self.status.data_ptr(), self.exact_only,
-                  tb.ico.ctypes.data, self.grad_table.data_ptr(), s)
+                  tb.ico.ctypes.data, self.grad_table.data_ptr(), self.accum.data_ptr(), s)
         _lib.call("vk_expand_frames", self.nframes.data_ptr(), self.prim.data_ptr(), self.sec.data_ptr(),
                   self.total.data_ptr(), self.kp_cap, self.maxf, tb.rot_table.data_ptr(), tb.K,
                   self.frames.data_ptr(), self.rot.data_ptr(), self.n_frames.data_ptr(), self.dropped.data_ptr(),
@@ -330,7 +331,7 @@ class Extractor:
                       self.nframes.data_ptr(), self.total.data_ptr(), self.kp_cap, self.maxf, self.kps.data_ptr(),
                       self.level_table.data_ptr(), tb.balls.data_ptr(), tb.ball_offsets.data_ptr(),
                       self.desc.data_ptr(), self.exact_only, self.status.data_ptr() + 8,
-                      self.grad_table.data_ptr(), s)
+                      self.grad_table.data_ptr(), self.accum.data_ptr(), s)
         else:
             code = KIND_CODE[cfg.descriptor]
             _lib.call("vk_describe_patch", code, self.frames.data_ptr(), self.rot.data_ptr(),

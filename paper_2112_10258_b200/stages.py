@@ -105,7 +105,7 @@ def run_orientation(pyr, keypoints, radius_factor=4.0, secondary_ratio=0.8, max_
     _lib.call("vk_orient", d_kps.data_ptr(), None, n, view.table.data_ptr(), d_balls.data_ptr(), d_off.data_ptr(),
               d_win.data_ptr(), d_win32.data_ptr(), d_dirs.data_ptr(), K, d_ok.data_ptr(), float(secondary_ratio), mf, _lib.ptr(weights),
               nframes.data_ptr(), prim.data_ptr(), sec.data_ptr(), status.data_ptr(), int(bool(exact)),
-              None if ico is None else ico.ctypes.data, None, _lib.stream_ptr())
+              None if ico is None else ico.ctypes.data, None, _lib.accum_work().data_ptr(), _lib.stream_ptr())
     if int(status[0].item()) & 1:
         raise DataError("orientation neighborhood lies entirely outside the volume")
     out = dict(nframes=nframes.cpu().numpy(), prim=prim.cpu().numpy().reshape(n, mf),
@@ -149,7 +149,7 @@ def run_descriptors(pyr, keypoints, rotations, kind="siftrank", pairs=None, patc
         count = t.ones(m, dtype=t.int32, device="cuda")
         _lib.call("vk_describe_siftrank", d_fr.data_ptr(), d_rot.data_ptr(), first.data_ptr(), count.data_ptr(), None,
                   m, 1, d_kps.data_ptr(), view.table.data_ptr(), d_balls.data_ptr(), d_off.data_ptr(),
-                  out.data_ptr(), int(bool(exact)), None, None, s)
+                  out.data_ptr(), int(bool(exact)), None, None, _lib.accum_work().data_ptr(), s)
     else:
         if patch_side < 1 or patch_side % 2 == 0:
             raise ParameterError(f"patch side must be odd and >= 1, got {patch_side}")

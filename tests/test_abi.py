@@ -31,7 +31,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     assert not missing, missing
     # every declared entry point has a ctypes signature in the binding
     assert set(names) <= set(_lib.SIGNATURES), set(names) - set(_lib.SIGNATURES)
-    assert lib.vk_abi_version() == 1
+    assert lib.vk_abi_version() == 2
 
 
 def test_record_layouts_match_header():
