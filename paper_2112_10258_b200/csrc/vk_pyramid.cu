@@ -26,202 +26,294 @@ struct Taps {
     float w[VK_MAX_TAPS];
 };
 
-constexpr int kTX = 32;       // tile width in x (one warp lane per column)
-constexpr int kTY = 32;       // tile height in y (8 warps x 4 rows)
+constexpr int kTX = 32;       // output tile width in x
+constexpr int kTY = 32;       // output tile height in y
 constexpr int kThreads = 256;
-constexpr int kMaxRingR = 10; // register-ring kernel covers radius 1..10
+constexpr int kMaxRingR = 10; // streaming kernel covers radius 1..10
 
+// Shared-memory geometry of the streaming blur for radius R.
+//  * in_s: the clamped input plane, (kTY+2R) rows x (kTX+2R) columns, stored
+//    as float2 row PAIRS ((row 2i, row 2i+1) at each column) so the x-pass
+//    multiplies two rows with one packed FMUL2 from one aligned register pair.
+//    Pitch COLSP (in float2) is 1 mod 16: the 4 row pairs x 4 segments of a
+//    half-warp hit 16 distinct 8-byte bank pairs.  Two buffers.
+//  * x_s: x-blurred rows, row-major, read by the y-pass as (x, x+1) pairs.
+//    Two buffers.
 template <int R>
 struct BlurGeom {
     static constexpr int P = 2 * R + 1;
-    static constexpr int ROWS = kTY + 2 * R;               // rows of the x-pass tile
-    static constexpr int COLS = kTX + 2 * R;               // input columns per row
-    static constexpr int V4 = (8 + 2 * R + 3) / 4;         // float4 per x-pass segment
-    static constexpr int XPW = 24 + 4 * V4;                // input row pitch (>= COLS)
-    static constexpr int XS = kTX + 4;                     // x-pass tile pitch
-    static constexpr int SMEM = (2 * ROWS * XPW + ROWS * XS) * 4;
+    static constexpr int ROWS = kTY + 2 * R;       // even
+    static constexpr int RP = ROWS / 2;
+    static constexpr int COLS = kTX + 2 * R;
+    static constexpr int COLSP = ((COLS + 15) / 16) * 16 + 1;  // == 1 mod 16
+    static constexpr int IN_F2 = RP * COLSP;         // float2 per staging buffer
+    static constexpr int XS = kTX + 4;               // x_s pitch (floats)
+    static constexpr int LROWS = (ROWS + 7) / 8;     // staging rows per warp
+    static constexpr int SMEM = (2 * IN_F2 * 2 + 2 * ROWS * XS + ROWS) * 4;
 };
 
-// Products of two taps at once: packed FMUL2 (two IEEE-rounded products); the
-// sums stay scalar FADDs in tap order.  ptxas never contracts FMUL2 + FADD
-// (it does contract FMUL2 + FADD2 into FFMA2, which would break parity).
+// Two taps' products with one packed FMUL2 (two IEEE-rounded products); sums
+// stay scalar FADDs in tap order.  ptxas contracts FMUL2 + FADD2 into FFMA2
+// even with --fmad=false (verified in SASS), so packed adds are not used.
 VK_D float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+VK_D void acc2(float2& a, float2 p) {
+    a.x = fadd(a.x, p.x);
+    a.y = fadd(a.y, p.y);
+}
 
+// One arriving y-blurred plane (z') in the z-pass.  The accumulator ring holds
+// the 2R+1 outputs z'-R .. z'+R in slots (phase + k) mod P; the arriving value
+// is multiplied once per distinct tap distance d (the kernel is symmetric, so
+// w[R-d] == w[R+d] and one product serves outputs z'-d and z'+d: the reference
+// rounds the same product twice, bit for bit the same number).  Output z'+R
+// starts (first tap: assignment), output z'-R receives its last tap and is
+// returned.  Every output still receives its taps in order -R..+R.
+template <int R, int C>
+VK_D void z_arrive(float2 (&r0)[2 * R + 1], float2 (&r1)[2 * R + 1], float2 v0, float2 v1, const Taps& taps,
+                   float2& o0, float2& o1) {
+    constexpr int P = 2 * R + 1;
+#pragma unroll
+    for (int d = 0; d <= R; ++d) {
+        const float w = taps.w[R + d];
+        const float2 p0 = fmul2(make_float2(w, w), v0), p1 = fmul2(make_float2(w, w), v1);
+        if (d == 0) {
+            acc2(r0[C], p0);
+            acc2(r1[C], p1);
+        } else {
+            const int up = (C + d) % P, dn = (C - d + P) % P;
+            if (d == R) {
+                r0[up] = p0;
+                r1[up] = p1;
+            } else {
+                acc2(r0[up], p0);
+                acc2(r1[up], p1);
+            }
+            acc2(r0[dn], p0);
+            acc2(r1[dn], p1);
+        }
+    }
+    o0 = r0[(C - R + P) % P];
+    o1 = r1[(C - R + P) % P];
+}
+
+// Binary dispatch on the (CTA-uniform) ring phase so every ring index is a
+// compile-time constant: the ring stays in registers and never moves.
+template <int R, int LO, int HI>
+VK_D void z_dispatch(int c, float2 (&r0)[2 * R + 1], float2 (&r1)[2 * R + 1], float2 v0, float2 v1,
+                     const Taps& taps, float2& o0, float2& o1) {
+    if constexpr (HI - LO == 1) {
+        z_arrive<R, LO>(r0, r1, v0, v1, taps, o0, o1);
+    } else {
+        constexpr int MID = (LO + HI) / 2;
+        if (c < MID) z_dispatch<R, LO, MID>(c, r0, r1, v0, v1, taps, o0, o1);
+        else z_dispatch<R, MID, HI>(c, r0, r1, v0, v1, taps, o0, o1);
+    }
+}
+
+// Radii >= 8 need more than 128 registers for the ring: one CTA per SM.
 template <int R>
-__global__ void __launch_bounds__(kThreads, 2)
-blur3d_ring_kernel(const float* __restrict__ src, float* __restrict__ dst, float* __restrict__ dog,
-                   float* __restrict__ half, int nx, int ny, int nz, int tz, int nzc, Taps taps) {
+constexpr int blur_min_blocks() { return R >= 8 ? 1 : 2; }
+
+// Streaming separable blur (x-fastest volumes): one CTA = a 32x32 (x, y)
+// output tile x a z-range.  Per distinct input plane: cp.async staging
+// (clamped = replicate padding), x-pass of (32+2R) rows, y-pass to 2x2
+// outputs per thread, then the plane "arrives" in the z ring.  Planes outside
+// [0, nz) are the clamped border plane: their x/y-passes are not recomputed,
+// the same value just arrives again.  Epilogues on each finished output
+// plane: level store, DoG = src - dst (finer minus coarser; the src values
+// are prefetched a plane ahead), and the ordered 2x2x2 mean of the handoff
+// level from the thread's own 2x2 (x, y) block and the previous plane (tile
+// origins and z_start are even).
+//
+// One barrier per plane: the x-pass of plane q reads in_s[q&1] and writes
+// x_s[q&1]; after the barrier the staging of plane q+2 into in_s[q&1] is
+// issued and the y-pass reads x_s[q&1] while other threads may already run
+// the x-pass of q+1 (other buffers).  Element offsets are 32-bit (the host
+// checks nb * volume < 2^32).
+template <int R>
+__global__ void __launch_bounds__(kThreads, blur_min_blocks<R>())
+blur3d_stream_kernel(const float* __restrict__ src, float* __restrict__ dst, float* __restrict__ dog,
+                     float* __restrict__ half, int nx, int ny, int nz, int tz, int nzc, Taps taps) {
     using G = BlurGeom<R>;
     constexpr int P = G::P;
     extern __shared__ float4 smem4[];
-    float* in_s = reinterpret_cast<float*>(smem4);
-    float* x_s = in_s + 2 * G::ROWS * G::XPW;
+    float2* in2 = reinterpret_cast<float2*>(smem4);
+    float* x_s = reinterpret_cast<float*>(in2 + 2 * G::IN_F2);           // 2 buffers
+    unsigned* roff_s = reinterpret_cast<unsigned*>(x_s + 2 * G::ROWS * G::XS);
 
     const int b = blockIdx.z / nzc;
     const int zc = blockIdx.z - b * nzc;
     const int z_start = zc * tz;
     const int z_end = min(nz, z_start + tz);
     const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
-    const long long plane = (long long)nx * ny;
-    const long long vol = plane * nz;
-    const float* s = src + b * vol;
+    const unsigned plane = (unsigned)nx * (unsigned)ny;
+    const unsigned vbase = (unsigned)b * plane * (unsigned)nz;  // element offset of volume b
     const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
 
-    // Loop-invariant clamped x offsets of this lane's (up to 2) tile columns.
-    constexpr int NCOL = (G::COLS + 31) / 32;
-    int gxo[NCOL];
-#pragma unroll
-    for (int k = 0; k < NCOL; ++k) gxo[k] = clampi(x0 - R + lane + 32 * k, 0, nx - 1);
+    // Staging: warp wy loads rows wy + 8k, lane loads columns lane and
+    // lane + 32; smem float index of (row r, column c) is
+    // ((r>>1)*COLSP + c)*2 + (r&1).  Clamped row offsets live in shared
+    // memory (kept out of registers: the z ring needs them).
+    const unsigned cx0 = (unsigned)clampi(x0 - R + lane, 0, nx - 1);
+    const unsigned cx1 = (unsigned)clampi(x0 - R + lane + 32, 0, nx - 1);
+    const int sbase = ((wy >> 1) * G::COLSP + lane) * 2 + (wy & 1);
+    for (int r = tid; r < G::ROWS; r += kThreads) roff_s[r] = vbase + (unsigned)clampi(y0 - R + r, 0, ny - 1) * (unsigned)nx;
+    __syncthreads();
 
-    auto load_plane = [&](int zp, int buf) {
-        const float* sp = s + (long long)clampi(zp, 0, nz - 1) * plane;
-        float* d = in_s + buf * G::ROWS * G::XPW;
+    auto load_plane = [&](int q, int buf) {
+        const unsigned qoff = (unsigned)q * plane;
+        float* d = reinterpret_cast<float*>(in2 + buf * G::IN_F2) + sbase;
 #pragma unroll
-        for (int r = wy; r < G::ROWS; r += kThreads / 32) {
-            const unsigned roff = (unsigned)clampi(y0 - R + r, 0, ny - 1) * (unsigned)nx;
-            float* drow = d + r * G::XPW + lane;
-#pragma unroll
-            for (int k = 0; k < NCOL; ++k)
-                if (lane + 32 * k < G::COLS) cp_async4(drow + 32 * k, sp + (roff + (unsigned)gxo[k]));
+        for (int k = 0; k < G::LROWS; ++k) {
+            if (wy + 8 * k < G::ROWS) {
+                const unsigned ro = roff_s[wy + 8 * k] + qoff;
+                cp_async4(d + k * 8 * G::COLSP, src + (ro + cx0));
+                if (lane + 32 < G::COLS) cp_async4(d + k * 8 * G::COLSP + 64, src + (ro + cx1));
+            }
         }
         cp_async_commit();
     };
 
-    float ring[4][P];
-    float prev[4];
+    float2 r0[P], r1[P];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        prev[j] = 0.f;
-#pragma unroll
-        for (int t = 0; t < P; ++t) ring[j][t] = 0.f;
-    }
+    for (int t = 0; t < P; ++t) r0[t] = r1[t] = make_float2(0.f, 0.f);
+    float2 pv0 = make_float2(0.f, 0.f), pv1 = make_float2(0.f, 0.f);
 
-    const int zp0 = z_start - R;
-    const int nplanes = (z_end - z_start) + 2 * R;
-    load_plane(zp0, 0);
-    for (int p = 0; p < nplanes; ++p) {
-        if (p + 1 < nplanes) load_plane(zp0 + p + 1, (p + 1) & 1);
-        else cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-        // ---- x-pass: 4 threads per tile row, 8 outputs each (pairs of outputs share FMUL2) ----
-        {
-            const int r = tid >> 2, sg = tid & 3;
-            if (r < G::ROWS) {
-                const float4* row = reinterpret_cast<const float4*>(in_s + (p & 1) * G::ROWS * G::XPW + r * G::XPW + sg * 8);
-                float v[4 * G::V4];
+    // x-pass role: lane -> (segment xsg = lane / 4 of 8, row pair xrp = warp * 4 + lane % 4)
+    const int xsg = lane >> 2, xrp = wy * 4 + (lane & 3);
+    // y-pass / z / epilogue role: column pair cp, row pair yp (2x2 outputs)
+    const int cp = tid & 15, yp = tid >> 4;
+    const int gx = x0 + 2 * cp, gy = y0 + 2 * yp;
+    const bool okx0 = gx < nx, okx1 = gx + 1 < nx, oky0 = gy < ny, oky1 = gy + 1 < ny;
+    const unsigned e00 = vbase + (unsigned)min(gy, ny - 1) * (unsigned)nx + (unsigned)min(gx, nx - 1);
+    const unsigned rowst = oky1 ? (unsigned)nx : 0u;  // clamped: in-bounds dummy reads only
+    const unsigned colst = okx1 ? 1u : 0u;
+
+    const int za = z_start - R, zb = z_end - 1 + R;  // arriving planes (unclamped)
+    const int qlo = max(0, za), qhi = min(nz - 1, zb);
+    int a = 0, c = 0;
+    load_plane(qlo, 0);
+    cp_async_wait<0>();
+    __syncthreads();
+    if (qlo < qhi) load_plane(qlo + 1, 1);
+    for (int q = qlo; q <= qhi; ++q) {
+        const int it = q - qlo;
+        const int reps = 1 + (q == qlo ? qlo - za : 0) + (q == qhi ? zb - qhi : 0);
+        // Prefetch the DoG sources of the first output this plane completes.
+        float s00 = 0.f, s01 = 0.f, s10 = 0.f, s11 = 0.f;
+        const int zo_first = z_start + a - 2 * R;
+        if (dog != nullptr && a >= 2 * R) {
+            const float* sv = src + (e00 + (unsigned)zo_first * plane);
+            s00 = __ldg(sv);
+            s01 = __ldg(sv + colst);
+            s10 = __ldg(sv + rowst);
+            s11 = __ldg(sv + rowst + colst);
+        }
+        // ---- x-pass: 2 rows x 4 outputs per thread, inputs streamed ----
+        float* xs = x_s + (it & 1) * G::ROWS * G::XS;
+        if (xrp < G::RP) {
+            const float2* row = in2 + (it & 1) * G::IN_F2 + xrp * G::COLSP + 4 * xsg;
+            float2 acc[4];
 #pragma unroll
-                for (int q = 0; q < G::V4; ++q) {
-                    float4 t4 = row[q];
-                    v[4 * q] = t4.x; v[4 * q + 1] = t4.y; v[4 * q + 2] = t4.z; v[4 * q + 3] = t4.w;
+            for (int i = 0; i < 4 + 2 * R; ++i) {
+                const float2 v = row[i];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int t = i - k;
+                    if (t < 0 || t > 2 * R) continue;
+                    const int dd = t < R ? R - t : t - R;
+                    const float w = taps.w[R + dd];
+                    const float2 p = fmul2(make_float2(w, w), v);
+                    if (t == 0) acc[k] = p;
+                    else acc2(acc[k], p);
                 }
-                float o[8];
+            }
+            *reinterpret_cast<float4*>(xs + (2 * xrp) * G::XS + 4 * xsg) = make_float4(acc[0].x, acc[1].x, acc[2].x, acc[3].x);
+            *reinterpret_cast<float4*>(xs + (2 * xrp + 1) * G::XS + 4 * xsg) = make_float4(acc[0].y, acc[1].y, acc[2].y, acc[3].y);
+        }
+        cp_async_wait<0>();  // plane q+1 staged (this thread's part)
+        __syncthreads();
+        if (q + 2 <= qhi) load_plane(q + 2, it & 1);
+        // ---- y-pass: rows 2yp, 2yp+1 x columns (2cp, 2cp+1) ----
+        float2 v0, v1;
+        {
+            const float* col = xs + (2 * yp) * G::XS + 2 * cp;
 #pragma unroll
-                for (int k = 0; k < 8; k += 2) {
-                    float2 pr = fmul2(make_float2(taps.w[0], taps.w[0]), make_float2(v[k], v[k + 1]));
-                    float a0 = pr.x, a1 = pr.y;
-#pragma unroll
-                    for (int t = 1; t < P; ++t) {
-                        pr = fmul2(make_float2(taps.w[t], taps.w[t]), make_float2(v[k + t], v[k + 1 + t]));
-                        a0 = fadd(a0, pr.x);
-                        a1 = fadd(a1, pr.y);
+            for (int i = 0; i < 2 + 2 * R; ++i) {
+                const float2 v = *reinterpret_cast<const float2*>(col + i * G::XS);
+                if (i <= 2 * R) {
+                    const int dd = i < R ? R - i : i - R;
+                    const float w = taps.w[R + dd];
+                    const float2 p = fmul2(make_float2(w, w), v);
+                    if (i == 0) v0 = p;
+                    else acc2(v0, p);
+                }
+                if (i >= 1) {
+                    const int t = i - 1;
+                    const int dd = t < R ? R - t : t - R;
+                    const float w = taps.w[R + dd];
+                    const float2 p = fmul2(make_float2(w, w), v);
+                    if (t == 0) v1 = p;
+                    else acc2(v1, p);
+                }
+            }
+        }
+        // ---- z-pass: the plane arrives once, or repeatedly at clamped borders ----
+        for (int rep = 0; rep < reps; ++rep) {
+            float2 o0, o1;
+            z_dispatch<R, 0, P>(c, r0, r1, v0, v1, taps, o0, o1);
+            if (a >= 2 * R) {
+                const int zo = z_start + a - 2 * R;
+                const unsigned eo = e00 + (unsigned)zo * plane;
+                if (dog != nullptr && rep > 0) {  // later outputs of a border plane
+                    const float* sv = src + eo;
+                    s00 = __ldg(sv);
+                    s01 = __ldg(sv + colst);
+                    s10 = __ldg(sv + rowst);
+                    s11 = __ldg(sv + rowst + colst);
+                }
+                float* dv = dst + eo;
+                if (oky0) {
+                    if (okx0) dv[0] = o0.x;
+                    if (okx1) dv[1] = o0.y;
+                }
+                if (oky1) {
+                    if (okx0) dv[nx] = o1.x;
+                    if (okx1) dv[nx + 1] = o1.y;
+                }
+                if (dog != nullptr) {
+                    float* gv = dog + eo;
+                    if (oky0) {
+                        if (okx0) gv[0] = __fsub_rn(s00, o0.x);
+                        if (okx1) gv[1] = __fsub_rn(s01, o0.y);
                     }
-                    o[k] = a0;
-                    o[k + 1] = a1;
+                    if (oky1) {
+                        if (okx0) gv[nx] = __fsub_rn(s10, o1.x);
+                        if (okx1) gv[nx + 1] = __fsub_rn(s11, o1.y);
+                    }
                 }
-                float4* xo = reinterpret_cast<float4*>(x_s + r * G::XS + sg * 8);
-                xo[0] = make_float4(o[0], o[1], o[2], o[3]);
-                xo[1] = make_float4(o[4], o[5], o[6], o[7]);
-            }
-        }
-        __syncthreads();
-        // ---- y-pass into the per-column z ring ----
-        {
-            float col[4 + 2 * R];
-#pragma unroll
-            for (int i = 0; i < 4 + 2 * R; ++i) col[i] = x_s[(4 * wy + i) * G::XS + lane];
-#pragma unroll
-            for (int j = 0; j < 4; j += 2) {
-                float2 pr = fmul2(make_float2(taps.w[0], taps.w[0]), make_float2(col[j], col[j + 1]));
-                float a0 = pr.x, a1 = pr.y;
-#pragma unroll
-                for (int t = 1; t < P; ++t) {
-                    pr = fmul2(make_float2(taps.w[t], taps.w[t]), make_float2(col[j + t], col[j + 1 + t]));
-                    a0 = fadd(a0, pr.x);
-                    a1 = fadd(a1, pr.y);
-                }
-#pragma unroll
-                for (int t = 0; t < P - 1; ++t) {
-                    ring[j][t] = ring[j][t + 1];
-                    ring[j + 1][t] = ring[j + 1][t + 1];
-                }
-                ring[j][P - 1] = a0;
-                ring[j + 1][P - 1] = a1;
-            }
-        }
-        if (p < 2 * R) continue;
-        // ---- z-pass + epilogues for output plane zo ----
-        const int zo = zp0 + p - R;
-        const int gx = x0 + lane;
-        float out[4];
-#pragma unroll
-        for (int j = 0; j < 4; j += 2) {
-            float2 pr = fmul2(make_float2(taps.w[0], taps.w[0]), make_float2(ring[j][0], ring[j + 1][0]));
-            float a0 = pr.x, a1 = pr.y;
-#pragma unroll
-            for (int t = 1; t < P; ++t) {
-                pr = fmul2(make_float2(taps.w[t], taps.w[t]), make_float2(ring[j][t], ring[j + 1][t]));
-                a0 = fadd(a0, pr.x);
-                a1 = fadd(a1, pr.y);
-            }
-            out[j] = a0;
-            out[j + 1] = a1;
-        }
-        {
-            // 32-bit offsets within the volume (a volume holds < 2^31 voxels)
-            float* dv = dst + b * vol + (long long)zo * plane;
-            float* gv = dog ? dog + b * vol + (long long)zo * plane : nullptr;
-            const float* sv = src + b * vol + (long long)zo * plane;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int gy = y0 + 4 * wy + j;
-                if (gx < nx && gy < ny) {
-                    const unsigned o = (unsigned)gy * (unsigned)nx + (unsigned)gx;
-                    dv[o] = out[j];
-                    if (gv) gv[o] = __fsub_rn(__ldg(sv + o), out[j]);
-                }
-            }
-        }
-        if (half != nullptr && (zo & 1)) {
-            float np_[4], no_[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                np_[j] = __shfl_down_sync(0xffffffffu, prev[j], 1);
-                no_[j] = __shfl_down_sync(0xffffffffu, out[j], 1);
-            }
-            const int hx = gx >> 1, hz = zo >> 1;
-            const int hnx = nx >> 1, hny = ny >> 1, hnz = nz >> 1;
-            if ((lane & 1) == 0 && hx < hnx && hz < hnz) {
-#pragma unroll
-                for (int j = 0; j < 4; j += 2) {
-                    const int hy = (y0 + 4 * wy + j) >> 1;
-                    if (hy < hny) {
+                if (half != nullptr && (zo & 1)) {
+                    const int hnx = nx >> 1, hny = ny >> 1, hnz = nz >> 1;
+                    const int hx = gx >> 1, hy = gy >> 1, hz = zo >> 1;
+                    if (hx < hnx && hy < hny && hz < hnz) {
                         // (dx, dy, dz) order of scalespace.py:129-135, then /8.
-                        float sm = prev[j];
-                        sm = fadd(sm, out[j]);
-                        sm = fadd(sm, prev[j + 1]);
-                        sm = fadd(sm, out[j + 1]);
-                        sm = fadd(sm, np_[j]);
-                        sm = fadd(sm, no_[j]);
-                        sm = fadd(sm, np_[j + 1]);
-                        sm = fadd(sm, no_[j + 1]);
+                        float sm = pv0.x;
+                        sm = fadd(sm, o0.x);
+                        sm = fadd(sm, pv1.x);
+                        sm = fadd(sm, o1.x);
+                        sm = fadd(sm, pv0.y);
+                        sm = fadd(sm, o0.y);
+                        sm = fadd(sm, pv1.y);
+                        sm = fadd(sm, o1.y);
                         half[(((long long)b * hnz + hz) * hny + hy) * hnx + hx] = fmul(sm, 0.125f);
                     }
                 }
+                pv0 = o0;
+                pv1 = o1;
             }
+            ++a;
+            c = (c + 1 == P) ? 0 : c + 1;
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) prev[j] = out[j];
     }
 }
 
@@ -414,23 +506,36 @@ static int launch_ring(const float* src, float* dst, float* dog, float* half, in
     using G = BlurGeom<R>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(blur3d_ring_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(blur3d_stream_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
         if (e != cudaSuccess) return cuda_status(e, "blur3d attribute");
         configured = true;
     }
     const int tiles = ((nx + kTX - 1) / kTX) * ((ny + kTY - 1) / kTY);
-    // z-chunking only when the batch does not fill ~1.5 waves (2 CTAs / SM):
-    // every chunk re-reads and re-blurs 2R halo planes.
+    // z-chunking: every chunk re-stages and re-blurs (x, y) 2R halo planes, so
+    // pick the chunk count that minimises waves x planes per CTA (chunks of at
+    // least 16 planes, even starts for the subsample epilogue).
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int nzc = 1;
-    while ((long long)tiles * nb * nzc < 3 * sms && (nz + nzc) / (nzc + 1) >= 16) ++nzc;
-    int tz = (nz + nzc - 1) / nzc;
-    tz += tz & 1;
-    nzc = (nz + tz - 1) / tz;
+    const long long slots = (long long)sms * blur_min_blocks<R>();
+    int nzc = 1, tz = nz + (nz & 1);
+    double best = -1.0;
+    for (int n = 1; n <= 16; ++n) {
+        int t = (nz + n - 1) / n;
+        t += t & 1;
+        const int nc = (nz + t - 1) / t;
+        if (n > 1 && t < 16) break;
+        const long long ctas = (long long)tiles * nb * nc;
+        const double waves = (double)((ctas + slots - 1) / slots);
+        const double cost = waves * (t + (nc > 1 ? 2 * R : R));
+        if (best < 0 || cost < best * 0.97) {
+            best = cost;
+            nzc = nc;
+            tz = t;
+        }
+    }
     dim3 grid((nx + kTX - 1) / kTX, (ny + kTY - 1) / kTY, nb * nzc);
-    blur3d_ring_kernel<R><<<grid, kThreads, G::SMEM, st>>>(src, dst, dog, half, nx, ny, nz, tz, nzc, taps);
+    blur3d_stream_kernel<R><<<grid, kThreads, G::SMEM, st>>>(src, dst, dog, half, nx, ny, nz, tz, nzc, taps);
     count_launch();
     return cuda_status(cudaGetLastError(), "blur3d launch");
 }
@@ -480,6 +585,13 @@ extern "C" int vk_blur3d(const float* src, float* dst, float* dog_out, float* ha
     for (int i = 0; i < 2 * radius + 1; ++i) taps.w[i] = taps_host[i];
     cudaStream_t st = as_stream(stream);
     if (half_out && (nx < 2 || ny < 2 || nz < 2)) half_out = nullptr;
+    // The streaming kernel shares each product between the two taps at the
+    // same distance; Gaussian taps (scalespace.py:35-42) are exactly symmetric.
+    bool symmetric = true;
+    for (int i = 0; i < radius; ++i) symmetric = symmetric && taps.w[i] == taps.w[2 * radius - i];
+    // The streaming kernel addresses the batch with 32-bit element offsets.
+    const bool small = (unsigned long long)nb * nx * ny * nz < (1ull << 32);
+    if (!symmetric || !small) return launch_generic(src, dst, dog_out, half_out, nb, nx, ny, nz, radius, taps, st);
     switch (radius) {
         case 1: return launch_ring<1>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, st);
         case 2: return launch_ring<2>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, st);

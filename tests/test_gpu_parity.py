@@ -99,6 +99,43 @@ def test_blur_all_radii_match_oracle():
         assert np.array_equal(got, want), f"sigma {sigma} radius {r} dims {dims}"
 
 
+def test_blur_fused_epilogues_batched():
+    """vk_blur3d with the DoG and 2x-subsample epilogues on a batch of odd-sized
+    volumes (partial tiles, z-chunking, clamped borders) for every radius the
+    streaming kernel instantiates: bit-equal to the oracle's blur3 / difference
+    / half (scalespace.py:91-110, 137-151)."""
+    import torch
+
+    from oracle import volkey_oracle as O
+    from paper_2112_10258_b200 import _lib
+
+    rng = np.random.default_rng(11)
+    for sigma, dims in ((0.3, (37, 9, 70)), (0.6, (33, 35, 64)), (0.9, (66, 40, 34)), (1.2, (45, 71, 40)),
+                        (1.5, (64, 64, 33)), (1.9, (35, 38, 90)), (2.2, (71, 33, 36)), (2.6, (40, 40, 47)),
+                        (2.9, (97, 65, 34)), (3.2, (33, 100, 41)), (3.6, (50, 37, 96))):
+        nb = 3
+        r, w = O.gauss_taps(sigma)
+        a = rng.standard_normal((nb,) + dims).astype(np.float32)  # numpy [b][x][y][z]
+        xf = np.ascontiguousarray(a.transpose(0, 3, 2, 1))         # x-fastest [b][z][y][x]
+        src = torch.from_numpy(xf).cuda()
+        dst = torch.empty_like(src)
+        dog = torch.empty_like(src)
+        hs = tuple(d // 2 for d in dims)
+        half = torch.empty((nb,) + hs[::-1], dtype=torch.float32, device="cuda")
+        wt = np.ascontiguousarray(w, dtype=np.float32)
+        _lib.call("vk_blur3d", src.data_ptr(), dst.data_ptr(), dog.data_ptr(), half.data_ptr(), nb, *dims,
+                  wt.ctypes.data, r, _lib.stream_ptr())
+        torch.cuda.synchronize()
+        got = dst.cpu().numpy().transpose(0, 3, 2, 1)
+        gdog = dog.cpu().numpy().transpose(0, 3, 2, 1)
+        ghalf = half.cpu().numpy().transpose(0, 3, 2, 1)
+        for i in range(nb):
+            want = O.blur3(a[i], w)
+            assert np.array_equal(got[i], want), f"blur sigma {sigma} radius {r} dims {dims} volume {i}"
+            assert np.array_equal(gdog[i], a[i] - want), f"dog sigma {sigma} radius {r}"
+            assert np.array_equal(ghalf[i], O.half(want)), f"half sigma {sigma} radius {r}"
+
+
 def test_subsample_units(golden_unit):
     g = golden_unit
     for i in range(4):
