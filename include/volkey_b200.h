@@ -249,9 +249,11 @@ int vk_describe_patch(int kind, const vk_frame* frames, const double* rot, const
 
 /* --------------------------------------------------------------- matching */
 /* nearest_neighbor_matches (match.py:81-121).  metric 0 = hamming on packed
- * bytes (nbytes per row), 1 = euclidean on int16 rows (dim per row),
- * 2 = euclidean on fp64 rows.  Outputs per query: best index, d1, d2 (fp64),
- * keep (d1 <= ratio_max * d2). */
+ * bytes (nbytes per row), 1 = euclidean on int8 rows (dim bytes per row;
+ * rows of 32/64/96/128 bytes at 16-byte aligned addresses run on the tensor
+ * cores, tcgen05.mma kind::i8 with s32 accumulators; other widths on a dp4a
+ * kernel), 2 = euclidean on fp64 rows.  Outputs per query: best index, d1, d2
+ * (fp64), keep (d1 <= ratio_max * d2). */
 int vk_match(int metric, const void* a, int na, const void* b, int nb_rows, int dim,
              double ratio_max, int* best, double* d1, double* d2, uint8_t* keep, void* stream);
 
@@ -261,6 +263,10 @@ int vk_match(int metric, const void* a, int na, const void* b, int nb_rows, int 
 int vk_match_excluding(int metric, const void* a, int na, const void* b, int nb_rows, int dim,
                        double ratio_max, int ex_lo, int ex_hi, int* best, double* d1, double* d2,
                        uint8_t* keep, void* stream);
+
+/* Select the int8 euclidean kernel: 0 = tensor cores where the shape allows
+ * (default), 1 = dp4a everywhere (cross-checks and benchmarks). */
+int vk_set_match_path(int path);
 
 #ifdef __cplusplus
 }

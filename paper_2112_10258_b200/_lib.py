@@ -51,6 +51,7 @@ SIGNATURES = {
     "vk_describe_patch": [I, P, P, P, I, P, P, P, P, I, P, P, I, P, I, P, P, P],
     "vk_match": [I, P, I, P, I, I, D, P, P, P, P, P],
     "vk_match_excluding": [I, P, I, P, I, I, D, I, I, P, P, P, P, P],
+    "vk_set_match_path": [I],
 }
 _RESTYPE = {"vk_last_error": C.c_char_p, "vk_launch_count": C.c_longlong, "vk_accum_work_bytes": C.c_longlong}
 

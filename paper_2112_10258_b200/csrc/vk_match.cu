@@ -22,6 +22,11 @@
 namespace vk {
 
 constexpr int kMatchThreads = 128;
+
+// 0: tensor-core path for int8 rows when the shape allows (default);
+// 1: the dp4a kernel (vk_set_match_path, used by the tests to cross-check).
+static int g_match_path = 0;
+static int match_path() { return g_match_path; }
 constexpr int kTileRows = 64;
 
 struct Best {
@@ -168,6 +173,17 @@ __global__ void match_merge_kernel(const T* __restrict__ pm1, const T* __restric
     keep[q] = e1 <= dmul(ratio, e2) ? 1 : 0;
 }
 
+void launch_merge_ll(const long long* pm1, const long long* pm2, const int* pi1, int na, int slices, int metric,
+                     double ratio, int* best, double* d1, double* d2, uint8_t* keep, cudaStream_t st) {
+    match_merge_kernel<long long><<<(na + 255) / 256, 256, 0, st>>>(pm1, pm2, pi1, na, slices, metric, ratio, best, d1,
+                                                                    d2, keep);
+    count_launch();
+}
+
+// vk_match_tc.cu: tcgen05 kind::i8 path for rank descriptors (-1: shape not covered).
+int match_i8_tensor(const uint8_t* a, int na, const uint8_t* b, int nb, int dim, double ratio, int ex_lo, int ex_hi,
+                    int* best, double* d1, double* d2, uint8_t* keep, cudaStream_t st);
+
 }  // namespace vk
 
 using namespace vk;
@@ -184,6 +200,11 @@ extern "C" int vk_match_excluding(int metric, const void* a, int na, const void*
     }
     if (na == 0) return VK_OK;
     cudaStream_t st = as_stream(stream);
+    if (metric == 1 && match_path() == 0) {
+        const int rc = match_i8_tensor(static_cast<const uint8_t*>(a), na, static_cast<const uint8_t*>(b), nb_rows, dim,
+                                       ratio_max, ex_lo, ex_hi, best, d1, d2, keep, st);
+        if (rc >= 0) return rc;
+    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -232,6 +253,15 @@ extern "C" int vk_match_excluding(int metric, const void* a, int na, const void*
     }
     cudaFreeAsync(scratch, st);
     return cuda_status(cudaGetLastError(), "match launch");
+}
+
+extern "C" int vk_set_match_path(int path) {
+    if (path < 0 || path > 1) {
+        set_error("vk_set_match_path: path must be 0 (tensor cores) or 1 (dp4a)");
+        return VK_ERR_PARAMETER;
+    }
+    g_match_path = path;
+    return VK_OK;
 }
 
 extern "C" int vk_match(int metric, const void* a, int na, const void* b, int nb_rows, int dim, double ratio_max,

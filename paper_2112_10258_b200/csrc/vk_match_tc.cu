@@ -1,0 +1,366 @@
+// vk_match_tc.cu -- nearest / second-nearest neighbour search for int8 rank
+// descriptors (SIFT-Rank, RRIEF) on the 5th-generation tensor cores.
+//
+// Reference: match.py:70-121 (euclidean_distances + nearest_neighbor_matches):
+// d2 = |a|^2 + |b|^2 - 2 a.b in float64, np.argmin (first minimum), second
+// order statistic, ratio test.  For int8 rows the dot products are exact in
+// int32 (tcgen05.mma kind::i8, s32 accumulators) and so is d2, so the integer
+// minimum / tie order is identical to the reference's float64 one.
+//
+// One CTA = 128 query rows (M = 128) x a slice of reference rows, swept in
+// tiles of 128 rows (N = 128; two CTAs per SM, 256 TMEM columns each):
+//   * the query tile sits in shared memory for the whole sweep; reference
+//     tiles are staged with cp.async (16-byte chunks) into the canonical
+//     no-swizzle K-major core-matrix layout (8 rows x 16 bytes per core
+//     matrix), double-buffered;
+//   * one elected thread issues K/32 tcgen05.mma per tile into one of two
+//     128-column TMEM accumulators and commits to an mbarrier, so the MMA of
+//     tile t+1 runs while all 8 warps reduce tile t;
+//   * epilogue: warp w reads TMEM lanes 32*(w%4).. (its query rows), columns
+//     128*(w/4).. of the tile (tcgen05.ld 32x32b.x32), forms d' = |b|^2 - 2 a.b
+//     and keeps the running (first) minimum + second minimum, testing four
+//     columns at a time against the current second minimum;
+//   * per (slice, row) partial results are merged in slice order by
+//     match_merge_kernel (vk_match.cu), which adds |a|^2 and applies the
+//     sqrt + ratio test in float64.
+// Rows [ex_lo, ex_hi) of the reference set are skipped (database matching:
+// the query subject's own rows) and later indices are reported compacted.
+#include <climits>
+
+#include "vk_common.cuh"
+
+namespace vk {
+
+constexpr int kTcM = 128;        // query rows per CTA
+constexpr int kTcN = 128;        // reference rows per tile (2 CTAs / SM share TMEM)
+constexpr int kTcThreads = 256;  // 8 warps
+
+// Canonical K-major no-swizzle layout: core matrix (8 rows x 16 B) at
+// (row / 8) * SBO + (kbyte / 16) * LBO, rows 16 B apart inside it.
+template <int KB>
+struct TcGeom {
+    static constexpr int KBYTES = 32 * KB;        // bytes per row (K)
+    static constexpr int LBO = 128;               // next 16-byte K chunk
+    static constexpr int SBO = (KBYTES / 16) * 128;  // next 8-row group
+    static constexpr int A_BYTES = kTcM * KBYTES;
+    static constexpr int B_BYTES = kTcN * KBYTES;
+    // smem: A | B[2] | norms[3][kTcN] | partial exchange | mbarriers | tmem addr
+    // (norms of tile t live in slot t % 3: tile t+2 is staged while the
+    // epilogue of tile t still reads them)
+    static constexpr int OFF_B = A_BYTES;
+    static constexpr int OFF_N = OFF_B + 2 * B_BYTES;
+    static constexpr int OFF_X = OFF_N + 3 * kTcN * 4;
+    static constexpr int OFF_BAR = OFF_X + kTcM * 16;
+    static constexpr int SMEM = OFF_BAR + 32;
+};
+
+VK_D unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+VK_D unsigned long long umma_desc(unsigned saddr, int lbo, int sbo) {
+    unsigned long long d = 0;
+    d |= (unsigned long long)((saddr & 0x3FFFF) >> 4);
+    d |= (unsigned long long)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (unsigned long long)((sbo >> 4) & 0x3FFF) << 32;
+    d |= 1ull << 46;  // descriptor version (sm_100)
+    return d;         // base offset 0, no swizzle
+}
+
+// kind::i8 instruction descriptor: D s32, A/B signed 8-bit, both K-major.
+constexpr unsigned tc_idesc(int m, int n) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((unsigned)(n >> 3) << 17) | ((unsigned)(m >> 4) << 24);
+}
+
+VK_D void cp16(unsigned dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0));
+}
+
+VK_D void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+VK_D void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+VK_D void mbar_wait_parity(unsigned bar, unsigned parity) {
+    unsigned ok = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    } while (!ok);
+}
+
+VK_D void tmem_ld32(unsigned taddr, int (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct Top2 {
+    int m1, m2, i1;
+};
+
+VK_D void top2_push(Top2& t, int d, int j) {
+    if (d < t.m1) {
+        t.m2 = t.m1;
+        t.m1 = d;
+        t.i1 = j;
+    } else if (d < t.m2) {
+        t.m2 = d;
+    }
+}
+
+// Stage reference tile rows [j0, j0 + kTcN) (zero rows past nb) + their norms.
+template <int KB>
+VK_D void stage_b(const uint8_t* __restrict__ b, const int* __restrict__ bnorm, int nb, int j0, unsigned sb,
+                  unsigned sn) {
+    using G = TcGeom<KB>;
+    constexpr int CH = G::KBYTES / 16;  // 16-byte chunks per row
+    for (int e = threadIdx.x; e < kTcN * CH; e += kTcThreads) {
+        const int r = e / CH, c = e - r * CH;
+        const int j = j0 + r;
+        const bool ok = j < nb;
+        cp16(sb + (unsigned)((r >> 3) * G::SBO + c * G::LBO + (r & 7) * 16),
+             b + (long long)(ok ? j : 0) * G::KBYTES + 16 * c, ok);
+    }
+    // the norms array is padded (zeros) to whole tiles
+    for (int e = threadIdx.x; e < kTcN / 4; e += kTcThreads) cp16(sn + 16u * e, bnorm + j0 + 4 * e, true);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kTcThreads, 2)
+match_i8_tc_kernel(const uint8_t* __restrict__ a, int na, const uint8_t* __restrict__ b, const int* __restrict__ bnorm,
+                   int nb, int tiles_per_slice, int ex_lo, int ex_hi, long long* __restrict__ pm1,
+                   long long* __restrict__ pm2, int* __restrict__ pi1) {
+    using G = TcGeom<KB>;
+    constexpr int CH = G::KBYTES / 16;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const unsigned s0 = su32(smem);
+    const unsigned sA = s0, sB = s0 + G::OFF_B, sN = s0 + G::OFF_N;
+    const int* nrm_s = reinterpret_cast<const int*>(smem + G::OFF_N);
+    int4* xch = reinterpret_cast<int4*>(smem + G::OFF_X);
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + G::OFF_BAR);
+    unsigned* tmem_slot = reinterpret_cast<unsigned*>(smem + G::OFF_BAR + 16);
+    const unsigned bar0 = su32(bars), bar1 = bar0 + 8;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int q0 = blockIdx.x * kTcM;
+    const int t_first = blockIdx.y * tiles_per_slice;
+    const int n_tiles = (nb + kTcN - 1) / kTcN;
+    const int t_last = min(n_tiles, t_first + tiles_per_slice);  // exclusive
+
+    // ---- setup: TMEM (2 x 256 columns), mbarriers, query tile, first tile ----
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int e = tid; e < kTcM * CH; e += kTcThreads) {
+        const int r = e / CH, c = e - r * CH;
+        const int q = q0 + r;
+        cp16(sA + (unsigned)((r >> 3) * G::SBO + c * G::LBO + (r & 7) * 16),
+             a + (long long)(q < na ? q : 0) * G::KBYTES + 16 * c, q < na);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (t_first < t_last) stage_b<KB>(b, bnorm, nb, t_first * kTcN, sB, sN);
+    if (t_first + 1 < t_last)
+        stage_b<KB>(b, bnorm, nb, (t_first + 1) * kTcN, sB + (unsigned)G::B_BYTES, sN + (unsigned)(kTcN * 4));
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const unsigned tmem = *tmem_slot;
+    constexpr unsigned IDESC = tc_idesc(kTcM, kTcN);
+
+    auto issue_mma = [&](int buf) {
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < KB; ++k) {
+                const unsigned long long da = umma_desc(sA + 256u * k, G::LBO, G::SBO);
+                const unsigned long long db = umma_desc(sB + (unsigned)(buf * G::B_BYTES) + 256u * k, G::LBO, G::SBO);
+                asm volatile(
+                    "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                    " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}"
+                    ::"r"(tmem + (unsigned)(buf * kTcN)), "l"(da), "l"(db), "r"(IDESC), "r"(k));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                         ::"r"(buf ? bar1 : bar0) : "memory");
+        }
+    };
+
+    if (t_first < t_last) issue_mma(0);
+
+    // Epilogue role: query row lr = 32 * (warp % 4) + lane, columns kTcN/2 * (warp / 4) ...
+    const int lr = 32 * (warp & 3) + lane;
+    const int ch = warp >> 2;
+    const unsigned trow = tmem + ((unsigned)(32 * (warp & 3)) << 16);
+    Top2 best{INT_MAX, INT_MAX, -1};
+
+    for (int t = t_first; t < t_last; ++t) {
+        const int it = t - t_first, buf = it & 1;
+        mbar_wait_parity(buf ? bar1 : bar0, (unsigned)(it >> 1) & 1u);
+        tc_fence_after();
+        // tile t+1 is staged (issued during the previous tile): start its MMA now.
+        if (t + 1 < t_last) {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc_fence_before();
+            __syncthreads();
+            tc_fence_after();
+            issue_mma(buf ^ 1);
+            // MMA t has finished reading its B buffer: stage tile t+2 into it.
+            if (t + 2 < t_last) stage_b<KB>(b, bnorm, nb, (t + 2) * kTcN, sB + (unsigned)(buf * G::B_BYTES),
+                                             sN + (unsigned)(((it + 2) % 3) * kTcN * 4));
+        }
+        // ---- epilogue of tile t ----
+        const int j0 = t * kTcN + (kTcN / 2) * ch;
+        const int* nt = nrm_s + (it % 3) * kTcN + (kTcN / 2) * ch;
+        const unsigned tcol = trow + (unsigned)(buf * kTcN + (kTcN / 2) * ch);
+        int v[kTcN / 2];
+        tmem_ld32(tcol, *reinterpret_cast<int(*)[32]>(v));
+        tmem_ld32(tcol + 32, *reinterpret_cast<int(*)[32]>(v + 32));
+        const int4* n4 = reinterpret_cast<const int4*>(nt);
+        if (!((j0 + kTcN / 2 > nb) || (j0 < ex_hi && j0 + kTcN / 2 > ex_lo))) {
+#pragma unroll
+            for (int g = 0; g < kTcN / 8; ++g) {
+                const int4 nn = n4[g];
+                const int d0 = nn.x - 2 * v[4 * g], d1 = nn.y - 2 * v[4 * g + 1];
+                const int d2 = nn.z - 2 * v[4 * g + 2], d3 = nn.w - 2 * v[4 * g + 3];
+                if (__builtin_expect(min(min(d0, d1), min(d2, d3)) < best.m2, 0)) {
+                    const int jb = j0 + 4 * g;
+                    top2_push(best, d0, jb);
+                    top2_push(best, d1, jb + 1);
+                    top2_push(best, d2, jb + 2);
+                    top2_push(best, d3, jb + 3);
+                }
+            }
+        } else {  // ragged last tile or excluded rows inside this half tile
+#pragma unroll
+            for (int k = 0; k < kTcN / 2; ++k) {
+                const int j = j0 + k;
+                if (j < nb && (j < ex_lo || j >= ex_hi)) top2_push(best, nt[k] - 2 * v[k], j);
+            }
+        }
+        tc_fence_before();
+    }
+
+    // ---- merge the two column halves of each row ----
+    __syncthreads();
+    if (ch == 1) xch[lr] = make_int4(best.m1, best.m2, best.i1, 0);
+    __syncthreads();
+    if (ch == 0) {
+        const int4 o = xch[lr];
+        Top2 m = best;
+        // the halves interleave by tile: ties go to the lower column index
+        if (o.x < m.m1 || (o.x == m.m1 && (unsigned)o.z < (unsigned)m.i1)) {
+            m.m2 = min(m.m1, o.y);
+            m.m1 = o.x;
+            m.i1 = o.z;
+        } else {
+            m.m2 = min(m.m2, o.x);
+        }
+        const int q = q0 + lr;
+        if (q < na) {
+            // |a|^2 from the staged query row (dp4a over its 16-byte chunks).
+            int na2 = 0;
+            for (int c = 0; c < CH; ++c) {
+                const uint4 w = *reinterpret_cast<const uint4*>(smem + (lr >> 3) * G::SBO + c * G::LBO + (lr & 7) * 16);
+                na2 = __dp4a((int)w.x, (int)w.x, na2);
+                na2 = __dp4a((int)w.y, (int)w.y, na2);
+                na2 = __dp4a((int)w.z, (int)w.z, na2);
+                na2 = __dp4a((int)w.w, (int)w.w, na2);
+            }
+            const long long o1 = (long long)blockIdx.y * na + q;
+            pm1[o1] = m.m1 == INT_MAX ? LLONG_MAX : (long long)na2 + m.m1;
+            pm2[o1] = m.m2 == INT_MAX ? LLONG_MAX : (long long)na2 + m.m2;
+            pi1[o1] = m.i1 < 0 ? -1 : (m.i1 < ex_lo ? m.i1 : (m.i1 >= ex_hi ? m.i1 - (ex_hi - ex_lo) : m.i1));
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// Squared norms of int8 rows (KBYTES bytes each); rows past n are 0.
+__global__ void row_norms_i8_kernel(const uint8_t* __restrict__ b, int n, int kbytes, int* __restrict__ out, int n_pad) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_pad) return;
+    int s = 0;
+    if (j < n) {
+        const uint32_t* r = reinterpret_cast<const uint32_t*>(b + (long long)j * kbytes);
+        for (int w = 0; w < kbytes / 4; ++w) {
+            const int v = (int)__ldg(r + w);
+            s = __dp4a(v, v, s);
+        }
+    }
+    out[j] = s;
+}
+
+// vk_match.cu: merge (slice, row) partials in slice order + sqrt + ratio test.
+void launch_merge_ll(const long long* pm1, const long long* pm2, const int* pi1, int na, int slices, int metric,
+                     double ratio, int* best, double* d1, double* d2, uint8_t* keep, cudaStream_t st);
+
+template <int KB>
+static int launch_tc(const uint8_t* a, int na, const uint8_t* b, int nb, double ratio, int ex_lo, int ex_hi, int* best,
+                     double* d1, double* d2, uint8_t* keep, cudaStream_t st) {
+    using G = TcGeom<KB>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(match_i8_tc_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        if (e != cudaSuccess) return cuda_status(e, "match tc attribute");
+        configured = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int qtiles = (na + kTcM - 1) / kTcM;
+    const int n_tiles = (nb + kTcN - 1) / kTcN;
+    int slices = (sms + qtiles - 1) / qtiles;  // fill the GPU with (query tile, slice) CTAs
+    if (slices > n_tiles) slices = n_tiles;
+    if (slices < 1) slices = 1;
+    const int per = (n_tiles + slices - 1) / slices;
+    slices = (n_tiles + per - 1) / per;
+    const int n_pad = n_tiles * kTcN;
+    const size_t part = (size_t)slices * na;
+    void* scratch = nullptr;
+    const size_t bytes = part * 16 + part * 4 + (size_t)n_pad * 4 + 16;
+    cudaError_t e = cudaMallocAsync(&scratch, bytes, st);
+    if (e != cudaSuccess) return cuda_status(e, "match tc scratch");
+    long long* pm1 = static_cast<long long*>(scratch);
+    long long* pm2 = pm1 + part;
+    int* pi1 = reinterpret_cast<int*>(pm2 + part);
+    int* norms = pi1 + part + ((4 - (part & 3)) & 3);  // 16-byte aligned (part*20 bytes precede)
+    row_norms_i8_kernel<<<(n_pad + 255) / 256, 256, 0, st>>>(b, nb, G::KBYTES, norms, n_pad);
+    count_launch();
+    match_i8_tc_kernel<KB><<<dim3(qtiles, slices), kTcThreads, G::SMEM, st>>>(a, na, b, norms, nb, per, ex_lo, ex_hi,
+                                                                             pm1, pm2, pi1);
+    count_launch();
+    launch_merge_ll(pm1, pm2, pi1, na, slices, 1, ratio, best, d1, d2, keep, st);
+    cudaFreeAsync(scratch, st);
+    return cuda_status(cudaGetLastError(), "match tc launch");
+}
+
+// Entry from vk_match_excluding for metric 1 rows whose byte width is a
+// multiple of 32 (<= 128) and 16-byte aligned pointers; returns -1 when the
+// shape is not covered (caller falls back to the dp4a kernel).
+int match_i8_tensor(const uint8_t* a, int na, const uint8_t* b, int nb, int dim, double ratio, int ex_lo, int ex_hi,
+                    int* best, double* d1, double* d2, uint8_t* keep, cudaStream_t st) {
+    if (dim % 32 != 0 || dim > 128 || ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15))
+        return -1;
+    switch (dim / 32) {
+        case 1: return launch_tc<1>(a, na, b, nb, ratio, ex_lo, ex_hi, best, d1, d2, keep, st);
+        case 2: return launch_tc<2>(a, na, b, nb, ratio, ex_lo, ex_hi, best, d1, d2, keep, st);
+        case 3: return launch_tc<3>(a, na, b, nb, ratio, ex_lo, ex_hi, best, d1, d2, keep, st);
+        default: return launch_tc<4>(a, na, b, nb, ratio, ex_lo, ex_hi, best, d1, d2, keep, st);
+    }
+}
+
+}  // namespace vk

@@ -80,7 +80,7 @@ def match_database(local: dict, ratio_max: float = 0.9, metric: str = "euclidean
         code = 0
     else:
         rows = np.concatenate([a.astype(np.int8) for a in arrs]) if arrs else np.zeros((0, 64), np.int8)
-        pad = (-rows.shape[1]) % 4
+        pad = (-rows.shape[1]) % 32 if rows.shape[1] <= 128 else (-rows.shape[1]) % 4
         code = 1
     rows = np.pad(rows, ((0, 0), (0, pad)))
     subj = np.concatenate([np.full(len(a), i, np.int32) for i, a in zip(ids, arrs)]) if arrs else np.zeros(0, np.int32)

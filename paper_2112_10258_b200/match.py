@@ -60,7 +60,7 @@ def _prepare(a: np.ndarray, b: np.ndarray, metric: str):
     if a_.dtype.kind in "iub" and b_.dtype.kind in "iub" and a_.size and b_.size \
             and min(a_.min(), b_.min()) >= -128 and max(a_.max(), b_.max()) <= 127:
         dim = a_.shape[1]
-        pad = (-dim) % 4
+        pad = (-dim) % 32 if dim <= 128 else (-dim) % 4  # zero columns: same dots and norms
         a8 = np.pad(a_.astype(np.int8), ((0, 0), (0, pad)))
         b8 = np.pad(b_.astype(np.int8), ((0, 0), (0, pad)))
         return 1, t.from_numpy(np.ascontiguousarray(a8)).cuda(), t.from_numpy(np.ascontiguousarray(b8)).cuda(), dim + pad

@@ -179,6 +179,58 @@ def test_nn_float_and_ties():
     assert [(m.index_a, m.index_b, m.distance, m.second_distance) for m in ms] == [(i, i, 0.0, 0.0) for i in range(10)]
 
 
+def _nn_raw(a8, b8, ratio, ex_lo=0, ex_hi=0, path=0):
+    import torch
+
+    from paper_2112_10258_b200 import _lib
+
+    _lib.call("vk_set_match_path", path)
+    try:
+        A = torch.from_numpy(np.ascontiguousarray(a8)).cuda()
+        B = torch.from_numpy(np.ascontiguousarray(b8)).cuda()
+        n = len(a8)
+        best = torch.empty(n, dtype=torch.int32, device="cuda")
+        d1 = torch.empty(n, dtype=torch.float64, device="cuda")
+        d2 = torch.empty(n, dtype=torch.float64, device="cuda")
+        keep = torch.empty(n, dtype=torch.uint8, device="cuda")
+        _lib.call("vk_match_excluding", 1, A.data_ptr(), n, B.data_ptr(), len(b8), a8.shape[1], float(ratio), ex_lo,
+                  ex_hi, best.data_ptr(), d1.data_ptr(), d2.data_ptr(), keep.data_ptr(), _lib.stream_ptr())
+        return best.cpu().numpy(), d1.cpu().numpy(), d2.cpu().numpy(), keep.cpu().numpy()
+    finally:
+        _lib.call("vk_set_match_path", 0)
+
+
+def test_nn_tensor_core_path_matches_oracle():
+    """tcgen05 kind::i8 matcher == dp4a matcher == oracle (match.py:70-121):
+    full-range int8 rows (not only rank permutations), duplicate rows (ties
+    keep the first index), ragged tile edges, 32..128-byte rows, and an
+    excluded row range straddling tile boundaries."""
+    from oracle import volkey_oracle as O
+
+    rng = np.random.default_rng(21)
+    for na, nb, dim, ex in ((300, 700, 64, (0, 0)), (129, 513, 32, (250, 300)), (77, 1030, 128, (0, 256)),
+                            (256, 257, 96, (0, 0)), (5, 3, 64, (0, 0))):
+        a = rng.integers(-128, 128, size=(na, dim)).astype(np.int8)
+        b = rng.integers(-128, 128, size=(nb, dim)).astype(np.int8)
+        b[nb // 2] = b[nb // 3]                     # a tie
+        a[0] = b[nb // 3]                           # ... that is the exact nearest neighbour of row 0
+        lo, hi = ex
+        got_tc = _nn_raw(a, b, 0.9, lo, hi, path=0)
+        got_dp = _nn_raw(a, b, 0.9, lo, hi, path=1)
+        for x, y in zip(got_tc, got_dp):
+            assert np.array_equal(x, y), (na, nb, dim, ex)
+        bb = np.concatenate([b[:lo], b[hi:]]).astype(np.int64)
+        ref = O.nn_match(a.astype(np.int64), bb, 1.0)
+        assert [int(i) for i in got_tc[0]] == [r[1] for r in ref]
+        assert np.array_equal(got_tc[1], np.array([r[2] for r in ref])), (na, nb, dim)
+        assert np.array_equal(got_tc[2], np.array([r[3] for r in ref])), (na, nb, dim)
+    # rank permutations (SIFT-Rank rows), configs[1]-sized
+    a = np.stack([rng.permutation(64) for _ in range(3333)]).astype(np.int8)
+    b = np.stack([rng.permutation(64) for _ in range(3290)]).astype(np.int8)
+    for x, y in zip(_nn_raw(a, b, 0.9, path=0), _nn_raw(a, b, 0.9, path=1)):
+        assert np.array_equal(x, y)
+
+
 # ------------------------------------------------------------ end to end
 @pytest.mark.parametrize("name", ["small0.npz", "small1.npz", "small2.npz", "soup_cfg2.npz"])
 def test_small_cases(name):
