@@ -132,8 +132,8 @@ VK_D void stage_b(const uint8_t* __restrict__ b, const int* __restrict__ bnorm, 
 template <int KB>
 __global__ void __launch_bounds__(kTcThreads, 2)
 match_i8_tc_kernel(const uint8_t* __restrict__ a, int na, const uint8_t* __restrict__ b, const int* __restrict__ bnorm,
-                   int nb, int tiles_per_slice, int ex_lo, int ex_hi, long long* __restrict__ pm1,
-                   long long* __restrict__ pm2, int* __restrict__ pi1) {
+                   const int* __restrict__ neq_flag, int nb, int tiles_per_slice, int ex_lo, int ex_hi,
+                   long long* __restrict__ pm1, long long* __restrict__ pm2, int* __restrict__ pi1) {
     using G = TcGeom<KB>;
     constexpr int CH = G::KBYTES / 16;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -177,6 +177,8 @@ match_i8_tc_kernel(const uint8_t* __restrict__ a, int na, const uint8_t* __restr
     __syncthreads();
     tc_fence_after();
     const unsigned tmem = *tmem_slot;
+    const bool eq = neq_flag[0] == 0;  // every reference row has the same norm
+    const int cnorm = bnorm[0];
     constexpr unsigned IDESC = tc_idesc(kTcM, kTcN);
 
     auto issue_mma = [&](int buf) {
@@ -228,17 +230,40 @@ match_i8_tc_kernel(const uint8_t* __restrict__ a, int na, const uint8_t* __restr
         tmem_ld32(tcol + 32, *reinterpret_cast<int(*)[32]>(v + 32));
         const int4* n4 = reinterpret_cast<const int4*>(nt);
         if (!((j0 + kTcN / 2 > nb) || (j0 < ex_hi && j0 + kTcN / 2 > ex_lo))) {
+            if (eq) {
+                // All reference norms equal C (rank permutations): d' = C - 2 a.b,
+                // so only dots above T = floor((C - m2) / 2) can enter the top 2.
+                int T = (int)(((long long)cnorm - best.m2) >> 1);
 #pragma unroll
-            for (int g = 0; g < kTcN / 8; ++g) {
-                const int4 nn = n4[g];
-                const int d0 = nn.x - 2 * v[4 * g], d1 = nn.y - 2 * v[4 * g + 1];
-                const int d2 = nn.z - 2 * v[4 * g + 2], d3 = nn.w - 2 * v[4 * g + 3];
-                if (__builtin_expect(min(min(d0, d1), min(d2, d3)) < best.m2, 0)) {
-                    const int jb = j0 + 4 * g;
-                    top2_push(best, d0, jb);
-                    top2_push(best, d1, jb + 1);
-                    top2_push(best, d2, jb + 2);
-                    top2_push(best, d3, jb + 3);
+                for (int g = 0; g < kTcN / 16; ++g) {
+                    const int* w = v + 8 * g;
+                    const int mx = max(__vimax3_s32(w[0], w[1], w[2]), __vimax3_s32(w[3], w[4], w[5]));
+                    if (__builtin_expect(max(mx, max(w[6], w[7])) > T, 0)) {
+                        const int jb = j0 + 8 * g;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) top2_push(best, cnorm - 2 * w[k], jb + k);
+                        T = (int)(((long long)cnorm - best.m2) >> 1);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int g = 0; g < kTcN / 16; ++g) {
+                    const int4 na_ = n4[2 * g], nb_ = n4[2 * g + 1];
+                    const int* w = v + 8 * g;
+                    const int d0 = na_.x - 2 * w[0], d1 = na_.y - 2 * w[1], d2 = na_.z - 2 * w[2], d3 = na_.w - 2 * w[3];
+                    const int d4 = nb_.x - 2 * w[4], d5 = nb_.y - 2 * w[5], d6 = nb_.z - 2 * w[6], d7 = nb_.w - 2 * w[7];
+                    const int mn = min(__vimin3_s32(d0, d1, d2), __vimin3_s32(d3, d4, min(d5, min(d6, d7))));
+                    if (__builtin_expect(mn < best.m2, 0)) {
+                        const int jb = j0 + 8 * g;
+                        top2_push(best, d0, jb);
+                        top2_push(best, d1, jb + 1);
+                        top2_push(best, d2, jb + 2);
+                        top2_push(best, d3, jb + 3);
+                        top2_push(best, d4, jb + 4);
+                        top2_push(best, d5, jb + 5);
+                        top2_push(best, d6, jb + 6);
+                        top2_push(best, d7, jb + 7);
+                    }
                 }
             }
         } else {  // ragged last tile or excluded rows inside this half tile
@@ -289,17 +314,22 @@ match_i8_tc_kernel(const uint8_t* __restrict__ a, int na, const uint8_t* __restr
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
-// Squared norms of int8 rows (KBYTES bytes each); rows past n are 0.
-__global__ void row_norms_i8_kernel(const uint8_t* __restrict__ b, int n, int kbytes, int* __restrict__ out, int n_pad) {
+// Squared norms of int8 rows (KBYTES bytes each); rows past n are 0.  neq[0]
+// (preset to 0) is set if any row's norm differs from row 0's.
+__global__ void row_norms_i8_kernel(const uint8_t* __restrict__ b, int n, int kbytes, int* __restrict__ out, int n_pad,
+                                    int* __restrict__ neq) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n_pad) return;
-    int s = 0;
+    int s = 0, s0 = 0;
     if (j < n) {
         const uint32_t* r = reinterpret_cast<const uint32_t*>(b + (long long)j * kbytes);
+        const uint32_t* r0 = reinterpret_cast<const uint32_t*>(b);
         for (int w = 0; w < kbytes / 4; ++w) {
-            const int v = (int)__ldg(r + w);
+            const int v = (int)__ldg(r + w), v0 = (int)__ldg(r0 + w);
             s = __dp4a(v, v, s);
+            s0 = __dp4a(v0, v0, s0);
         }
+        if (s != s0) neq[0] = 1;
     }
     out[j] = s;
 }
@@ -331,17 +361,20 @@ static int launch_tc(const uint8_t* a, int na, const uint8_t* b, int nb, double 
     const int n_pad = n_tiles * kTcN;
     const size_t part = (size_t)slices * na;
     void* scratch = nullptr;
-    const size_t bytes = part * 16 + part * 4 + (size_t)n_pad * 4 + 16;
+    const size_t bytes = part * 16 + part * 4 + (size_t)n_pad * 4 + 32;
     cudaError_t e = cudaMallocAsync(&scratch, bytes, st);
     if (e != cudaSuccess) return cuda_status(e, "match tc scratch");
     long long* pm1 = static_cast<long long*>(scratch);
     long long* pm2 = pm1 + part;
     int* pi1 = reinterpret_cast<int*>(pm2 + part);
     int* norms = pi1 + part + ((4 - (part & 3)) & 3);  // 16-byte aligned (part*20 bytes precede)
-    row_norms_i8_kernel<<<(n_pad + 255) / 256, 256, 0, st>>>(b, nb, G::KBYTES, norms, n_pad);
+    int* neq = norms + n_pad;
+    e = cudaMemsetAsync(neq, 0, 4, st);
+    if (e != cudaSuccess) return cuda_status(e, "match tc flag");
+    row_norms_i8_kernel<<<(n_pad + 255) / 256, 256, 0, st>>>(b, nb, G::KBYTES, norms, n_pad, neq);
     count_launch();
-    match_i8_tc_kernel<KB><<<dim3(qtiles, slices), kTcThreads, G::SMEM, st>>>(a, na, b, norms, nb, per, ex_lo, ex_hi,
-                                                                             pm1, pm2, pi1);
+    match_i8_tc_kernel<KB><<<dim3(qtiles, slices), kTcThreads, G::SMEM, st>>>(a, na, b, norms, neq, nb, per, ex_lo,
+                                                                             ex_hi, pm1, pm2, pi1);
     count_launch();
     launch_merge_ll(pm1, pm2, pi1, na, slices, 1, ratio, best, d1, d2, keep, st);
     cudaFreeAsync(scratch, st);
