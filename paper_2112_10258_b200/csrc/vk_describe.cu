@@ -80,30 +80,37 @@ __device__ __noinline__ int sr_gbits_exact(const float* data, int nx, int ny, in
     return (g0 > 0.0) + 2 * (g1 > 0.0) + 4 * (g2 > 0.0);
 }
 
+// Rare path: reference fp64 octant bits of the rotated integer offset.
+__device__ __noinline__ int sr_obits_exact(int ox, int oy, int oz, const double* R) {
+    const double o0 = (double)ox, o1 = (double)oy, o2 = (double)oz;
+    return (dot3_blas(o0, o1, o2, R[0], R[3], R[6]) > 0.0) + 2 * (dot3_blas(o0, o1, o2, R[1], R[4], R[7]) > 0.0) +
+           4 * (dot3_blas(o0, o1, o2, R[2], R[5], R[8]) > 0.0);
+}
+
 // Fast SIFT-Rank bin of one voxel for one frame.  Each octant bit is taken
 // from the fp32 rotated component when it clears its error bound (<= ~5 u32 of
-// the L1 norm; bound 1e-6), otherwise from the reference's fp64 FMA chain:
-// offset components need only the integer offset and R (offsets on lines /
-// planes through the centre give exact zeros for axes with zero coordinates),
-// gradient components need the exact fp64 gradient (rare).
+// the L1 norm; bound 1e-6), otherwise from the reference's fp64 FMA chain
+// (out of line, so the common path issues no fp64 at all): offset components
+// need only the integer offset and R (offsets on lines / planes through the
+// centre give exact zeros for axes with zero coordinates), gradient
+// components need the exact fp64 gradient (rare).
 VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const double* R, const float* Rf,
                      const float* data, int nx, int ny, int nz, int x, int y, int z) {
     const float fx = (float)ox, fy = (float)oy, fz = (float)oz;
     const float eo = 1.0e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
     const float eg = 1.0e-6f * (fabsf(gx) + fabsf(gy) + fabsf(gz)) + 1.0e-40f;
     int sp = 0, og = 0;
-    bool gsure = true;
+    bool osure = true, gsure = true;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
         const float r = fmaf(fz, Rf[6 + j], fmaf(fy, Rf[3 + j], fx * Rf[j]));
         const float g = fmaf(gz, Rf[6 + j], fmaf(gy, Rf[3 + j], gx * Rf[j]));
-        bool rb;
-        if (fabsf(r) > eo) rb = r > 0.f;
-        else rb = dot3_blas((double)ox, (double)oy, (double)oz, R[j], R[3 + j], R[6 + j]) > 0.0;
-        sp |= (int)rb << j;
+        sp |= (int)(r > 0.f) << j;
         og |= (int)(g > 0.f) << j;
+        osure = osure && fabsf(r) > eo;
         gsure = gsure && fabsf(g) > eg;
     }
+    if (!osure) sp = sr_obits_exact(ox, oy, oz, R);
     if (!gsure) og = sr_gbits_exact(data, nx, ny, nz, x, y, z, R);
     return 8 * sp + og;
 }
