@@ -10,9 +10,11 @@ include/volkey_b200.h).  There is no CPU fallback: compute entry points raise
 __version__ = "0.1.0"
 
 from .config import PipelineConfig
+from .consensus import (ConsensusResult, HoughSettings, SimilarityTransform7DOF, count_inlier_matches, hough_consensus,
+                        match_records, similarity_from_correspondences, vote_transform)
 from .detect import Keypoint, detect_keypoints
 from .engine import Extractor
-from .errors import DataError, DeviceError, ParameterError, VolkeyError
+from .errors import DataError, DeviceError, NoConsensusError, ParameterError, VolkeyError
 from .match import Match, nearest_neighbor_matches
 from .pipeline import ExtractionResult, assign_orientations, extract_batch, extract_features
 from .scalespace import build_dog_pyramid, build_gaussian_pyramid
@@ -34,6 +36,15 @@ __all__ = [
     "DeviceVolume",
     "Match",
     "nearest_neighbor_matches",
+    "hough_consensus",
+    "match_records",
+    "count_inlier_matches",
+    "vote_transform",
+    "similarity_from_correspondences",
+    "HoughSettings",
+    "ConsensusResult",
+    "SimilarityTransform7DOF",
+    "NoConsensusError",
     "VolkeyError",
     "ParameterError",
     "DataError",

@@ -2,9 +2,10 @@
 in-scope part of volkey match.py (match.py:19-27, 64-121, 362-370).
 
 ``nearest_neighbor_matches`` runs ``vk_match``: exact integer arithmetic for
-rank (int8) and packed-bit descriptors, fp64 for anything else.  The
-7-DOF Hough consensus (match.py:124-359) is out of scope for this round
-(SURVEY.md §8(f) "next" #1); ``match_descriptors`` is match_records without it.
+rank (int8, tcgen05 tensor cores) and packed-bit (popcount) descriptors, fp64
+for anything else.  The 7-DOF Hough consensus (match.py:124-359) and
+``match_records`` live in consensus.py; ``match_descriptors`` is
+match_records without the consensus step.
 """
 
 from __future__ import annotations

@@ -1,0 +1,77 @@
+"""CPU: 7-DOF Hough consensus (match.py:124-359) against golden vectors made by
+the real reference (tests/golden/make_hough_golden.py), and the batched-numpy
+equivalences it relies on."""
+
+import math
+
+import numpy as np
+import pytest
+
+from paper_2112_10258_b200 import consensus as C
+from paper_2112_10258_b200.detect import Keypoint
+from paper_2112_10258_b200.match import Match
+from paper_2112_10258_b200.orient import OrientationFrame
+
+from conftest import load_golden
+
+
+def _pairs(g, p):
+    kps = [Keypoint(tuple(float(c) for c in pos), float(s), int(o), int(l), float(d), "peak" if sg > 0 else "valley")
+           for pos, s, o, l, d, sg in zip(g[p + "kp_pos"], g[p + "kp_sigma"], g[p + "kp_octave"], g[p + "kp_level"],
+                                          g[p + "kp_dog"], g[p + "kp_sign"])]
+    return [(kps[int(k)], OrientationFrame(np.array(r))) for k, r in zip(g[p + "fr_kp"], g[p + "fr_rot"])]
+
+
+@pytest.mark.parametrize("kind", ["siftrank", "brief", "rrief"])
+def test_hough_consensus_matches_reference(kind):
+    g, h = load_golden("pair.npz"), load_golden("hough.npz")
+    pa, pb = _pairs(g, "a_"), _pairs(g, "b_")
+    matches = [Match(int(r[0]), int(r[1]), float(r[2]), float(r[3])) for r in g[f"nn_{kind}"]]
+    res = C.hough_consensus(matches, pa, pb, C.HoughSettings())
+    pos = {(m.index_a, m.index_b, m.distance, m.second_distance): i for i, m in enumerate(matches)}
+    got = [pos[(m.index_a, m.index_b, m.distance, m.second_distance)] for m in res.inliers]
+    assert got == h[f"{kind}_inliers"].tolist()
+    assert res.cell_votes == int(h[f"{kind}_cell_votes"])
+    assert res.transform.scale == float(h[f"{kind}_scale"])
+    assert np.array_equal(res.transform.rotation, h[f"{kind}_rotation"])
+    assert np.array_equal(res.transform.translation, h[f"{kind}_translation"])
+
+
+def test_vote_transform_batched_equals_per_match():
+    g = load_golden("pair.npz")
+    pa, pb = _pairs(g, "a_"), _pairs(g, "b_")
+    matches = [Match(int(r[0]), int(r[1]), float(r[2]), float(r[3])) for r in g["nn_siftrank"]]
+    scale, rot, trans, _, _ = C._votes(matches, pa, pb)
+    for i, m in enumerate(matches[:300]):
+        t = C.vote_transform(pa[m.index_a][0], pa[m.index_a][1], pb[m.index_b][0], pb[m.index_b][1])
+        assert t.scale == scale[i]
+        assert np.array_equal(t.rotation, rot[i]) and np.array_equal(t.translation, trans[i])
+
+
+def test_stacked_products_equal_per_call_products():
+    """The per-slice BLAS equivalences consensus.py relies on."""
+    rng = np.random.default_rng(0)
+    n = 2000
+    a, b, x = rng.standard_normal((n, 3, 3)), rng.standard_normal((3, 3)), rng.standard_normal((n, 3)) * 50
+    assert np.array_equal(np.matmul(a, b.T), np.array([a[i] @ b.T for i in range(n)]))
+    assert np.array_equal(np.matmul(a, x[:, :, None])[:, :, 0], np.array([a[i] @ x[i] for i in range(n)]))
+    assert np.array_equal(np.matmul(x[:, None, :], b.T)[:, 0], np.array([np.atleast_2d(x[i]) @ b.T for i in range(n)])[:, 0])
+    assert np.array_equal(np.sqrt(np.matmul(x[:, None, :], x[:, :, None])[:, 0, 0]),
+                          np.array([np.linalg.norm(x[i]) for i in range(n)]))
+    d = C.icosphere_directions()
+    dd = np.ascontiguousarray(np.broadcast_to(d, (n,) + d.shape))
+    assert np.array_equal(np.matmul(dd, x[:, :, None])[:, :, 0], np.array([d @ x[i] for i in range(n)]))
+
+
+def test_consensus_errors_and_identity():
+    from paper_2112_10258_b200.errors import NoConsensusError, ParameterError
+
+    with pytest.raises(ParameterError):
+        C.hough_consensus([], [], [])
+    kp = Keypoint((10.0, 20.0, 30.0), 2.0, 0, 1, 0.1, "peak")
+    fr = OrientationFrame(np.eye(3))
+    pairs = [(kp, fr)]
+    with pytest.raises(NoConsensusError):  # one vote < min_votes
+        C.hough_consensus([Match(0, 0, 0.0, 1.0)], pairs, pairs)
+    t = C.similarity_from_correspondences(np.eye(3) * 5, np.eye(3) * 5)
+    assert math.isclose(t.scale, 1.0) and np.allclose(t.rotation, np.eye(3))
