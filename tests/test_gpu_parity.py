@@ -316,6 +316,19 @@ def test_pair_matching():
         assert np.array_equal(got, g[f"nn_{kind}"]), kind
 
 
+def test_count_inlier_matches_end_to_end():
+    """configs[1] accuracy metric end to end: GPU extraction of both volumes,
+    GPU nearest neighbours, host Hough consensus == the reference's inliers
+    (tests/golden/hough.npz)."""
+    h = load_golden("hough.npz")
+    va, vb = synthetic.match_pair()
+    for kind in ("siftrank", "brief", "rrief"):
+        n, rep = vk.count_inlier_matches(vk.Volume(va), vk.Volume(vb), PipelineConfig(descriptor=kind))
+        assert n == len(h[f"{kind}_inliers"]), kind
+        assert rep["transform"].scale == float(h[f"{kind}_scale"])
+        assert np.array_equal(rep["transform"].translation, h[f"{kind}_translation"])
+
+
 def test_batch_equals_single():
     """Batched extraction (volume-major SoA) equals one-volume extraction."""
     vols = [small_volume(load_golden(f"small{i}.npz")) for i in (0, 2)]
