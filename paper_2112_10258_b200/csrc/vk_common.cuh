@@ -108,6 +108,16 @@ VK_D void gradient_at(const float* __restrict__ d, int nx, int ny, int nz, int x
     gz = dmul(dsub(vzh, vzl), (zh - zl) == 2 ? 0.5 : 1.0);
 }
 
+// Prefetch the voxel `ahead` planes above (x, y, z) into L1: the z-major ball
+// walks touch each plane first as the z+1 neighbour of the plane below, so a
+// few planes of lead time hide the L2 / HBM latency of that first touch.
+VK_D void prefetch_plane_ahead(const float* __restrict__ d, int nx, int ny, int nz, int x, int y, int z, int ahead) {
+    if (z + ahead < nz) {
+        const float* p = d + (((unsigned)(z + ahead) * (unsigned)ny + (unsigned)y) * (unsigned)nx + (unsigned)x);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+    }
+}
+
 // The six axis neighbours of (x, y, z) as loaded fp32 values plus the
 // central/one-sided divisor scale per axis (volume.py:244-264).
 struct Nb6 {

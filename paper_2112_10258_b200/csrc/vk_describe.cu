@@ -22,6 +22,7 @@
 namespace vk {
 
 constexpr int kSrThreads = 256;
+constexpr int kPrefetchPlanes = 3;  // z-plane lead of the L1 prefetch in the ball walk
 constexpr int kSrWarps = kSrThreads / 32;
 constexpr int kSrBins = 64;
 constexpr int kPatchThreads = 256;
@@ -149,6 +150,7 @@ VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const fl
                     mag = q.w;
                     has = mag > 0.f;  // |g| > 0 exactly when g != 0 (fp64 norm, never underflows in fp32)
                 } else {
+                    prefetch_plane_ahead(data, L.nx, L.ny, L.nz, x, y, z, kPrefetchPlanes);
                     const Nb6 nb = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
                     grad32(nb, gx, gy, gz);
                     has = !(gx == 0.f && gy == 0.f && gz == 0.f);  // zero vote: no bin changes
