@@ -264,6 +264,13 @@ int vk_match_excluding(int metric, const void* a, int na, const void* b, int nb_
                        double ratio_max, int ex_lo, int ex_hi, int* best, double* d1, double* d2,
                        uint8_t* keep, void* stream);
 
+/* Database matching in one launch (tensor cores): int8 rank rows of
+ * dim = 32/64/96/128 bytes; query row i excludes the reference rows
+ * [row_ex[2i], row_ex[2i+1]) (device array) and reports compacted indices.
+ * Each query's remaining reference set must hold >= 2 rows. */
+int vk_match_rows_excluding(const void* a, int na, const void* b, int nb_rows, int dim, double ratio_max,
+                            const int* row_ex, int* best, double* d1, double* d2, uint8_t* keep, void* stream);
+
 /* Select the int8 euclidean kernel: 0 = tensor cores where the shape allows
  * (default), 1 = dp4a everywhere (cross-checks and benchmarks). */
 int vk_set_match_path(int path);

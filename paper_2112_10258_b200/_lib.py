@@ -52,6 +52,7 @@ SIGNATURES = {
     "vk_match": [I, P, I, P, I, I, D, P, P, P, P, P],
     "vk_match_excluding": [I, P, I, P, I, I, D, I, I, P, P, P, P, P],
     "vk_set_match_path": [I],
+    "vk_match_rows_excluding": [P, I, P, I, I, D, P, P, P, P, P, P],
 }
 _RESTYPE = {"vk_last_error": C.c_char_p, "vk_launch_count": C.c_longlong, "vk_accum_work_bytes": C.c_longlong}
 

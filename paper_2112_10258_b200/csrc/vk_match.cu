@@ -182,7 +182,7 @@ void launch_merge_ll(const long long* pm1, const long long* pm2, const int* pi1,
 
 // vk_match_tc.cu: tcgen05 kind::i8 path for rank descriptors (-1: shape not covered).
 int match_i8_tensor(const uint8_t* a, int na, const uint8_t* b, int nb, int dim, double ratio, int ex_lo, int ex_hi,
-                    int* best, double* d1, double* d2, uint8_t* keep, cudaStream_t st);
+                    const int2* row_ex, int* best, double* d1, double* d2, uint8_t* keep, cudaStream_t st);
 
 }  // namespace vk
 
@@ -202,7 +202,7 @@ extern "C" int vk_match_excluding(int metric, const void* a, int na, const void*
     cudaStream_t st = as_stream(stream);
     if (metric == 1 && match_path() == 0) {
         const int rc = match_i8_tensor(static_cast<const uint8_t*>(a), na, static_cast<const uint8_t*>(b), nb_rows, dim,
-                                       ratio_max, ex_lo, ex_hi, best, d1, d2, keep, st);
+                                       ratio_max, ex_lo, ex_hi, nullptr, best, d1, d2, keep, st);
         if (rc >= 0) return rc;
     }
     int dev = 0, sms = 148;
@@ -253,6 +253,25 @@ extern "C" int vk_match_excluding(int metric, const void* a, int na, const void*
     }
     cudaFreeAsync(scratch, st);
     return cuda_status(cudaGetLastError(), "match launch");
+}
+
+extern "C" int vk_match_rows_excluding(const void* a, int na, const void* b, int nb_rows, int dim, double ratio_max,
+                                       const int* row_ex, int* best, double* d1, double* d2, uint8_t* keep,
+                                       void* stream) {
+    if (!a || !b || na < 0 || nb_rows < 3 || dim < 1 || !row_ex || !best || !d1 || !d2 || !keep ||
+        !(ratio_max > 0.0 && ratio_max <= 1.0)) {
+        set_error("vk_match_rows_excluding: bad arguments (na=%d nb=%d dim=%d)", na, nb_rows, dim);
+        return VK_ERR_PARAMETER;
+    }
+    if (na == 0) return VK_OK;
+    const int rc = match_i8_tensor(static_cast<const uint8_t*>(a), na, static_cast<const uint8_t*>(b), nb_rows, dim,
+                                   ratio_max, 0, 0, reinterpret_cast<const int2*>(row_ex), best, d1, d2, keep,
+                                   as_stream(stream));
+    if (rc < 0) {
+        set_error("vk_match_rows_excluding: rows must be 32/64/96/128 bytes at 16-byte aligned addresses");
+        return VK_ERR_PARAMETER;
+    }
+    return rc;
 }
 
 extern "C" int vk_set_match_path(int path) {

@@ -24,7 +24,9 @@
 //     match_merge_kernel (vk_match.cu), which adds |a|^2 and applies the
 //     sqrt + ratio test in float64.
 // Rows [ex_lo, ex_hi) of the reference set are skipped (database matching:
-// the query subject's own rows) and later indices are reported compacted.
+// the query subject's own rows) and later indices are reported compacted; the
+// range is either one for all queries or per query row (row_ex), so a whole
+// database of subjects is matched in one launch.
 #include <climits>
 
 #include "vk_common.cuh"
@@ -132,7 +134,8 @@ VK_D void stage_b(const uint8_t* __restrict__ b, const int* __restrict__ bnorm, 
 template <int KB>
 __global__ void __launch_bounds__(kTcThreads, 2)
 match_i8_tc_kernel(const uint8_t* __restrict__ a, int na, const uint8_t* __restrict__ b, const int* __restrict__ bnorm,
-                   const int* __restrict__ neq_flag, int nb, int tiles_per_slice, int ex_lo, int ex_hi,
+                   const int* __restrict__ neq_flag, int nb, int tiles_per_slice, int ex_lo_all, int ex_hi_all,
+                   const int2* __restrict__ row_ex,
                    long long* __restrict__ pm1, long long* __restrict__ pm2, int* __restrict__ pi1) {
     using G = TcGeom<KB>;
     constexpr int CH = G::KBYTES / 16;
@@ -204,6 +207,12 @@ match_i8_tc_kernel(const uint8_t* __restrict__ a, int na, const uint8_t* __restr
     const int ch = warp >> 2;
     const unsigned trow = tmem + ((unsigned)(32 * (warp & 3)) << 16);
     Top2 best{INT_MAX, INT_MAX, -1};
+    int ex_lo = ex_lo_all, ex_hi = ex_hi_all;
+    if (row_ex != nullptr) {
+        const int2 e = row_ex[min(q0 + lr, na - 1)];
+        ex_lo = e.x;
+        ex_hi = e.y;
+    }
 
     for (int t = t_first; t < t_last; ++t) {
         const int it = t - t_first, buf = it & 1;
@@ -339,8 +348,8 @@ void launch_merge_ll(const long long* pm1, const long long* pm2, const int* pi1,
                      double ratio, int* best, double* d1, double* d2, uint8_t* keep, cudaStream_t st);
 
 template <int KB>
-static int launch_tc(const uint8_t* a, int na, const uint8_t* b, int nb, double ratio, int ex_lo, int ex_hi, int* best,
-                     double* d1, double* d2, uint8_t* keep, cudaStream_t st) {
+static int launch_tc(const uint8_t* a, int na, const uint8_t* b, int nb, double ratio, int ex_lo, int ex_hi,
+                     const int2* row_ex, int* best, double* d1, double* d2, uint8_t* keep, cudaStream_t st) {
     using G = TcGeom<KB>;
     static bool configured = false;
     if (!configured) {
@@ -353,8 +362,10 @@ static int launch_tc(const uint8_t* a, int na, const uint8_t* b, int nb, double 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int qtiles = (na + kTcM - 1) / kTcM;
     const int n_tiles = (nb + kTcN - 1) / kTcN;
-    int slices = (sms + qtiles - 1) / qtiles;  // fill the GPU with (query tile, slice) CTAs
-    if (slices > n_tiles) slices = n_tiles;
+    // (query tile, slice) CTAs: about four waves of two CTAs per SM, so long
+    // reference sets are split even when there are few query tiles
+    int slices = (8 * sms + qtiles - 1) / qtiles;
+    if (slices > n_tiles / 8) slices = n_tiles / 8;  // >= 8 tiles per CTA: amortise setup and the merge
     if (slices < 1) slices = 1;
     const int per = (n_tiles + slices - 1) / slices;
     slices = (n_tiles + per - 1) / per;
@@ -374,7 +385,7 @@ static int launch_tc(const uint8_t* a, int na, const uint8_t* b, int nb, double 
     row_norms_i8_kernel<<<(n_pad + 255) / 256, 256, 0, st>>>(b, nb, G::KBYTES, norms, n_pad, neq);
     count_launch();
     match_i8_tc_kernel<KB><<<dim3(qtiles, slices), kTcThreads, G::SMEM, st>>>(a, na, b, norms, neq, nb, per, ex_lo,
-                                                                             ex_hi, pm1, pm2, pi1);
+                                                                             ex_hi, row_ex, pm1, pm2, pi1);
     count_launch();
     launch_merge_ll(pm1, pm2, pi1, na, slices, 1, ratio, best, d1, d2, keep, st);
     cudaFreeAsync(scratch, st);
@@ -385,14 +396,14 @@ static int launch_tc(const uint8_t* a, int na, const uint8_t* b, int nb, double 
 // multiple of 32 (<= 128) and 16-byte aligned pointers; returns -1 when the
 // shape is not covered (caller falls back to the dp4a kernel).
 int match_i8_tensor(const uint8_t* a, int na, const uint8_t* b, int nb, int dim, double ratio, int ex_lo, int ex_hi,
-                    int* best, double* d1, double* d2, uint8_t* keep, cudaStream_t st) {
+                    const int2* row_ex, int* best, double* d1, double* d2, uint8_t* keep, cudaStream_t st) {
     if (dim % 32 != 0 || dim > 128 || ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15))
         return -1;
     switch (dim / 32) {
-        case 1: return launch_tc<1>(a, na, b, nb, ratio, ex_lo, ex_hi, best, d1, d2, keep, st);
-        case 2: return launch_tc<2>(a, na, b, nb, ratio, ex_lo, ex_hi, best, d1, d2, keep, st);
-        case 3: return launch_tc<3>(a, na, b, nb, ratio, ex_lo, ex_hi, best, d1, d2, keep, st);
-        default: return launch_tc<4>(a, na, b, nb, ratio, ex_lo, ex_hi, best, d1, d2, keep, st);
+        case 1: return launch_tc<1>(a, na, b, nb, ratio, ex_lo, ex_hi, row_ex, best, d1, d2, keep, st);
+        case 2: return launch_tc<2>(a, na, b, nb, ratio, ex_lo, ex_hi, row_ex, best, d1, d2, keep, st);
+        case 3: return launch_tc<3>(a, na, b, nb, ratio, ex_lo, ex_hi, row_ex, best, d1, d2, keep, st);
+        default: return launch_tc<4>(a, na, b, nb, ratio, ex_lo, ex_hi, row_ex, best, d1, d2, keep, st);
     }
 }
 

@@ -87,6 +87,30 @@ def match_database(local: dict, ratio_max: float = 0.9, metric: str = "euclidean
     d_rows = t.from_numpy(np.ascontiguousarray(rows)).cuda()
     db, _, ranges = gather_database(d_rows, t.from_numpy(subj).cuda(), group)
     out = {}
+    dim = db.shape[1]
+    if code == 1 and dim % 32 == 0 and dim <= 128 and len(rows):
+        # one tensor-core launch for every local query row, each excluding its
+        # own subject's rows (vk_match_rows_excluding)
+        n = len(rows)
+        ex = np.empty((n, 2), dtype=np.int32)
+        off = 0
+        for i, a in zip(ids, arrs):
+            ex[off: off + len(a)] = ranges[i]
+            off += len(a)
+        row_ex = t.from_numpy(ex).cuda()
+        best = t.empty(n, dtype=t.int32, device="cuda")
+        d1 = t.empty(n, dtype=t.float64, device="cuda")
+        d2 = t.empty(n, dtype=t.float64, device="cuda")
+        keep = t.empty(n, dtype=t.uint8, device="cuda")
+        _lib.call("vk_match_rows_excluding", d_rows.data_ptr(), n, db.data_ptr(), db.shape[0], dim, float(ratio_max),
+                  row_ex.data_ptr(), best.data_ptr(), d1.data_ptr(), d2.data_ptr(), keep.data_ptr(), _lib.stream_ptr())
+        hb, h1, h2, hk = best.cpu().numpy(), d1.cpu().numpy(), d2.cpu().numpy(), keep.cpu().numpy()
+        off = 0
+        for i, a in zip(ids, arrs):
+            sl = slice(off, off + len(a))
+            out[i] = (hb[sl], h1[sl], h2[sl], hk[sl])
+            off += len(a)
+        return out
     off = 0
     for i, a in zip(ids, arrs):
         q = d_rows[off: off + len(a)]

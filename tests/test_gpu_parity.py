@@ -424,13 +424,16 @@ def test_database_matching_single_rank():
         s.close()
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("nccl", rank=0, world_size=1)
+    bits = {i: rng.integers(0, 256, size=(int(rng.integers(20, 60)), 8)).astype(np.uint8) for i in range(5)}
     try:
-        got = match_database(subjects, 0.9, "euclidean")
+        got = match_database(subjects, 0.9, "euclidean")   # one tensor-core launch, per-row exclusions
+        got_h = match_database(bits, 0.9, "hamming")         # popcount kernel, per subject
     finally:
         dist.destroy_process_group()
-    for i, a in subjects.items():
-        others = np.concatenate([subjects[j] for j in sorted(subjects) if j != i])
-        ref = O.nn_match(a, others, 0.9, "euclidean")
-        best, d1, d2, keep = got[i]
-        mine = [(q, int(best[q]), float(d1[q]), float(d2[q])) for q in np.flatnonzero(keep)]
-        assert mine == ref, f"subject {i}"
+    for subj, res, metric in ((subjects, got, "euclidean"), (bits, got_h, "hamming")):
+        for i, a in subj.items():
+            others = np.concatenate([subj[j] for j in sorted(subj) if j != i])
+            ref = O.nn_match(a, others, 0.9, metric)
+            best, d1, d2, keep = res[i]
+            mine = [(q, int(best[q]), float(d1[q]), float(d2[q])) for q in np.flatnonzero(keep)]
+            assert mine == ref, f"{metric} subject {i}"
