@@ -280,6 +280,38 @@ def test_brain_volume():
 
 
 @pytest.mark.slow
+@pytest.mark.slow
+def test_large_volume_configs3():
+    """configs[3]: 256^3 soup volume, num_octaves=4 -> 9228 keypoints / 16509
+    frames; every keypoint field, frame rotation and descriptor of all three
+    kinds hash-equal to the reference's (tests/golden/large256.npz)."""
+    g = load_golden("large256.npz")
+    vol = synthetic.soup_volume((256, 256, 256), np.random.default_rng(synthetic.BRAIN_SEED), noise=0.01)
+    assert sha(vol) == str(g["input_sha"])
+    for kind in ("siftrank", "brief", "rrief"):
+        res = vk.extract_features(vk.Volume(vol), PipelineConfig(num_octaves=4, descriptor=kind))
+        kps = res.keypoints
+        if kind == "siftrank":
+            arrays = dict(
+                kp_pos=np.array([k.position for k in kps], dtype=np.float64).reshape(-1, 3),
+                kp_sigma=np.array([k.sigma for k in kps], dtype=np.float64),
+                kp_octave=np.array([k.octave for k in kps], dtype=np.int32),
+                kp_level=np.array([k.level for k in kps], dtype=np.int32),
+                kp_dog=np.array([k.dog_value for k in kps], dtype=np.float64),
+                kp_sign=np.array([1 if k.sign == "peak" else -1 for k in kps], dtype=np.int8))
+            idx = {id(k): i for i, k in enumerate(kps)}
+            arrays["fr_kp"] = np.array([idx[id(k)] for k, _ in res.oriented], dtype=np.int32)
+            arrays["fr_rot"] = np.array([f.rotation for _, f in res.oriented], dtype=np.float64).reshape(-1, 3, 3)
+            for k, v in arrays.items():
+                assert len(v) == int(g[k + "_len"]) and sha(v) == str(g[k + "_sha"]), k
+            got = np.array([[sha(lv.data) for lv in o.levels] for o in res.pyramid.octaves])
+            assert np.array_equal(got, g["pyr_sha"]), "gaussian pyramid differs"
+            got = np.array([[sha(lv.data) for lv in o.levels] for o in res.dog.octaves])
+            assert np.array_equal(got, g["dog_sha"]), "DoG pyramid differs"
+        desc = vk.descriptor.descriptor_array(res.records, kind).astype(np.uint8)
+        assert len(desc) == int(g[f"desc_{kind}_len"]) and sha(desc) == str(g[f"desc_{kind}_sha"]), kind
+
+
 def test_fast_and_exact_accumulation_agree():
     """The bounded parallel accumulation must give the same frames and ranks
     as forcing the reference-order accumulation everywhere."""
