@@ -183,8 +183,10 @@ long long vk_accum_work_bytes(int device);
  * orient.py:339-343).  Outputs: weights (n x K fp64, nullable), nframes[n],
  * prim/sec[n*max_frames].  status[1] counts exact-order fallbacks.  status[0] |= 1 when a keypoint's neighbourhood lies
  * outside its volume (DataError, orient.py:291-292).  ico_host (nullable, K==42
- * only): 12 icosahedron-vertex indices into dirs followed by 12x5 indices of
- * the edge midpoints around each vertex, enabling the screened argmax.
+ * only): int[132] = 12 icosahedron-vertex indices into dirs, 12x5 indices of
+ * the edge midpoints around each vertex, and the same 12x5 midpoints ordered
+ * by neighbour kind (tables.icosphere_structure), enabling the screened and
+ * the fast argmax.
  * exact_only != 0 forces the reference accumulation order and the brute-force
  * argmax for every keypoint (weights then bit-identical to the reference).
  * grads (nullable, indexed like levels): precomputed gradient volumes

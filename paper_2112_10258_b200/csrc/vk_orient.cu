@@ -74,11 +74,13 @@ struct IcoT {
     int valid;
     int vert[12];  // vertex of construction order 6*a + 3*b + group (tables.icosphere_structure)
     int adj[12][5];
+    int kind[12][5];  // the same midpoints by neighbour kind (fast argmax)
 };
 
 struct IcoSh {
     float4 cd[12 * 6];  // per vertex slot: the vertex and its 5 midpoints (fp32 xyz)
     int ci[12 * 6];     // their direction indices
+    int fk[12 * 6];     // per vertex slot: the vertex, then its midpoints by kind
 };
 
 // Rare path (kept out of line so its fp64 work is never hoisted): exact
@@ -104,13 +106,71 @@ __device__ __noinline__ int nearest_dir_ico_exact(const double* dirs, const IcoS
     return bi;
 }
 
+// Fast exact argmax for the common case: one icosahedron vertex clearly
+// nearest (its group value leads the others by more than the screen margin and
+// both of its signs are clear).  The nearest of the 42 directions is then the
+// vertex or one of its 5 edge midpoints, and all of those scores follow from
+// |g| components: in the winning group's axes (p, q, r) the vertex scores
+// (|p| + phi|q|) / |V| and the midpoint with neighbour W scores
+// (V.g + W.g) / (2 phi) with W.g in {phi|p| +- |r|, |q| +- phi|r|, phi|q| - |p|}.
+// Each score is within ~3e-7 |g|_1 of the exact dot, so a winner clear of the
+// runner-up by 2e-6 |g|_1 is the exact np.argmax; otherwise the caller falls
+// back.  Returns -1 when the fast case does not apply or is not certain.
+VK_D int nearest_dir_fast(const IcoSh& ic, float gx, float gy, float gz, float ax, float ay, float az, float l1,
+                          float vA, float vB, float vC, float m) {
+    constexpr float PHI = 1.6180339887498949f;
+    constexpr float CV = 0.52573111211913359f;  // 1 / sqrt(2 + phi)
+    constexpr float CM = 0.30901699437494742f;  // 1 / (2 phi)
+    // winning group and its (p, q, r) = (+-1 axis, +-phi axis, zero axis)
+    float best, second, p, q, r, gp, gq, gr;
+    int grp;
+    if (vA >= vB && vA >= vC) {
+        best = vA; second = fmaxf(vB, vC); grp = 0; p = ay; q = az; r = ax; gp = gy; gq = gz; gr = gx;
+    } else if (vB >= vC) {
+        best = vB; second = fmaxf(vA, vC); grp = 1; p = ax; q = ay; r = az; gp = gx; gq = gy; gr = gz;
+    } else {
+        best = vC; second = fmaxf(vA, vB); grp = 2; p = az; q = ax; r = ay; gp = gz; gq = gx; gr = gy;
+    }
+    if (!(best - second > m) || 2.f * p <= m || 2.f * PHI * q <= m) return -1;
+    const int slot = 6 * (gp > 0.f) + 3 * (gq > 0.f) + grp;
+    const float c0 = CV * best;
+    const float c1 = CM * (best + fmaf(PHI, p, r)), c2 = CM * (best + fmaf(PHI, p, -r));
+    const float c3 = CM * (best + fmaf(PHI, r, q)), c4 = CM * (best + fmaf(-PHI, r, q));
+    const float c5 = CM * (best + fmaf(PHI, q, -p));
+    // top two of six (pairwise, then across the pair winners)
+    const bool s01 = c0 >= c1, s23 = c2 >= c3, s45 = c4 >= c5;
+    const float m01 = s01 ? c0 : c1, n01 = s01 ? c1 : c0;
+    const float m23 = s23 ? c2 : c3, n23 = s23 ? c3 : c2;
+    const float m45 = s45 ? c4 : c5, n45 = s45 ? c5 : c4;
+    float b1, b2;
+    int w;
+    if (m01 >= m23 && m01 >= m45) {
+        b1 = m01; b2 = fmaxf(n01, fmaxf(m23, m45)); w = s01 ? 0 : 1;
+    } else if (m23 >= m45) {
+        b1 = m23; b2 = fmaxf(n23, fmaxf(m01, m45)); w = s23 ? 2 : 3;
+    } else {
+        b1 = m45; b2 = fmaxf(n45, fmaxf(m01, m23)); w = s45 ? 4 : 5;
+    }
+    if (!(b1 - b2 > 2.0e-6f * l1)) return -1;
+    // candidate -> neighbour kind: c1/c2 = (p-phi, r sign == / != sign(g_r)), c3/c4 likewise, c5
+    const bool rp = gr > 0.f;
+    int kind = w;  // 0: the vertex itself
+    if (w == 1) kind = rp ? 1 : 2;
+    else if (w == 2) kind = rp ? 2 : 1;
+    else if (w == 3) kind = rp ? 3 : 4;
+    else if (w == 4) kind = rp ? 4 : 3;
+    return ic.fk[6 * slot + kind];
+}
+
 VK_D int nearest_dir_ico(const double* dirs, const IcoSh& ic, float gx, float gy, float gz, const Nb6& nb) {
     constexpr float PHI = 1.6180339887498949f;
     const float ax = fabsf(gx), ay = fabsf(gy), az = fabsf(gz);
     const float l1 = ax + ay + az;
     const float vA = fmaf(PHI, az, ay), vB = fmaf(PHI, ay, ax), vC = fmaf(PHI, ax, az);
-    const float best = fmaxf(vA, fmaxf(vB, vC));
     const float m = 1.0e-5f * 2.7f * l1;
+    const int fast = nearest_dir_fast(ic, gx, gy, gz, ax, ay, az, l1, vA, vB, vC, m);
+    if (fast >= 0) return fast;
+    const float best = fmaxf(vA, fmaxf(vB, vC));
     // candidate vertex slots: construction index 6*a + 3*b + group, a/b = 1 for the + sign
     unsigned slots = 0;
     auto add_group = [&](float v, int grp, float ca, float cb, float wa, float wb) {
@@ -184,6 +244,7 @@ gradient_volume_kernel(const float* __restrict__ level, float4* __restrict__ g4,
         const int k = c == 0 ? ico.vert[v] : ico.adj[v][c - 1];
         ic.ci[tid] = k;
         ic.cd[tid] = make_float4((float)dirs_g[3 * k], (float)dirs_g[3 * k + 1], (float)dirs_g[3 * k + 2], 0.f);
+        ic.fk[tid] = c == 0 ? ico.vert[v] : ico.kind[v][c - 1];
     }
     __syncthreads();
     const long long vol = (long long)nx * ny * nz;
@@ -294,6 +355,7 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         const int k = c == 0 ? ico.vert[v] : ico.adj[v][c - 1];
         ic.ci[tid] = k;
         ic.cd[tid] = make_float4((float)dirs_g[3 * k], (float)dirs_g[3 * k + 1], (float)dirs_g[3 * k + 2], 0.f);
+        ic.fk[tid] = c == 0 ? ico.vert[v] : ico.kind[v][c - 1];
     }
     for (int i = tid; i < K * K; i += kOriThreads) sh.ok[i] = pair_ok[i];
     const int n_kp = n_kp_dev ? min(*n_kp_dev, n_kp_max) : n_kp_max;
@@ -569,6 +631,7 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
         for (int v = 0; v < 12; ++v) {
             ico.vert[v] = ico_host[v];
             for (int m = 0; m < 5; ++m) ico.adj[v][m] = ico_host[12 + 5 * v + m];
+            for (int m = 0; m < 5; ++m) ico.kind[v][m] = ico_host[72 + 5 * v + m];
         }
     }
     orient_kernel<<<grid, kOriThreads, 0, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
@@ -629,6 +692,7 @@ extern "C" int vk_gradient_volume(const float* level, void* g4, uint8_t* bin, in
     for (int v = 0; v < 12; ++v) {
         ico.vert[v] = ico_host[v];
         for (int m = 0; m < 5; ++m) ico.adj[v][m] = ico_host[12 + 5 * v + m];
+        for (int m = 0; m < 5; ++m) ico.kind[v][m] = ico_host[72 + 5 * v + m];
     }
     long long blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;

@@ -81,9 +81,12 @@ def icosphere_directions() -> np.ndarray:
 
 @lru_cache(maxsize=1)
 def icosphere_structure() -> np.ndarray:
-    """int32[12 + 60]: indices (into icosphere_directions()) of the 12
-    icosahedron vertices, then for each vertex the 5 edge midpoints around it.
-    Enables the screened exact argmax of csrc/vk_orient.cu."""
+    """int32[12 + 60 + 60]: indices (into icosphere_directions()) of the 12
+    icosahedron vertices, then for each vertex the 5 edge midpoints around it,
+    then for each vertex the same 5 midpoints by neighbour kind for the fast
+    argmax of csrc/vk_orient.cu: vertex (p: +-1, q: +-phi, r: 0) in its group's
+    (p, q, r) axes meets (p: s_p phi, r: +1), (p: s_p phi, r: -1),
+    (q: s_q, r: +phi), (q: s_q, r: -phi), (p: -s_p, q: s_q phi)."""
     dirs = icosphere_directions()
     phi = (1.0 + math.sqrt(5.0)) / 2.0
     pts = []
@@ -104,7 +107,24 @@ def icosphere_structure() -> np.ndarray:
                 mids.append(int(np.argmin(np.linalg.norm(dirs - m / np.linalg.norm(m), axis=1))))
         assert len(mids) == 5
         adj.append(sorted(mids))
-    out = np.array(vidx + [m for a in adj for m in a], dtype=np.int32)
+    fast = []
+    axes = {0: (1, 2, 0), 1: (0, 1, 2), 2: (2, 0, 1)}  # group -> (p, q, r) axes (+-1, +-phi, 0 coordinates)
+    for s in range(12):
+        grp = s % 3
+        pa, qa, ra = axes[grp]
+        V = np.array(pts[s])
+        sp, sq = np.sign(V[pa]), np.sign(V[qa])
+        kinds = []
+        for coef in ((sp * phi, 0.0, 1.0), (sp * phi, 0.0, -1.0), (0.0, sq, phi), (0.0, sq, -phi), (-sp, sq * phi, 0.0)):
+            W = np.zeros(3)
+            W[pa], W[qa], W[ra] = coef
+            assert abs(np.sum((V - W) ** 2) - 4.0) < 1e-9  # an icosahedron edge
+            m = V / np.linalg.norm(V) + W / np.linalg.norm(W)
+            k = int(np.argmin(np.linalg.norm(dirs - m / np.linalg.norm(m), axis=1)))
+            assert k in adj[s]
+            kinds.append(k)
+        fast += kinds
+    out = np.array(vidx + [m for a in adj for m in a] + fast, dtype=np.int32)
     assert len(set(vidx)) == 12
     out.setflags(write=False)
     return out

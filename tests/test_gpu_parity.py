@@ -250,6 +250,38 @@ def test_gradient_histograms_exact(name):
         assert np.array_equal(h.weights, g["hist"][i]), f"keypoint {i}"
 
 
+def test_nearest_direction_exact_on_dense_gradients():
+    """The screened / fast icosphere argmax (csrc/vk_orient.cu) on every voxel
+    of blurred random and quantised volumes (millions of gradients, incl.
+    exact ties and axis-aligned gradients) == np.argmax of the reference's
+    fp64 dots g @ dirs.T (orient.py:89-125), zero gradients -> 255."""
+    import torch
+
+    from oracle import volkey_oracle as O
+    from paper_2112_10258_b200 import _lib, tables
+
+    dirs = tables.icosphere_directions()
+    ico = np.ascontiguousarray(tables.icosphere_structure())
+    d_dirs = torch.from_numpy(np.ascontiguousarray(dirs)).cuda()
+    rng = np.random.default_rng(17)
+    r, w = O.gauss_taps(1.2)
+    smooth = O.blur3(rng.standard_normal((48, 40, 36)).astype(np.float32), w)
+    for vol in (smooth, np.round(smooth * 64.0).astype(np.float32) / 64.0,
+                (rng.integers(0, 3, size=(40, 40, 40)) * 0.5).astype(np.float32)):
+        nx, ny, nz = vol.shape
+        xf = torch.from_numpy(np.ascontiguousarray(vol.transpose(2, 1, 0))).cuda()
+        g4 = torch.empty((nz, ny, nx, 4), dtype=torch.float32, device="cuda")
+        bins = torch.empty((nz, ny, nx), dtype=torch.uint8, device="cuda")
+        _lib.call("vk_gradient_volume", xf.data_ptr(), g4.data_ptr(), bins.data_ptr(), 1, nx, ny, nz,
+                  d_dirs.data_ptr(), ico.ctypes.data, _lib.stream_ptr())
+        got = bins.cpu().numpy().transpose(2, 1, 0).reshape(-1)
+        idx = np.indices(vol.shape).reshape(3, -1).T
+        g = O.grads_at(vol, idx)
+        want = np.argmax(g @ dirs.T, axis=1)
+        want[np.all(g == 0.0, axis=1)] = 255
+        assert np.array_equal(got, want)
+
+
 def test_stage_api_composition():
     """build_gaussian_pyramid -> build_dog_pyramid -> detect_keypoints ->
     assign_orientations -> describe_all, the composition of
