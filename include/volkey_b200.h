@@ -122,6 +122,17 @@ int vk_transpose_xfast_to_zfast(const float* src, float* dst, int nb, int nx, in
 int vk_blur3d(const float* src, float* dst, float* dog_out, float* half_out,
               int nb, int nx, int ny, int nz, const float* taps_host, int radius, void* stream);
 
+/* vk_blur3d with caller-owned scratch for the split (x, y) + z path: work
+ * holds work_floats floats (>= nb*nx*ny*nz, else the call allocates its own,
+ * stream-ordered). */
+int vk_blur3d_ws(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny, int nz,
+                 const float* taps_host, int radius, float* work, long long work_floats, void* stream);
+
+/* Blur kernel selection: 0 = split (x, y) kernel + z kernel through an
+ * intermediate level (default), 1 = fused single-pass streaming kernel.
+ * Results are bit-identical. */
+int vk_set_blur_path(int path);
+
 /* The tail of the pyramid in one launch (scalespace.py:186-251 for octaves
  * whose levels hold <= 16384 voxels): one CTA per volume runs every level of
  * octaves 0..n_oct-1 of this call in shared memory.  dims_host: 3 per octave;

@@ -17,6 +17,7 @@
 //    minus the coarser one), and the ordered 2x2x2 mean of the handoff level
 //    for the next octave (needs even tile origins and an even z start).
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "vk_common.cuh"
 
@@ -107,6 +108,37 @@ VK_D void z_dispatch(int c, float2 (&r0)[2 * R + 1], float2 (&r1)[2 * R + 1], fl
         constexpr int MID = (LO + HI) / 2;
         if (c < MID) z_dispatch<R, LO, MID>(c, r0, r1, v0, v1, taps, o0, o1);
         else z_dispatch<R, MID, HI>(c, r0, r1, v0, v1, taps, o0, o1);
+    }
+}
+
+// Single-ring variant (one float2 column pair per thread) for blur_z_kernel.
+template <int R, int C>
+VK_D float2 z_arrive1(float2 (&r0)[2 * R + 1], float2 v0, const Taps& taps) {
+    constexpr int P = 2 * R + 1;
+#pragma unroll
+    for (int d = 0; d <= R; ++d) {
+        const float w = taps.w[R + d];
+        const float2 p0 = fmul2(make_float2(w, w), v0);
+        if (d == 0) {
+            acc2(r0[C], p0);
+        } else {
+            const int up = (C + d) % P, dn = (C - d + P) % P;
+            if (d == R) r0[up] = p0;
+            else acc2(r0[up], p0);
+            acc2(r0[dn], p0);
+        }
+    }
+    return r0[(C - R + P) % P];
+}
+
+template <int R, int LO, int HI>
+VK_D float2 z_dispatch1(int c, float2 (&r0)[2 * R + 1], float2 v0, const Taps& taps) {
+    if constexpr (HI - LO == 1) {
+        return z_arrive1<R, LO>(r0, v0, taps);
+    } else {
+        constexpr int MID = (LO + HI) / 2;
+        if (c < MID) return z_dispatch1<R, LO, MID>(c, r0, v0, taps);
+        return z_dispatch1<R, MID, HI>(c, r0, v0, taps);
     }
 }
 
@@ -314,6 +346,195 @@ blur3d_stream_kernel(const float* __restrict__ src, float* __restrict__ dst, flo
             ++a;
             c = (c + 1 == P) ? 0 : c + 1;
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Split blur: an (x, y) pass kernel writing an intermediate level, then a z
+// pass kernel with the fused epilogues.  Same arithmetic as above (x, then y,
+// then z; every product rounded, sums in tap order; the z pass in accumulator
+// form with one product per tap distance), but two simple kernels: no z ring
+// in the (x, y) kernel (short-lived CTAs, one plane each, high occupancy) and
+// no shared memory or barriers in the z kernel (one column pair per thread,
+// coalesced loads).  The intermediate costs 8 more HBM bytes per voxel; both
+// kernels then run near their own roofline.
+constexpr int kXyTX = 32;  // (x, y) tile of the xy kernel
+constexpr int kXyTY = 64;
+
+template <int R>
+struct XyGeom {
+    static constexpr int ROWS = kXyTY + 2 * R;        // even
+    static constexpr int RP = ROWS / 2;
+    static constexpr int COLS = kXyTX + 2 * R;
+    static constexpr int COLSP = ((COLS + 15) / 16) * 16 + 1;
+    static constexpr int IN_F2 = (RP * COLSP + 1) & ~1;  // even: x_s stays 16-byte aligned
+    static constexpr int XS = kXyTX + 4;
+    static constexpr int SMEM = (IN_F2 * 2 + ROWS * XS + ROWS) * 4;
+    static constexpr int ITEMS = RP * 4;               // x-pass items: row pair x 8-output segment
+};
+
+template <int R>
+__global__ void __launch_bounds__(kThreads, 4)
+blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, int ny, int nz, Taps taps) {
+    using G = XyGeom<R>;
+    extern __shared__ float4 smem4[];
+    float2* in2 = reinterpret_cast<float2*>(smem4);
+    float* x_s = reinterpret_cast<float*>(in2 + G::IN_F2);
+    unsigned* roff_s = reinterpret_cast<unsigned*>(x_s + G::ROWS * G::XS);
+    const int bz = blockIdx.z;  // b * nz + z
+    const int x0 = blockIdx.x * kXyTX, y0 = blockIdx.y * kXyTY;
+    const unsigned plane = (unsigned)nx * (unsigned)ny;
+    const unsigned pbase = (unsigned)bz * plane;
+    const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+    for (int r = tid; r < G::ROWS; r += kThreads) roff_s[r] = pbase + (unsigned)clampi(y0 - R + r, 0, ny - 1) * (unsigned)nx;
+    __syncthreads();
+    // stage the clamped plane tile into the row-pair interleaved layout
+    {
+        const unsigned cx0 = (unsigned)clampi(x0 - R + lane, 0, nx - 1);
+        const unsigned cx1 = (unsigned)clampi(x0 - R + lane + 32, 0, nx - 1);
+        float* d = reinterpret_cast<float*>(in2) + ((wy >> 1) * G::COLSP + lane) * 2 + (wy & 1);
+#pragma unroll 4
+        for (int k = 0; wy + 8 * k < G::ROWS; ++k) {
+            const unsigned ro = roff_s[wy + 8 * k];
+            cp_async4(d + k * 8 * G::COLSP, src + (ro + cx0));
+            if (lane + 32 < G::COLS) cp_async4(d + k * 8 * G::COLSP + 64, src + (ro + cx1));
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+    }
+    __syncthreads();
+    // x-pass: items (row pair, 8-output segment), 2 rows x 8 outputs each
+    for (int it = tid; it < G::ITEMS; it += kThreads) {
+        const int rp = it >> 2, sg = it & 3;
+        const float2* row = in2 + rp * G::COLSP + 8 * sg;
+        float2 acc[8];
+#pragma unroll
+        for (int i = 0; i < 8 + 2 * R; ++i) {
+            const float2 v = row[i];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int t = i - k;
+                if (t < 0 || t > 2 * R) continue;
+                const int dd = t < R ? R - t : t - R;
+                const float w = taps.w[R + dd];
+                const float2 pr = fmul2(make_float2(w, w), v);
+                if (t == 0) acc[k] = pr;
+                else acc2(acc[k], pr);
+            }
+        }
+        float4* xa = reinterpret_cast<float4*>(x_s + (2 * rp) * G::XS + 8 * sg);
+        float4* xb = reinterpret_cast<float4*>(x_s + (2 * rp + 1) * G::XS + 8 * sg);
+        xa[0] = make_float4(acc[0].x, acc[1].x, acc[2].x, acc[3].x);
+        xa[1] = make_float4(acc[4].x, acc[5].x, acc[6].x, acc[7].x);
+        xb[0] = make_float4(acc[0].y, acc[1].y, acc[2].y, acc[3].y);
+        xb[1] = make_float4(acc[4].y, acc[5].y, acc[6].y, acc[7].y);
+    }
+    __syncthreads();
+    // y-pass: column pair cp (16), row quad yq (16): 2 x 4 outputs per thread
+    const int cp = tid & 15, yq = tid >> 4;
+    const float* col = x_s + (4 * yq) * G::XS + 2 * cp;
+    float2 o[4];
+#pragma unroll
+    for (int i = 0; i < 4 + 2 * R; ++i) {
+        const float2 v = *reinterpret_cast<const float2*>(col + i * G::XS);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int t = i - k;
+            if (t < 0 || t > 2 * R) continue;
+            const int dd = t < R ? R - t : t - R;
+            const float w = taps.w[R + dd];
+            const float2 pr = fmul2(make_float2(w, w), v);
+            if (t == 0) o[k] = pr;
+            else acc2(o[k], pr);
+        }
+    }
+    const int gx = x0 + 2 * cp;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int gy = y0 + 4 * yq + k;
+        if (gy < ny) {
+            float* t = tmp + (pbase + (unsigned)gy * (unsigned)nx + (unsigned)gx);
+            if (gx < nx) t[0] = o[k].x;
+            if (gx + 1 < nx) t[1] = o[k].y;
+        }
+    }
+}
+
+// z pass over the (x, y)-blurred intermediate: thread = column pair
+// (gx, gx+1) of row gy; warp = 16 column pairs x rows (y, y+1) so the 2x2x2
+// subsample block of a thread is completed by lane ^ 16.  Planes outside
+// [0, nz) are the clamped border plane (re-read, L1-resident).
+template <int R>
+__global__ void __launch_bounds__(kThreads)
+blur_z_kernel(const float* __restrict__ tmp, const float* __restrict__ src, float* __restrict__ dst,
+              float* __restrict__ dog, float* __restrict__ half, int nx, int ny, int nz, int tz, int nzc, Taps taps) {
+    constexpr int P = 2 * R + 1;
+    const int b = blockIdx.z / nzc;
+    const int zc = blockIdx.z - b * nzc;
+    const int z_start = zc * tz;
+    const int z_end = min(nz, z_start + tz);
+    const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+    const int gx = blockIdx.x * 32 + 2 * (lane & 15);
+    const int gy = blockIdx.y * 16 + 2 * wy + (lane >> 4);
+    const bool okx0 = gx < nx, okx1 = gx + 1 < nx, oky = gy < ny;
+    const unsigned plane = (unsigned)nx * (unsigned)ny;
+    const unsigned vbase = (unsigned)b * plane * (unsigned)nz;
+    const unsigned e0 = vbase + (unsigned)min(gy, ny - 1) * (unsigned)nx + (unsigned)min(gx, nx - 1);
+    const unsigned cst = okx1 ? 1u : 0u;
+    float2 r0[P];
+#pragma unroll
+    for (int t = 0; t < P; ++t) r0[t] = make_float2(0.f, 0.f);
+    float2 pv = make_float2(0.f, 0.f);
+    const int za = z_start - R, zb = z_end - 1 + R;
+    auto ld = [&](int zp) {
+        const float* t = tmp + (e0 + (unsigned)clampi(zp, 0, nz - 1) * plane);
+        return make_float2(__ldg(t), __ldg(t + cst));
+    };
+    float2 vn = ld(za);
+    int c = 0;
+    for (int zp = za; zp <= zb; ++zp) {
+        const float2 v = vn;
+        if (zp < zb) vn = ld(zp + 1);
+        float2 sv = make_float2(0.f, 0.f);
+        const int zo = zp - R;
+        const bool out = zo >= z_start;
+        if (out && dog != nullptr) {
+            const float* sp = src + (e0 + (unsigned)zo * plane);
+            sv = make_float2(__ldg(sp), __ldg(sp + cst));
+        }
+        const float2 o = z_dispatch1<R, 0, P>(c, r0, v, taps);
+        c = (c + 1 == P) ? 0 : c + 1;
+        if (!out) continue;
+        float* dv = dst + (e0 + (unsigned)zo * plane);
+        if (oky) {
+            if (okx0) dv[0] = o.x;
+            if (okx1) dv[1] = o.y;
+        }
+        if (dog != nullptr && oky) {
+            float* gv = dog + (e0 + (unsigned)zo * plane);
+            if (okx0) gv[0] = __fsub_rn(sv.x, o.x);
+            if (okx1) gv[1] = __fsub_rn(sv.y, o.y);
+        }
+        if (half != nullptr) {
+            // (dx, dy, dz) order of scalespace.py:129-135: this thread holds
+            // rows y (lanes 0-15) or y+1 (lanes 16-31) of planes zo-1 (pv), zo (o)
+            const float2 qv = make_float2(__shfl_xor_sync(0xffffffffu, pv.x, 16), __shfl_xor_sync(0xffffffffu, pv.y, 16));
+            const float2 qo = make_float2(__shfl_xor_sync(0xffffffffu, o.x, 16), __shfl_xor_sync(0xffffffffu, o.y, 16));
+            const int hnx = nx >> 1, hny = ny >> 1, hnz = nz >> 1;
+            const int hx = gx >> 1, hy = gy >> 1, hz = zo >> 1;
+            if ((zo & 1) && lane < 16 && hx < hnx && hy < hny && hz < hnz) {
+                float sm = pv.x;
+                sm = fadd(sm, o.x);
+                sm = fadd(sm, qv.x);
+                sm = fadd(sm, qo.x);
+                sm = fadd(sm, pv.y);
+                sm = fadd(sm, o.y);
+                sm = fadd(sm, qv.y);
+                sm = fadd(sm, qo.y);
+                half[(((long long)b * hnz + hz) * hny + hy) * hnx + hx] = fmul(sm, 0.125f);
+            }
+        }
+        pv = o;
     }
 }
 
@@ -540,6 +761,44 @@ static int launch_ring(const float* src, float* dst, float* dog, float* half, in
     return cuda_status(cudaGetLastError(), "blur3d launch");
 }
 
+// Split path: (x, y) kernel into `work` (nb * volume floats), then the z kernel.
+static int kZWaves = 4, kZMinChunkR = 4;  // z chunking (tuned on B200; env-overridable for sweeps)
+template <int R>
+static int launch_split(const float* src, float* dst, float* dog, float* half, int nb, int nx, int ny, int nz,
+                        const Taps& taps, float* work, cudaStream_t st) {
+    using G = XyGeom<R>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(blur_xy_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        if (e != cudaSuccess) return cuda_status(e, "blur xy attribute");
+        configured = true;
+    }
+    static bool env_read = false;
+    if (!env_read) {
+        if (const char* e = getenv("VK_Z_WAVES")) kZWaves = atoi(e) > 0 ? atoi(e) : kZWaves;
+        if (const char* e = getenv("VK_Z_MINCHUNK")) kZMinChunkR = atoi(e) > 0 ? atoi(e) : kZMinChunkR;
+        env_read = true;
+    }
+    dim3 g1((nx + kXyTX - 1) / kXyTX, (ny + kXyTY - 1) / kXyTY, nb * nz);
+    blur_xy_kernel<R><<<g1, kThreads, G::SMEM, st>>>(src, work, nx, ny, nz, taps);
+    count_launch();
+    // z chunks: enough CTAs for ~4 waves, each chunk >= 4R planes (the 2R
+    // warm-up arrivals are overhead), even starts for the subsample epilogue
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long cols = (long long)((nx + 31) / 32) * ((ny + 15) / 16) * nb;
+    int nzc = 1;
+    while (cols * nzc < (long long)kZWaves * 8 * sms && (nz + nzc) / (nzc + 1) >= kZMinChunkR * R && nzc < 64) ++nzc;
+    int tz = (nz + nzc - 1) / nzc;
+    tz += tz & 1;
+    nzc = (nz + tz - 1) / tz;
+    dim3 g2((nx + 31) / 32, (ny + 15) / 16, nb * nzc);
+    blur_z_kernel<R><<<g2, kThreads, 0, st>>>(work, src, dst, dog, half, nx, ny, nz, tz, nzc, taps);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "blur split launch");
+}
+
 static int launch_generic(const float* src, float* dst, float* dog, float* half, int nb, int nx, int ny, int nz,
                           int R, const Taps& taps, cudaStream_t st) {
     const long long total = (long long)nb * nx * ny * nz;
@@ -573,10 +832,23 @@ static int launch_generic(const float* src, float* dst, float* dog, float* half,
 
 using namespace vk;
 
-extern "C" int vk_blur3d(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny,
-                         int nz, const float* taps_host, int radius, void* stream) {
+// 0: split (x, y) + z kernels (default), 1: fused streaming kernel.
+static int g_blur_path = 0;
+
+extern "C" int vk_set_blur_path(int path) {
+    if (path < 0 || path > 1) {
+        set_error("vk_set_blur_path: path must be 0 (split xy + z) or 1 (fused streaming)");
+        return VK_ERR_PARAMETER;
+    }
+    g_blur_path = path;
+    return VK_OK;
+}
+
+extern "C" int vk_blur3d_ws(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny,
+                            int nz, const float* taps_host, int radius, float* work, long long work_floats,
+                            void* stream) {
     if (!src || !dst || !taps_host || nb < 0 || nx < 1 || ny < 1 || nz < 1 || radius < 1 ||
-        2 * radius + 1 > VK_MAX_TAPS) {
+        2 * radius + 1 > VK_MAX_TAPS || work_floats < 0) {
         set_error("vk_blur3d: bad arguments (nb=%d dims=%d,%d,%d radius=%d)", nb, nx, ny, nz, radius);
         return VK_ERR_PARAMETER;
     }
@@ -585,13 +857,38 @@ extern "C" int vk_blur3d(const float* src, float* dst, float* dog_out, float* ha
     for (int i = 0; i < 2 * radius + 1; ++i) taps.w[i] = taps_host[i];
     cudaStream_t st = as_stream(stream);
     if (half_out && (nx < 2 || ny < 2 || nz < 2)) half_out = nullptr;
-    // The streaming kernel shares each product between the two taps at the
-    // same distance; Gaussian taps (scalespace.py:35-42) are exactly symmetric.
+    // Both kernels share each product between the two taps at the same
+    // distance; Gaussian taps (scalespace.py:35-42) are exactly symmetric.
     bool symmetric = true;
     for (int i = 0; i < radius; ++i) symmetric = symmetric && taps.w[i] == taps.w[2 * radius - i];
-    // The streaming kernel addresses the batch with 32-bit element offsets.
-    const bool small = (unsigned long long)nb * nx * ny * nz < (1ull << 32);
-    if (!symmetric || !small) return launch_generic(src, dst, dog_out, half_out, nb, nx, ny, nz, radius, taps, st);
+    // ... and address the batch with 32-bit element offsets.
+    const long long total = (long long)nb * nx * ny * nz;
+    const bool small = (unsigned long long)total < (1ull << 32);
+    if (!symmetric || !small || radius > kMaxRingR)
+        return launch_generic(src, dst, dog_out, half_out, nb, nx, ny, nz, radius, taps, st);
+    if (g_blur_path == 0) {
+        float* w = work;
+        const bool own = w == nullptr || work_floats < total;
+        if (own) {
+            cudaError_t e = cudaMallocAsync(&w, total * 4, st);
+            if (e != cudaSuccess) return cuda_status(e, "blur scratch");
+        }
+        int rc;
+        switch (radius) {
+            case 1: rc = launch_split<1>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
+            case 2: rc = launch_split<2>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
+            case 3: rc = launch_split<3>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
+            case 4: rc = launch_split<4>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
+            case 5: rc = launch_split<5>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
+            case 6: rc = launch_split<6>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
+            case 7: rc = launch_split<7>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
+            case 8: rc = launch_split<8>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
+            case 9: rc = launch_split<9>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
+            default: rc = launch_split<10>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
+        }
+        if (own) cudaFreeAsync(w, st);
+        return rc;
+    }
     switch (radius) {
         case 1: return launch_ring<1>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, st);
         case 2: return launch_ring<2>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, st);
@@ -602,9 +899,13 @@ extern "C" int vk_blur3d(const float* src, float* dst, float* dog_out, float* ha
         case 7: return launch_ring<7>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, st);
         case 8: return launch_ring<8>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, st);
         case 9: return launch_ring<9>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, st);
-        case 10: return launch_ring<10>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, st);
-        default: return launch_generic(src, dst, dog_out, half_out, nb, nx, ny, nz, radius, taps, st);
+        default: return launch_ring<10>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, st);
     }
+}
+
+extern "C" int vk_blur3d(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny,
+                         int nz, const float* taps_host, int radius, void* stream) {
+    return vk_blur3d_ws(src, dst, dog_out, half_out, nb, nx, ny, nz, taps_host, radius, nullptr, 0, stream);
 }
 
 extern "C" int vk_subsample_half(const float* src, float* dst, int nb, int nx, int ny, int nz, void* stream) {

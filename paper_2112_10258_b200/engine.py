@@ -177,6 +177,8 @@ class Extractor:
             self.input = input
         else:
             self.input = t.empty((B, nz, ny, nx), dtype=f32, device="cuda")
+        # (x, y)-blurred intermediate of the split blur (vk_blur3d_ws), one octave-0 level
+        self.blur_work = t.empty(B * nx * ny * nz, dtype=f32, device="cuda")
         self.levels, self.dogs = [], []
         for (ox, oy, oz) in self.plan.octave_dims:
             self.levels.append([t.empty((B, oz, oy, ox), dtype=f32, device="cuda") for _ in range(L)])
@@ -252,15 +254,15 @@ class Extractor:
             if o == 0:
                 k = P.taps[0]
                 with rec("convolution", o, 0):
-                    _lib.call("vk_blur3d", self.input.data_ptr(), lv[0].data_ptr(), None, None, B, nx, ny, nz,
-                              k.weights.ctypes.data, k.radius, s)
+                    _lib.call("vk_blur3d_ws", self.input.data_ptr(), lv[0].data_ptr(), None, None, B, nx, ny, nz,
+                              k.weights.ctypes.data, k.radius, self.blur_work.data_ptr(), self.blur_work.numel(), s)
             for i in range(1, L):
                 k = P.taps[i]
                 half = self.levels[o + 1][0].data_ptr() if (i == handoff and o + 1 < P.n_octaves) else None
                 with rec("convolution", o, i):
-                    _lib.call("vk_blur3d", lv[i - 1].data_ptr(), lv[i].data_ptr(),
+                    _lib.call("vk_blur3d_ws", lv[i - 1].data_ptr(), lv[i].data_ptr(),
                               dg[i - 1].data_ptr() if with_dog else None, half, B, nx, ny, nz,
-                              k.weights.ctypes.data, k.radius, s)
+                              k.weights.ctypes.data, k.radius, self.blur_work.data_ptr(), self.blur_work.numel(), s)
         if small < P.n_octaves:
             import ctypes as C
 

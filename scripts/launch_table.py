@@ -15,6 +15,6 @@ for k, v in sorted(data.items()):
     t = v.get("gpu__time_duration.sum", 0) / 1e3
     tot += t
     rw = (v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0)) / 1e6
-    print(f"{k[0]:3d} {k[1]:40s} {k[2]:14s} {t:9.1f} us  dram {rw:8.1f} MB  {rw / max(t, 1e-9) / 1e3:6.2f} TB/s"
+    print(f"{k[0]:3d} {k[1]:40s} {k[2]:14s} {t:9.1f} us  dram {rw:8.1f} MB  {rw / max(t, 1e-9):6.2f} TB/s"
           f"  inst {v.get('smsp__inst_executed.sum', 0) / 1e6:8.1f} M")
 print(f"total {tot:.1f} us")
