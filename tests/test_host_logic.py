@@ -15,7 +15,7 @@ def test_icosphere_screening_claim():
     the kernel additionally keeps every vertex within a margin)."""
     d = T.icosphere_directions()
     st = T.icosphere_structure()
-    vert, adj = st[:12], st[12:].reshape(12, 5)
+    vert, adj = st[:12], st[12:72].reshape(12, 5)
     rng = np.random.default_rng(0)
     g = rng.normal(size=(400000, 3))
     # plus directions near Voronoi boundaries: midpoints of random direction pairs
@@ -25,6 +25,43 @@ def test_icosphere_screening_claim():
     vb = np.argmax(g @ d[vert].T, axis=1)
     cand = np.concatenate([vert[vb][:, None], adj[vb]], axis=1)
     assert (cand == best[:, None]).any(axis=1).all()
+
+
+def test_icosphere_fast_kind_table():
+    """The fast argmax of csrc/vk_orient.cu (nearest_dir_fast), restated in
+    fp64 numpy: the winning vertex group, its (p, q, r) axes, the six scores
+    (vertex + 5 midpoints by neighbour kind) and the kind table of
+    tables.icosphere_structure give np.argmax(g @ dirs.T) whenever the top two
+    scores are separated."""
+    d = T.icosphere_directions()
+    st = T.icosphere_structure()
+    vert, kind = st[:12], st[72:].reshape(12, 5)
+    phi = (1.0 + 5 ** 0.5) / 2.0
+    rng = np.random.default_rng(1)
+    g = rng.normal(size=(200000, 3))
+    ax, ay, az = np.abs(g).T
+    vA, vB, vC = ay + phi * az, ax + phi * ay, az + phi * ax
+    grp = np.argmax(np.stack([vA, vB, vC], axis=1), axis=1)
+    perm = {0: (1, 2, 0), 1: (0, 1, 2), 2: (2, 0, 1)}
+    pqr = np.stack([np.abs(g)[np.arange(len(g)), [perm[k][i] for k in grp]] for i in range(3)], axis=1)
+    sg = np.stack([g[np.arange(len(g)), [perm[k][i] for k in grp]] for i in range(3)], axis=1)
+    p, q, r = pqr.T
+    best = p + phi * q
+    cv, cm = 1.0 / np.sqrt(2.0 + phi), 1.0 / (2.0 * phi)
+    sc = np.stack([cv * best, cm * (best + phi * p + r), cm * (best + phi * p - r), cm * (best + q + phi * r),
+                   cm * (best + q - phi * r), cm * (best + phi * q - p)], axis=1)
+    w = np.argmax(sc, axis=1)
+    srt = np.sort(sc, axis=1)
+    clear = srt[:, -1] - srt[:, -2] > 1e-9
+    slot = 6 * (sg[:, 0] > 0) + 3 * (sg[:, 1] > 0) + grp
+    rp = sg[:, 2] > 0
+    k = np.select([w == 0, w == 1, w == 2, w == 3, w == 4], [0, np.where(rp, 1, 2), np.where(rp, 2, 1),
+                                                             np.where(rp, 3, 4), np.where(rp, 4, 3)], 5)
+    fk = np.concatenate([vert[:, None], kind], axis=1)
+    got = fk[slot, k]
+    want = np.argmax(g @ d.T, axis=1)
+    assert clear.mean() > 0.99
+    assert np.array_equal(got[clear], want[clear])
 
 
 def test_plan_matches_reference_schedule():
