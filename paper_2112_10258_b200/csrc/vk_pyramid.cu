@@ -142,6 +142,20 @@ VK_D float2 z_dispatch1(int c, float2 (&r0)[2 * R + 1], float2 v0, const Taps& t
     }
 }
 
+// Two consecutive arrivals per dispatch (phases C, C+1): halves the dispatch
+// cost per plane in blur_z_kernel.
+template <int R, int LO, int HI>
+VK_D void z_dispatch2(int c, float2 (&r0)[2 * R + 1], float2 v0, float2 v1, const Taps& taps, float2& o0, float2& o1) {
+    if constexpr (HI - LO == 1) {
+        o0 = z_arrive1<R, LO>(r0, v0, taps);
+        o1 = z_arrive1<R, (LO + 1) % (2 * R + 1)>(r0, v1, taps);
+    } else {
+        constexpr int MID = (LO + HI) / 2;
+        if (c < MID) z_dispatch2<R, LO, MID>(c, r0, v0, v1, taps, o0, o1);
+        else z_dispatch2<R, MID, HI>(c, r0, v0, v1, taps, o0, o1);
+    }
+}
+
 // Radii >= 8 need more than 128 registers for the ring: one CTA per SM.
 template <int R>
 constexpr int blur_min_blocks() { return R >= 8 ? 1 : 2; }
@@ -388,16 +402,23 @@ blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, i
     const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
     for (int r = tid; r < G::ROWS; r += kThreads) roff_s[r] = pbase + (unsigned)clampi(y0 - R + r, 0, ny - 1) * (unsigned)nx;
     __syncthreads();
-    // stage the clamped plane tile into the row-pair interleaved layout
+    // Stage the clamped plane tile into the row-pair interleaved layout: one
+    // warp instruction copies 16 columns x a row pair, lane l taking column
+    // l/2 of row 2*rp + (l&1), so the 32 lanes write 32 consecutive floats
+    // (conflict-free); clamped column offsets are per-thread constants.
     {
-        const unsigned cx0 = (unsigned)clampi(x0 - R + lane, 0, nx - 1);
-        const unsigned cx1 = (unsigned)clampi(x0 - R + lane + 32, 0, nx - 1);
-        float* d = reinterpret_cast<float*>(in2) + ((wy >> 1) * G::COLSP + lane) * 2 + (wy & 1);
-#pragma unroll 4
-        for (int k = 0; wy + 8 * k < G::ROWS; ++k) {
-            const unsigned ro = roff_s[wy + 8 * k];
-            cp_async4(d + k * 8 * G::COLSP, src + (ro + cx0));
-            if (lane + 32 < G::COLS) cp_async4(d + k * 8 * G::COLSP + 64, src + (ro + cx1));
+        constexpr int NCH = (G::COLS + 15) / 16;
+        const int sdr = lane & 1, sdc = lane >> 1;
+        unsigned cx[NCH];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) cx[ch] = (unsigned)clampi(x0 - R + 16 * ch + sdc, 0, nx - 1);
+        float* d = reinterpret_cast<float*>(in2) + lane;
+#pragma unroll 2
+        for (int rp = wy; rp < G::RP; rp += 8) {
+            const unsigned ro = roff_s[2 * rp + sdr];
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+                if (16 * ch + sdc < G::COLS) cp_async4(d + (rp * G::COLSP + 16 * ch) * 2, src + (ro + cx[ch]));
         }
         cp_async_commit();
         cp_async_wait<0>();
@@ -465,7 +486,7 @@ blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, i
 // subsample block of a thread is completed by lane ^ 16.  Planes outside
 // [0, nz) are the clamped border plane (re-read, L1-resident).
 template <int R>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
 blur_z_kernel(const float* __restrict__ tmp, const float* __restrict__ src, float* __restrict__ dst,
               float* __restrict__ dog, float* __restrict__ half, int nx, int ny, int nz, int tz, int nzc, Taps taps) {
     constexpr int P = 2 * R + 1;
@@ -486,31 +507,24 @@ blur_z_kernel(const float* __restrict__ tmp, const float* __restrict__ src, floa
     for (int t = 0; t < P; ++t) r0[t] = make_float2(0.f, 0.f);
     float2 pv = make_float2(0.f, 0.f);
     const int za = z_start - R, zb = z_end - 1 + R;
-    auto ld = [&](int zp) {
-        const float* t = tmp + (e0 + (unsigned)clampi(zp, 0, nz - 1) * plane);
+    auto ld = [&](const float* base, int zp) {
+        const float* t = base + (e0 + (unsigned)clampi(zp, 0, nz - 1) * plane);
         return make_float2(__ldg(t), __ldg(t + cst));
     };
-    float2 vn = ld(za);
+    // Two arrivals per step (the arrival count tz + 2R is even); loads run two
+    // steps ahead for the intermediate and one step ahead for the DoG source.
+    float2 q0 = ld(tmp, za), q1 = ld(tmp, za + 1), q2 = ld(tmp, za + 2), q3 = ld(tmp, za + 3);
+    const bool want_src = dog != nullptr;
+    float2 s0 = want_src ? ld(src, z_start) : make_float2(0.f, 0.f);
+    float2 s1 = want_src ? ld(src, z_start + 1) : make_float2(0.f, 0.f);
     int c = 0;
-    for (int zp = za; zp <= zb; ++zp) {
-        const float2 v = vn;
-        if (zp < zb) vn = ld(zp + 1);
-        float2 sv = make_float2(0.f, 0.f);
-        const int zo = zp - R;
-        const bool out = zo >= z_start;
-        if (out && dog != nullptr) {
-            const float* sp = src + (e0 + (unsigned)zo * plane);
-            sv = make_float2(__ldg(sp), __ldg(sp + cst));
-        }
-        const float2 o = z_dispatch1<R, 0, P>(c, r0, v, taps);
-        c = (c + 1 == P) ? 0 : c + 1;
-        if (!out) continue;
+    auto epilogue = [&](int zo, float2 o, float2 sv) {
         float* dv = dst + (e0 + (unsigned)zo * plane);
         if (oky) {
             if (okx0) dv[0] = o.x;
             if (okx1) dv[1] = o.y;
         }
-        if (dog != nullptr && oky) {
+        if (want_src && oky) {
             float* gv = dog + (e0 + (unsigned)zo * plane);
             if (okx0) gv[0] = __fsub_rn(sv.x, o.x);
             if (okx1) gv[1] = __fsub_rn(sv.y, o.y);
@@ -535,6 +549,27 @@ blur_z_kernel(const float* __restrict__ tmp, const float* __restrict__ src, floa
             }
         }
         pv = o;
+    };
+    for (int zp = za; zp <= zb; zp += 2) {
+        const float2 v0 = q0, v1 = q1;
+        q0 = q2;
+        q1 = q3;
+        if (zp + 4 <= zb) q2 = ld(tmp, zp + 4);
+        if (zp + 5 <= zb) q3 = ld(tmp, zp + 5);
+        const int zo = zp - R;  // outputs zo, zo + 1 (zo and z_start are even)
+        const bool out = zo >= z_start;
+        const float2 sv0 = s0, sv1 = s1;
+        if (out && want_src) {
+            if (zo + 2 < z_end) s0 = ld(src, zo + 2);
+            if (zo + 3 < z_end) s1 = ld(src, zo + 3);
+        }
+        float2 o0, o1;
+        z_dispatch2<R, 0, P>(c, r0, v0, v1, taps, o0, o1);
+        c += 2;
+        if (c >= P) c -= P;
+        if (!out) continue;
+        epilogue(zo, o0, sv0);
+        if (zo + 1 < z_end) epilogue(zo + 1, o1, sv1);
     }
 }
 
