@@ -372,12 +372,12 @@ blur3d_stream_kernel(const float* __restrict__ src, float* __restrict__ dst, flo
 // no shared memory or barriers in the z kernel (one column pair per thread,
 // coalesced loads).  The intermediate costs 8 more HBM bytes per voxel; both
 // kernels then run near their own roofline.
-constexpr int kXyTX = 32;  // (x, y) tile of the xy kernel
-constexpr int kXyTY = 64;
+constexpr int kXyTX = 32;  // (x, y) tile of the xy kernel: 32 x TY (TY = 64 or 96)
 
-template <int R>
+template <int R, int TY>
 struct XyGeom {
-    static constexpr int ROWS = kXyTY + 2 * R;        // even
+    static constexpr int YR = TY / 16;                // y-pass rows per thread (16 row groups)
+    static constexpr int ROWS = TY + 2 * R;           // even
     static constexpr int RP = ROWS / 2;
     static constexpr int COLS = kXyTX + 2 * R;
     static constexpr int COLSP = ((COLS + 15) / 16) * 16 + 1;
@@ -387,16 +387,16 @@ struct XyGeom {
     static constexpr int ITEMS = RP * 4;               // x-pass items: row pair x 8-output segment
 };
 
-template <int R>
+template <int R, int TY>
 __global__ void __launch_bounds__(kThreads, 4)
 blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, int ny, int nz, Taps taps) {
-    using G = XyGeom<R>;
+    using G = XyGeom<R, TY>;
     extern __shared__ float4 smem4[];
     float2* in2 = reinterpret_cast<float2*>(smem4);
     float* x_s = reinterpret_cast<float*>(in2 + G::IN_F2);
     unsigned* roff_s = reinterpret_cast<unsigned*>(x_s + G::ROWS * G::XS);
     const int bz = blockIdx.z;  // b * nz + z
-    const int x0 = blockIdx.x * kXyTX, y0 = blockIdx.y * kXyTY;
+    const int x0 = blockIdx.x * kXyTX, y0 = blockIdx.y * TY;
     const unsigned plane = (unsigned)nx * (unsigned)ny;
     const unsigned pbase = (unsigned)bz * plane;
     const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
@@ -451,15 +451,16 @@ blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, i
         xb[1] = make_float4(acc[4].y, acc[5].y, acc[6].y, acc[7].y);
     }
     __syncthreads();
-    // y-pass: column pair cp (16), row quad yq (16): 2 x 4 outputs per thread
+    // y-pass: column pair cp (16), row group yq (16): 2 x YR outputs per thread
+    constexpr int YR = G::YR;
     const int cp = tid & 15, yq = tid >> 4;
-    const float* col = x_s + (4 * yq) * G::XS + 2 * cp;
-    float2 o[4];
+    const float* col = x_s + (YR * yq) * G::XS + 2 * cp;
+    float2 o[YR];
 #pragma unroll
-    for (int i = 0; i < 4 + 2 * R; ++i) {
+    for (int i = 0; i < YR + 2 * R; ++i) {
         const float2 v = *reinterpret_cast<const float2*>(col + i * G::XS);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < YR; ++k) {
             const int t = i - k;
             if (t < 0 || t > 2 * R) continue;
             const int dd = t < R ? R - t : t - R;
@@ -471,8 +472,8 @@ blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, i
     }
     const int gx = x0 + 2 * cp;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int gy = y0 + 4 * yq + k;
+    for (int k = 0; k < YR; ++k) {
+        const int gy = y0 + YR * yq + k;
         if (gy < ny) {
             float* t = tmp + (pbase + (unsigned)gy * (unsigned)nx + (unsigned)gx);
             if (gx < nx) t[0] = o[k].x;
@@ -798,25 +799,35 @@ static int launch_ring(const float* src, float* dst, float* dog, float* half, in
 
 // Split path: (x, y) kernel into `work` (nb * volume floats), then the z kernel.
 static int kZWaves = 4, kZMinChunkR = 4;  // z chunking (tuned on B200; env-overridable for sweeps)
-template <int R>
-static int launch_split(const float* src, float* dst, float* dog, float* half, int nb, int nx, int ny, int nz,
-                        const Taps& taps, float* work, cudaStream_t st) {
-    using G = XyGeom<R>;
+template <int R, int TY>
+static int launch_xy(const float* src, float* work, int nb, int nx, int ny, int nz, const Taps& taps, cudaStream_t st) {
+    using G = XyGeom<R, TY>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(blur_xy_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(blur_xy_kernel<R, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
         if (e != cudaSuccess) return cuda_status(e, "blur xy attribute");
         configured = true;
     }
+    dim3 g1((nx + kXyTX - 1) / kXyTX, (ny + TY - 1) / TY, nb * nz);
+    blur_xy_kernel<R, TY><<<g1, kThreads, G::SMEM, st>>>(src, work, nx, ny, nz, taps);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "blur xy launch");
+}
+
+template <int R>
+static int launch_split(const float* src, float* dst, float* dog, float* half, int nb, int nx, int ny, int nz,
+                        const Taps& taps, float* work, cudaStream_t st) {
     static bool env_read = false;
     if (!env_read) {
         if (const char* e = getenv("VK_Z_WAVES")) kZWaves = atoi(e) > 0 ? atoi(e) : kZWaves;
         if (const char* e = getenv("VK_Z_MINCHUNK")) kZMinChunkR = atoi(e) > 0 ? atoi(e) : kZMinChunkR;
         env_read = true;
     }
-    dim3 g1((nx + kXyTX - 1) / kXyTX, (ny + kXyTY - 1) / kXyTY, nb * nz);
-    blur_xy_kernel<R><<<g1, kThreads, G::SMEM, st>>>(src, work, nx, ny, nz, taps);
-    count_launch();
+    // taller tiles (less x-pass halo, fewer y-pass loads) unless they waste rows
+    const bool tall = ((ny + 95) / 96) * 96 <= ((ny + 63) / 64) * 64;
+    const int rc1 = tall ? launch_xy<R, 96>(src, work, nb, nx, ny, nz, taps, st)
+                         : launch_xy<R, 64>(src, work, nb, nx, ny, nz, taps, st);
+    if (rc1 != VK_OK) return rc1;
     // z chunks: enough CTAs for ~4 waves, each chunk >= 4R planes (the 2R
     // warm-up arrivals are overhead), even starts for the subsample epilogue
     int sms = 148, dev = 0;
