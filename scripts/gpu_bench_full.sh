@@ -17,9 +17,9 @@ fi
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-matching > $O/launches_run.log 2>&1; echo "launches rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-  --log-file $O/pyramid_dram.csv -k regex:"blur3d|small_oct|detect|orient_kernel|siftrank|order|frame" \
+  --log-file $O/pyramid_dram.csv -k regex:"blur|small_oct|detect|orient_kernel|siftrank|order|frame" \
   python scripts/profile_step.py --batch 16 --steps 1 > $O/pyramid_dram.log 2>&1; echo "dram rc=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"blur3d_stream_kernel" --launch-skip 5 --launch-count 1 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"blur_xy" --launch-skip 5 --launch-count 1 \
   -o $O/blur10_full python scripts/profile_step.py --batch 12 --steps 1 > /dev/null 2>&1; echo "blur full rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"match_i8_tc" -o $O/match_full \
   python scripts/match_prof.py > /dev/null 2>&1; echo "match full rc=$?"
