@@ -284,6 +284,18 @@ int vk_match_excluding(int metric, const void* a, int na, const void* b, int nb_
 int vk_match_rows_excluding(const void* a, int na, const void* b, int nb_rows, int dim, double ratio_max,
                             const int* row_ex, int* best, double* d1, double* d2, uint8_t* keep, void* stream);
 
+/* ------------------------------------------------------------- key files */
+/* Host-side formatter of keyfiles.py:35-122 text lines (no device work):
+ * "x y z sigma octave level dog_value sign" (+ 9 row-major rotation reals when
+ * rot != NULL) (+ payload: kind 1 = payload_len decimal ranks per record,
+ * kind 2 = payload_len packed bytes as lowercase hex), reals as "%.9g".
+ * Writes at most cap bytes into out and returns the bytes the n records need
+ * (call again with a larger buffer if that exceeds cap); -1 on bad arguments. */
+long long vk_format_records(long long n, const double* pos, const double* sigma, const int* octave,
+                            const int* level, const double* dog, const signed char* sign, const double* rot,
+                            const unsigned char* payload, int payload_kind, int payload_len, char* out,
+                            long long cap);
+
 /* Select the int8 euclidean kernel: 0 = tensor cores where the shape allows
  * (default), 1 = dp4a everywhere (cross-checks and benchmarks). */
 int vk_set_match_path(int path);

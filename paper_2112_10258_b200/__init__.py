@@ -14,6 +14,7 @@ from .consensus import (ConsensusResult, HoughSettings, SimilarityTransform7DOF,
                         match_records, similarity_from_correspondences, vote_transform)
 from .detect import Keypoint, detect_keypoints
 from .engine import Extractor
+from .ingest import load_nifti_subset, load_raw, load_volume, read_raw_header, save_raw
 from .errors import DataError, DeviceError, NoConsensusError, ParameterError, VolkeyError
 from .match import Match, nearest_neighbor_matches
 from .pipeline import ExtractionResult, assign_orientations, extract_batch, extract_features
@@ -33,6 +34,11 @@ __all__ = [
     "build_dog_pyramid",
     "build_gaussian_pyramid",
     "Volume",
+    "load_raw",
+    "save_raw",
+    "read_raw_header",
+    "load_nifti_subset",
+    "load_volume",
     "DeviceVolume",
     "Match",
     "nearest_neighbor_matches",

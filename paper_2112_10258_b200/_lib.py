@@ -54,9 +54,11 @@ SIGNATURES = {
     "vk_match": [I, P, I, P, I, I, D, P, P, P, P, P],
     "vk_match_excluding": [I, P, I, P, I, I, D, I, I, P, P, P, P, P],
     "vk_set_match_path": [I],
+    "vk_format_records": [LL, P, P, P, P, P, P, P, P, I, I, P, LL],
     "vk_match_rows_excluding": [P, I, P, I, I, D, P, P, P, P, P, P],
 }
-_RESTYPE = {"vk_last_error": C.c_char_p, "vk_launch_count": C.c_longlong, "vk_accum_work_bytes": C.c_longlong}
+_RESTYPE = {"vk_last_error": C.c_char_p, "vk_launch_count": C.c_longlong, "vk_accum_work_bytes": C.c_longlong,
+            "vk_format_records": C.c_longlong}
 
 # device record layouts (must match include/volkey_b200.h)
 LEVEL_DTYPE = np.dtype([("base", "<u8"), ("vol_stride", "<i8"), ("nx", "<i4"), ("ny", "<i4"), ("nz", "<i4"),

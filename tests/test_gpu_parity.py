@@ -393,6 +393,22 @@ def test_count_inlier_matches_end_to_end():
         assert np.array_equal(rep["transform"].translation, h[f"{kind}_translation"])
 
 
+def test_write_soa_equals_record_writer(tmp_path):
+    """keyfiles.write_soa straight from Extractor.results() == the record-based
+    writer on the same extraction (both byte-identical to the reference format)."""
+    from paper_2112_10258_b200 import keyfiles as kf
+
+    vols = [small_volume(load_golden(f"small{i}.npz"))[:40, :44, :36] for i in (0, 2)]
+    for kind in ("siftrank", "brief"):
+        cfg = PipelineConfig(descriptor=kind)
+        soa = vk.extract_batch(np.stack(vols), cfg)
+        for b, v in enumerate(vols):
+            kf.write_soa(tmp_path / "soa.txt", soa, kind, 64, cfg.seed, volume=b)
+            res = vk.extract_features(vk.Volume(v), cfg)
+            kf.write_descriptors(tmp_path / "rec.txt", res.records, kind, 64, cfg.seed)
+            assert (tmp_path / "soa.txt").read_bytes() == (tmp_path / "rec.txt").read_bytes(), (kind, b)
+
+
 def test_batch_equals_single():
     """Batched extraction (volume-major SoA) equals one-volume extraction."""
     vols = [small_volume(load_golden(f"small{i}.npz")) for i in (0, 2)]
