@@ -347,8 +347,9 @@ class Extractor:
         rec = rec or _no_stage
         self.enqueue_pyramid(s, rec=rec)
         self.enqueue_detect(s, rec=rec)
-        with rec("gradients", -1, -1):
-            self.enqueue_gradients(s)
+        if self.grad_levels:  # optional dense gradient volumes (not a reference stage)
+            with rec("gradients", -1, -1):
+                self.enqueue_gradients(s)
         with rec("orient", -1, -1):
             self.enqueue_orient(s)
         with rec("descriptor", -1, -1):

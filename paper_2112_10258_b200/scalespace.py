@@ -32,9 +32,13 @@ def _check_exec(workers: int, chunk: int) -> None:
 
 
 def _stage(recorder):
-    """recorder.stage(...) that also waits for the GPU, so wall time = device time."""
+    """recorder.stage(...) that also waits for the GPU, so wall time = device
+    time; recorders that time with CUDA events (``device = True``,
+    timing.DeviceStageRecorder) are used as they are, without synchronising."""
     if recorder is None:
         return lambda *a: nullcontext()
+    if getattr(recorder, "device", False):
+        return recorder.stage
 
     def ctx(name, octave, level):
         inner = recorder.stage(name, octave, level)
