@@ -92,104 +92,11 @@ detect_kernel(DogPtrs dogs, int nlev, int nx, int ny, int nz, int seg_base, int 
 }
 
 // Band 0 (the default): a strict extremum must first beat its 26 same-level
-// neighbours.  One thread streams one (x, y) column through z keeping the 3x3
-// in-plane max / min of the previous, current and next plane in registers
-// (loads of the plane after next are issued a step ahead), so the prefilter
-// costs ~9 coalesced loads and ~20 min/max per voxel.  Survivors (a few per
-// cent) are confirmed against the 54 neighbours in the adjacent DoG levels with
-// exactly the reference comparisons (detect.py:65-76); NaN neighbours never
-// let a non-extremum through because the confirmation uses > / < like numpy.
-struct Plane9 {
-    float v[9];
-};
-
-VK_D void load_plane9(Plane9& q, const float* __restrict__ p, int nx) {
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-        for (int dx = 0; dx < 3; ++dx) q.v[3 * dy + dx] = __ldg(p + (dy - 1) * nx + (dx - 1));
-}
-
-VK_D void stats8(const Plane9& q, float& M8, float& m8, float& c) {
-    c = q.v[4];
-    M8 = fmaxf(fmaxf(fmaxf(q.v[0], q.v[1]), fmaxf(q.v[2], q.v[3])), fmaxf(fmaxf(q.v[5], q.v[6]), fmaxf(q.v[7], q.v[8])));
-    m8 = fminf(fminf(fminf(q.v[0], q.v[1]), fminf(q.v[2], q.v[3])), fminf(fminf(q.v[5], q.v[6]), fminf(q.v[7], q.v[8])));
-}
-
-__global__ void __launch_bounds__(128)
-detect_band0_kernel(DogPtrs dogs, int nlev, int nx, int ny, int nz, int seg_base, float cmin,
-                    unsigned long long* __restrict__ keys, int* __restrict__ counts, int cap) {
-    const int x = 1 + blockIdx.x * 32 + threadIdx.x;
-    const int y = 1 + blockIdx.y * 4 + threadIdx.y;
-    const int lev = 1 + blockIdx.z % nlev;
-    const int b = blockIdx.z / nlev;
-    const long long plane = (long long)nx * ny;
-    const long long vol = plane * nz;
-    const bool valid = x < nx - 1 && y < ny - 1;
-    const int xs = valid ? x : 1, ys = valid ? y : 1;  // invalid lanes shadow a valid column
-    const float* col = dogs.p[lev] + (long long)b * vol + (long long)ys * nx + xs;
-    const float* lo = dogs.p[lev - 1] + (long long)b * vol + (long long)ys * nx + xs;
-    const float* hi = dogs.p[lev + 1] + (long long)b * vol + (long long)ys * nx + xs;
-    const int lane = (threadIdx.y * 32 + threadIdx.x) & 31;
-    int* cnt = counts + b;
-    unsigned long long* kb = keys + (long long)b * cap;
-
-    Plane9 nxt;
-    float Mp, mp, Mc, mc, cc;  // plane z-1 (3x3 incl. centre), plane z (8-neighbourhood + centre)
-    {
-        Plane9 q;
-        load_plane9(q, col, nx);
-        float M8, m8, c;
-        stats8(q, M8, m8, c);
-        Mp = fmaxf(M8, c);
-        mp = fminf(m8, c);
-        load_plane9(q, col + plane, nx);
-        stats8(q, Mc, mc, cc);
-        load_plane9(nxt, col + 2 * plane, nx);
-    }
-    for (int z = 1; z <= nz - 2; ++z) {
-        float Mn8, mn8, cn;
-        stats8(nxt, Mn8, mn8, cn);
-        if (z + 2 <= nz - 1) load_plane9(nxt, col + (long long)(z + 2) * plane, nx);
-        const float Mn = fmaxf(Mn8, cn), mn = fminf(mn8, cn);
-        bool hit = false, valley = false;
-        if (valid && fabsf(cc) >= cmin) {
-            const bool pk = cc > fmaxf(fmaxf(Mp, Mc), Mn);
-            const bool vl = cc < fminf(fminf(mp, mc), mn);
-            if (pk || vl) {
-                // confirm against the 54 neighbours of the adjacent DoG levels
-                bool ok = true;
-                const long long zo = (long long)z * plane;
-#pragma unroll 1
-                for (int o = 0; o < 54 && ok; ++o) {
-                    const int l = o / 27, r = o % 27;
-                    const float* v = (l == 0 ? lo : hi) + zo + (long long)(r / 9 - 1) * plane + (long long)((r / 3) % 3 - 1) * nx + (r % 3 - 1);
-                    const float n = __ldg(v);
-                    ok = pk ? (cc > n) : (cc < n);
-                }
-                hit = ok;
-                valley = vl;
-            }
-        }
-        const unsigned mask = __ballot_sync(0xffffffffu, hit);
-        if (mask) {
-            const int leader = __ffs(mask) - 1;
-            int base = 0;
-            if (lane == leader) base = atomicAdd(cnt, __popc(mask));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (hit) {
-                const int slot = base + __popc(mask & ((1u << lane) - 1));
-                if (slot < cap) kb[slot] = make_key(seg_base + lev, x, y, z, valley ? 1 : 0);
-            }
-        }
-        Mp = fmaxf(Mc, cc);
-        mp = fminf(mc, cc);
-        Mc = Mn8;
-        mc = mn8;
-        cc = cn;
-    }
-}
-
+// neighbours (prefilter on in-plane 3x3 max / min of the previous, current and
+// next plane, streamed in registers); survivors (a few per cent) are confirmed
+// against the 54 neighbours in the adjacent DoG levels with exactly the
+// reference comparisons (detect.py:65-76); NaN neighbours never let a
+// non-extremum through the confirmation because it uses > / < like numpy.
 // Band 0, register-blocked: a warp covers 30 output columns (lanes 1..30;
 // lanes 0 and 31 only load the x halo) and each thread 4 consecutive output
 // rows, streaming z.  Per plane a thread loads 6 rows of its column (coalesced,
