@@ -284,6 +284,17 @@ int vk_match_excluding(int metric, const void* a, int na, const void* b, int nb_
 int vk_match_rows_excluding(const void* a, int na, const void* b, int nb_rows, int dim, double ratio_max,
                             const int* row_ex, int* best, double* d1, double* d2, uint8_t* keep, void* stream);
 
+/* ------------------------------------------------------ point evaluations */
+/* gradients_at (volume.py:244-264): fp64 central / one-sided differences at
+ * n integer voxels idx[3i..3i+2] = (x, y, z) of an x-fastest fp32 volume
+ * (device pointers); out[3i..3i+2]. */
+int vk_gradients_at(const float* data, int nx, int ny, int nz, const long long* idx, long long n, double* out,
+                    void* stream);
+/* sample_trilinear_array (volume.py:203-236): clamped trilinear interpolation
+ * in fp64 at n points pts[3i..3i+2] (index units); out[i]. */
+int vk_sample_trilinear(const float* data, int nx, int ny, int nz, const double* pts, long long n, double* out,
+                        void* stream);
+
 /* ------------------------------------------------------------- key files */
 /* Host-side formatter of keyfiles.py:35-122 text lines (no device work):
  * "x y z sigma octave level dog_value sign" (+ 9 row-major rotation reals when

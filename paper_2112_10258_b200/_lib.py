@@ -55,6 +55,8 @@ SIGNATURES = {
     "vk_match_excluding": [I, P, I, P, I, I, D, I, I, P, P, P, P, P],
     "vk_set_match_path": [I],
     "vk_format_records": [LL, P, P, P, P, P, P, P, P, I, I, P, LL],
+    "vk_gradients_at": [P, I, I, I, P, LL, P, P],
+    "vk_sample_trilinear": [P, I, I, I, P, LL, P, P],
     "vk_match_rows_excluding": [P, I, P, I, I, D, P, P, P, P, P, P],
 }
 _RESTYPE = {"vk_last_error": C.c_char_p, "vk_launch_count": C.c_longlong, "vk_accum_work_bytes": C.c_longlong,

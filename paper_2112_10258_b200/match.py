@@ -112,3 +112,18 @@ def match_descriptors(records_a, records_b, config):
     a = descriptor_array(records_a, kind)
     b = descriptor_array(records_b, kind)
     return nearest_neighbor_matches(a, b, config.ratio_max, metric, config.workers), kind
+
+
+_CONSENSUS = ("SimilarityTransform7DOF", "rotation_angle_deg", "HoughSettings", "ConsensusResult", "vote_transform",
+              "similarity_from_correspondences", "hough_consensus", "settings_from_config", "match_records",
+              "count_inlier_matches")
+
+
+def __getattr__(name):
+    """volkey.match also holds the consensus API (match.py:31-401): re-export
+    it lazily from consensus.py (which imports this module)."""
+    if name in _CONSENSUS:
+        from . import consensus
+
+        return getattr(consensus, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

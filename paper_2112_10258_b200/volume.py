@@ -100,3 +100,77 @@ def device_of(v: Volume):
     if isinstance(v, DeviceVolume):
         return v.device
     return to_device(v.data)
+
+
+@dataclass(frozen=True)
+class VoxelIndex:
+    """volume.py:49-56."""
+
+    x: int
+    y: int
+    z: int
+
+    def within(self, dims) -> bool:
+        return 0 <= self.x < dims[0] and 0 <= self.y < dims[1] and 0 <= self.z < dims[2]
+
+
+def _dev_data(data):
+    """x-fastest device tensor for a numpy data[x, y, z] array or a Volume."""
+    if isinstance(data, Volume):
+        return device_of(data), data.dims
+    a = np.asarray(data, dtype=np.float32)
+    return to_device(a), a.shape
+
+
+def gradients_at(data, indices) -> np.ndarray:
+    """volume.py:244-264 on the GPU: fp64 central differences in the interior,
+    one-sided at borders, at integer voxel indices (N, 3) -> (N, 3)."""
+    t = _lib.torch()
+    dev, (nx, ny, nz) = _dev_data(data)
+    idx = np.ascontiguousarray(np.atleast_2d(np.asarray(indices, dtype=np.int64)))
+    n = len(idx)
+    if n and (idx.shape[1] != 3 or (idx < 0).any() or (idx >= np.array([nx, ny, nz])).any()):
+        raise IndexError("gradients_at: voxel index outside the volume")
+    d_idx = t.from_numpy(idx).cuda()
+    out = t.empty((max(n, 1), 3), dtype=t.float64, device="cuda")
+    _lib.call("vk_gradients_at", _lib.ptr(dev), nx, ny, nz, d_idx.data_ptr(), n, out.data_ptr(), _lib.stream_ptr())
+    return out[:n].cpu().numpy()
+
+
+def central_gradient(volume: Volume, idx: VoxelIndex) -> np.ndarray:
+    """volume.py:267-269: gradient at one voxel."""
+    return gradients_at(volume, np.array([[idx.x, idx.y, idx.z]]))[0]
+
+
+def sample_trilinear_array(data, points) -> np.ndarray:
+    """volume.py:203-236 on the GPU: clamped trilinear interpolation in fp64 at
+    continuous points (N, 3) or (3,), index units."""
+    t = _lib.torch()
+    dev, (nx, ny, nz) = _dev_data(data)
+    pts = np.asarray(points, dtype=np.float64)
+    single = pts.ndim == 1
+    pts = np.ascontiguousarray(np.atleast_2d(pts))
+    n = len(pts)
+    d_pts = t.from_numpy(pts).cuda()
+    out = t.empty(max(n, 1), dtype=t.float64, device="cuda")
+    _lib.call("vk_sample_trilinear", _lib.ptr(dev), nx, ny, nz, d_pts.data_ptr(), n, out.data_ptr(), _lib.stream_ptr())
+    res = out[:n].cpu().numpy()
+    return res[0] if single else res
+
+
+def trilinear_sample(volume: Volume, point) -> float:
+    """volume.py:239-241."""
+    return float(sample_trilinear_array(volume, np.asarray(point, dtype=np.float64)))
+
+
+_INGEST = ("load_raw", "save_raw", "read_raw_header", "load_nifti_subset", "load_volume")
+
+
+def __getattr__(name):
+    """volkey.volume also holds the loaders (volume.py:73-200): re-export them
+    lazily from ingest.py (which imports this module)."""
+    if name in _INGEST:
+        from . import ingest
+
+        return getattr(ingest, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

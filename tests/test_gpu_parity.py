@@ -517,3 +517,30 @@ def test_database_matching_single_rank():
             best, d1, d2, keep = res[i]
             mine = [(q, int(best[q]), float(d1[q]), float(d2[q])) for q in np.flatnonzero(keep)]
             assert mine == ref, f"{metric} subject {i}"
+
+
+def test_point_samplers_match_oracle():
+    """gradients_at (volume.py:244-264) and sample_trilinear_array
+    (volume.py:203-236) on the GPU == the oracle, bit for bit, including
+    border voxels, clamped out-of-range points and degenerate (1-voxel) axes."""
+    from oracle import volkey_oracle as O
+    from paper_2112_10258_b200.volume import (VoxelIndex, central_gradient, gradients_at, sample_trilinear_array,
+                                              trilinear_sample)
+
+    rng = np.random.default_rng(11)
+    for dims in ((17, 23, 9), (1, 5, 4), (6, 1, 1)):
+        data = rng.standard_normal(dims).astype(np.float32)
+        idx = np.stack([rng.integers(0, d, 500) for d in dims], axis=1)
+        idx[:8] = [[0, 0, 0], [dims[0] - 1, dims[1] - 1, dims[2] - 1]] * 4
+        assert np.array_equal(gradients_at(data, idx), O.grads_at(data, idx))
+        pts = rng.uniform(-2.0, np.array(dims) + 1.0, size=(700, 3))
+        pts[:4] = [[0, 0, 0], np.array(dims) - 1.0, [0.5, 0.5, 0.5], np.array(dims) - 1.5]
+        assert np.array_equal(sample_trilinear_array(data, pts), O.trilinear(data, pts))
+        one = sample_trilinear_array(data, pts[5])
+        assert np.ndim(one) == 0 and one == O.trilinear(data, pts[5:6])[0]
+        v = vk.Volume(data)
+        assert trilinear_sample(v, pts[6]) == float(O.trilinear(data, pts[6:7])[0])
+        assert np.array_equal(central_gradient(v, VoxelIndex(*idx[9])), O.grads_at(data, idx[9:10])[0])
+    assert gradients_at(data, np.zeros((0, 3), dtype=np.int64)).shape == (0, 3)
+    with pytest.raises(IndexError):
+        gradients_at(data, [[dims[0], 0, 0]])
