@@ -17,7 +17,7 @@ import numpy as np
 from .errors import DataError, DeviceError, ParameterError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvolkey_b200.so")
+LIB_PATH = os.environ.get("VK_LIB_PATH") or os.path.join(_HERE, "libvolkey_b200.so")  # override: A/B variants
 
 P = C.c_void_p
 I = C.c_int

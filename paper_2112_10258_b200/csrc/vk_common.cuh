@@ -147,6 +147,26 @@ VK_D Nb6 load_nb6(const float* __restrict__ d, int nx, int ny, int nz, int x, in
     return n;
 }
 
+// load_nb6 for a voxel with all six neighbours inside the volume (central
+// differences on every axis); c is its linear index, plane = nx * ny.
+VK_D Nb6 load_nb6_interior(const float* __restrict__ d, unsigned nx, unsigned plane, unsigned c) {
+    Nb6 n;
+    n.xh = __ldg(d + (c + 1u));
+    n.xl = __ldg(d + (c - 1u));
+    n.yh = __ldg(d + (c + nx));
+    n.yl = __ldg(d + (c - nx));
+    n.zh = __ldg(d + (c + plane));
+    n.zl = __ldg(d + (c - plane));
+    n.sx = n.sy = n.sz = 0.5f;
+    return n;
+}
+
+// Every voxel of a keypoint's ball (offsets within +-r per axis) has all six
+// neighbours inside the volume.
+VK_HD bool ball_interior(int cx, int cy, int cz, int r, int nx, int ny, int nz) {
+    return cx > r && cy > r && cz > r && cx + r + 1 < nx && cy + r + 1 < ny && cz + r + 1 < nz;
+}
+
 // Exact fp64 gradient from the loaded neighbours: the fp64 difference of two
 // fp32 values is exact and the scale is a power of two.
 VK_D void grad64(const Nb6& n, double& gx, double& gy, double& gz) {

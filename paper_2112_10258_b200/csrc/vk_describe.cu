@@ -23,7 +23,6 @@ namespace vk {
 
 constexpr int kSrThreads = 256;
 constexpr int kPrefetchPlanes = 3;  // z-plane lead of the L1 prefetch in the ball walk
-constexpr int kSrWarps = kSrThreads / 32;
 constexpr int kSrBins = 64;
 constexpr int kPatchThreads = 256;
 constexpr int kMaxSide = 31;
@@ -95,7 +94,20 @@ __device__ __noinline__ int sr_obits_exact(int ox, int oy, int oz, const double*
 // need only the integer offset and R (offsets on lines / planes through the
 // centre give exact zeros for axes with zero coordinates), gradient
 // components need the exact fp64 gradient (rare).
-VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const double* R, const float* Rf,
+//
+// Rc holds the frame's columns (R[0][j], R[1][j], R[2][j], 0) as fp32 in
+// shared memory, read with a volatile vector load per use: the compiler would
+// otherwise hoist 9 x F rotation floats into registers for the whole walk and
+// halve the resident warps of this latency-bound loop.
+VK_D float4 lds_col(const float4* p) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+}
+
+VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const double* R, const float4* Rc,
                      const float* data, int nx, int ny, int nz, int x, int y, int z) {
     const float fx = (float)ox, fy = (float)oy, fz = (float)oz;
     const float eo = 1.0e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
@@ -104,8 +116,9 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
     bool osure = true, gsure = true;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        const float r = fmaf(fz, Rf[6 + j], fmaf(fy, Rf[3 + j], fx * Rf[j]));
-        const float g = fmaf(gz, Rf[6 + j], fmaf(gy, Rf[3 + j], gx * Rf[j]));
+        const float4 c = lds_col(Rc + j);
+        const float r = fmaf(fz, c.z, fmaf(fy, c.y, fx * c.x));
+        const float g = fmaf(gz, c.z, fmaf(gy, c.y, gx * c.x));
         sp |= (int)(r > 0.f) << j;
         og |= (int)(g > 0.f) << j;
         osure = osure && fabsf(r) > eo;
@@ -116,15 +129,19 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
     return 8 * sp + og;
 }
 
-// Fast walk of one keypoint's ball for NF frames (rotations in registers);
-// returns the number of in-volume ball voxels seen by this thread.  With a
-// precomputed gradient volume (g4 != null) each visit is one float4 load.
-template <int NF>
+// Fast walk of one keypoint's ball for NF frames; returns the number of
+// in-volume ball voxels seen by this thread.  INTERIOR: the whole ball and its
+// gradient stencil lie inside the volume (no bounds tests, no one-sided
+// differences).  With a precomputed gradient volume (g4 != null) each visit is
+// one float4 load.
+template <int NF, bool INTERIOR>
 VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const float4* g4, const vk_ball& ball,
-                 const int* __restrict__ ball_offsets, const double* Rs, const float* Rfs, double* hist, int F) {
+                 const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist, int F) {
     const int tid = threadIdx.x;
     const int step = blockDim.x;
+    const unsigned plane = (unsigned)L.nx * (unsigned)L.ny;
     int cnt = 0;
+    hist = vote_copy(hist);
     int pn = tid < ball.count ? __ldg(ball_offsets + ball.zstart + tid) : 0;
     for (int base = 0; base < ball.count; base += step) {
         const int j = base + tid;
@@ -140,10 +157,11 @@ VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const fl
             x = kp.ix + ox;
             y = kp.iy + oy;
             z = kp.iz + oz;
-            if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
+            if (INTERIOR || (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz)) {
                 ++cnt;
+                const unsigned c = ((unsigned)z * (unsigned)L.ny + (unsigned)y) * (unsigned)L.nx + (unsigned)x;
                 if (g4) {
-                    const float4 q = __ldg(g4 + (((unsigned)z * (unsigned)L.ny + (unsigned)y) * (unsigned)L.nx + (unsigned)x));
+                    const float4 q = __ldg(g4 + c);
                     gx = q.x;
                     gy = q.y;
                     gz = q.z;
@@ -151,7 +169,8 @@ VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const fl
                     has = mag > 0.f;  // |g| > 0 exactly when g != 0 (fp64 norm, never underflows in fp32)
                 } else {
                     prefetch_plane_ahead(data, L.nx, L.ny, L.nz, x, y, z, kPrefetchPlanes);
-                    const Nb6 nb = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
+                    const Nb6 nb = INTERIOR ? load_nb6_interior(data, (unsigned)L.nx, plane, c)
+                                            : load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
                     grad32(nb, gx, gy, gz);
                     has = !(gx == 0.f && gy == 0.f && gz == 0.f);  // zero vote: no bin changes
                     if (has) mag = norm3_f32(gx, gy, gz);
@@ -161,13 +180,30 @@ VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const fl
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             if (f >= F) break;
-            const int bin = has ? sr_bin_fast(ox, oy, oz, gx, gy, gz, Rs + 9 * f, Rfs + 9 * f, data, L.nx, L.ny, L.nz, x,
+            const int bin = has ? sr_bin_fast(ox, oy, oz, gx, gy, gz, Rs + 9 * f, Rc + 3 * f, data, L.nx, L.ny, L.nz, x,
                                               y, z)
                                 : -1;
             red_vote(hist + f * kSrBins, bin, mag);
         }
     }
     return cnt;
+}
+
+template <bool INTERIOR>
+VK_D int sr_walk_frames(const vk_kp& kp, const vk_level& L, const float* data, const float4* g4, const vk_ball& ball,
+                        const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist,
+                        int F) {
+    switch (F) {
+        case 1: return sr_walk<1, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);
+        case 2: return sr_walk<2, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);
+        case 3: return sr_walk<3, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);
+        case 4: return sr_walk<4, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);
+        default: {  // > 4 frames: two passes of up to 4 frames
+            const int cnt = sr_walk<4, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, 4);
+            sr_walk<4, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs + 36, Rc + 12, hist + 4 * kSrBins, F - 4);
+            return cnt;
+        }
+    }
 }
 
 // Stable ascending ranks of 64 values: rank_b = #{j : w_j < w_b or (w_j == w_b and j < b)}.
@@ -222,7 +258,10 @@ __device__ __noinline__ void sr_exact_frame(const float* data, const vk_level& L
 // One CTA per work item = one keypoint and its F frames (contiguous in the
 // frame list).  The ball is walked in z-major order (coalesced gathers);
 // each voxel's gradient is computed once and voted into all F frames.
-__global__ void __launch_bounds__(kSrThreads, 2)
+#ifndef VK_SR_MIN_BLOCKS
+#define VK_SR_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(kSrThreads, VK_SR_MIN_BLOCKS)
 siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ rot,
                 const int* __restrict__ item_first, const int* __restrict__ item_count,
                 const int* __restrict__ n_items_dev, int n_items_max, const vk_kp* __restrict__ kps,
@@ -234,7 +273,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
     __shared__ double w[kSrBins];
     __shared__ int order[kSrBins];
     __shared__ double Rs[VK_MAX_FRAMES * 9];
-    __shared__ float Rfs[VK_MAX_FRAMES * 9];
+    __shared__ float4 Rc[VK_MAX_FRAMES * 3];
     __shared__ int xb[kSrThreads];
     __shared__ double xv[kSrThreads];
     __shared__ int n_inside;
@@ -251,7 +290,12 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
         __syncthreads();  // previous item done with the shared buffers
         for (int i = tid; i < F * 9; i += kSrThreads) {
             Rs[i] = rot[(long long)first * 9 + i];
-            Rfs[i] = (float)Rs[i];
+        }
+        __syncthreads();
+        for (int i = tid; i < F * 3; i += kSrThreads) {
+            const double* R = Rs + 9 * (i / 3);
+            const int j = i % 3;
+            Rc[i] = make_float4((float)R[j], (float)R[3 + j], (float)R[6 + j], 0.f);
         }
         zero_hist(hist, F * kSrBins);
         if (tid == 0) n_inside = 0;
@@ -265,17 +309,10 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                 const vk_gradlevel GL = grads[kp.lvl];
                 if (GL.g4) g4 = reinterpret_cast<const float4*>(GL.g4) + (long long)kp.vol * GL.vol_stride;
             }
-            switch (F) {
-                case 1: cnt = sr_walk<1>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, F); break;
-                case 2: cnt = sr_walk<2>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, F); break;
-                case 3: cnt = sr_walk<3>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, F); break;
-                case 4: cnt = sr_walk<4>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, F); break;
-                default:  // > 4 frames: two passes of up to 4 frames
-                    cnt = sr_walk<4>(kp, L, data, g4, ball, ball_offsets, Rs, Rfs, hist, 4);
-                    sr_walk<4>(kp, L, data, g4, ball, ball_offsets, Rs + 36, Rfs + 36, hist + 4 * kSrBins,
-                               F - 4);
-                    break;
-            }
+            if (ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz))
+                cnt = sr_walk_frames<true>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);
+            else
+                cnt = sr_walk_frames<false>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);
         } else {
             for (int j = tid; j < ball.count; j += kSrThreads) {
                 const int p = __ldg(ball_offsets + ball.start + j);
@@ -436,7 +473,7 @@ extern "C" int vk_describe_siftrank(const vk_frame* frames, const double* rot, c
         return VK_ERR_PARAMETER;
     }
     if (n_items_max == 0) return VK_OK;
-    siftrank_kernel<<<grid_for(n_items_max, kAccumCtasPerSm), kSrThreads, 0, as_stream(stream)>>>(
+    siftrank_kernel<<<accum_grid(siftrank_kernel, kSrThreads, n_items_max), kSrThreads, 0, as_stream(stream)>>>(
         frames, rot, item_first, item_count, n_items_dev, n_items_max, kps, levels, balls, ball_offsets, max_f,
         ranks_out, exact_only, stats, grads, work);
     count_launch();

@@ -15,22 +15,54 @@
 
 namespace vk {
 
-// Histogram slots per CTA in the accumulation workspace (>= VK_MAX_FRAMES x 64
-// SIFT-Rank bins and >= VK_MAX_DIRS orientation bins).
-constexpr int kAccumSlot = VK_MAX_FRAMES * 64;
+// Each CTA accumulates into kVoteCopies copies of its histogram, lane l
+// voting into copy l % kVoteCopies: lanes of one warp that pick the same bin
+// hit different L2 addresses instead of serialising on one.  The copies are
+// summed when the histogram is read (fp64, any order: the bounds hold for
+// every summation order).
+#ifndef VK_VOTE_COPIES
+#define VK_VOTE_COPIES 1
+#endif
+constexpr int kVoteCopies = VK_VOTE_COPIES;
+// Doubles per copy (>= VK_MAX_FRAMES x 64 SIFT-Rank bins and >= VK_MAX_DIRS
+// orientation bins).
+constexpr int kCopyStride = VK_MAX_FRAMES * 64;
+// Histogram slots per CTA in the accumulation workspace.
+constexpr int kAccumSlot = kCopyStride * kVoteCopies;
 // Persistent grids launch at most this many CTAs per SM.
 constexpr int kAccumCtasPerSm = 4;
+
+// Grid of a persistent accumulation kernel: every CTA resident at once (the
+// occupancy the kernel's registers allow, at most kAccumCtasPerSm per SM), so
+// no CTA waits for a second wave with its share of the items.
+template <class Kernel>
+inline int accum_grid(Kernel kernel, int threads, int n_items) {
+    int dev = 0, sms = 148, occ = kAccumCtasPerSm;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ < 1) occ = 1;
+    const int g = sms * (occ < kAccumCtasPerSm ? occ : kAccumCtasPerSm);
+    return n_items < g ? n_items : g;
+}
+
+// This thread's copy of the CTA histogram.
+VK_D double* vote_copy(double* hist) { return hist + (threadIdx.x & (kVoteCopies - 1)) * kCopyStride; }
 
 VK_D void red_vote(double* hist, int bin, float v) {
     if (bin >= 0) atomicAdd(hist + bin, (double)v);  // result unused -> RED.E.ADD.F64.RN
 }
 
-// Zero this CTA's first n histogram entries (the caller synchronises).
+// Zero the first n entries of every copy (the caller synchronises).
 VK_D void zero_hist(double* hist, int n) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) hist[i] = 0.0;
+    for (int i = threadIdx.x; i < n * kVoteCopies; i += blockDim.x) hist[(i / n) * kCopyStride + i % n] = 0.0;
 }
 
-// Read a reduced entry back after a __syncthreads (L2, bypassing L1).
-VK_D double read_hist(const double* hist, int i) { return __ldcg(hist + i); }
+// Entry i summed over the copies, after a __syncthreads (L2, bypassing L1).
+VK_D double read_hist(const double* hist, int i) {
+    double s = __ldcg(hist + i);
+#pragma unroll
+    for (int c = 1; c < kVoteCopies; ++c) s += __ldcg(hist + c * kCopyStride + i);
+    return s;
+}
 
 }  // namespace vk

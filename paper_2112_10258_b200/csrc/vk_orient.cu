@@ -229,6 +229,41 @@ VK_D int ori_vote_fast(const Nb6& n, const float* __restrict__ win32, int d2, co
     return nearest_dir(dirs, K, x64, y64, z64);
 }
 
+// Fast z-major ball walk (consecutive lanes take consecutive x: coalesced
+// gathers); INTERIOR: ball and gradient stencil inside the volume.  Returns
+// this thread's count of in-volume voxels.
+template <bool INTERIOR>
+VK_D int ori_walk(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
+                  const int* __restrict__ ball_offsets, const float* __restrict__ win32, const double* dirs,
+                  const IcoSh* icp, int K, double* hist) {
+    const int tid = threadIdx.x;
+    const unsigned plane = (unsigned)L.nx * (unsigned)L.ny;
+    hist = vote_copy(hist);
+    int inside_cnt = 0;
+    int pn = tid < ball.count ? __ldg(ball_offsets + ball.zstart + tid) : 0;
+    for (int base = 0; base < ball.count; base += kOriThreads) {
+        const int j = base + tid;
+        const int p = pn;
+        if (j + kOriThreads < ball.count) pn = __ldg(ball_offsets + ball.zstart + j + kOriThreads);
+        int bin = -1;
+        float vote = 0.f;
+        if (j < ball.count) {
+            const int ox = unpack_off(p, 0), oy = unpack_off(p, 1), oz = unpack_off(p, 2);
+            const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
+            if (INTERIOR || (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz)) {
+                ++inside_cnt;
+                const Nb6 nb = INTERIOR ? load_nb6_interior(data, (unsigned)L.nx, plane,
+                                                            ((unsigned)z * (unsigned)L.ny + (unsigned)y) *
+                                                                    (unsigned)L.nx + (unsigned)x)
+                                        : load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
+                bin = ori_vote_fast(nb, win32, ox * ox + oy * oy + oz * oz, dirs, icp, K, vote);
+            }
+        }
+        red_vote(hist, bin, vote);
+    }
+    return inside_cnt;
+}
+
 // Dense per-voxel gradient data for a batched level: (gx, gy, gz, |g|) with
 // |g| evaluated in fp64 (no fp32 underflow for tiny nonzero gradients) and
 // rounded once, plus the exact nearest icosphere direction (255 for g == 0).
@@ -398,28 +433,12 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
                         }
                     }
                 }
-                red_vote(hist, bin, vote);
+                red_vote(vote_copy(hist), bin, vote);
             }
         } else if (!exact_only) {
-            // z-major ball walk: consecutive lanes take consecutive x -> coalesced gathers
-            int pn = tid < ball.count ? __ldg(ball_offsets + ball.zstart + tid) : 0;
-            for (int base = 0; base < ball.count; base += kOriThreads) {
-                const int j = base + tid;
-                const int p = pn;
-                if (j + kOriThreads < ball.count) pn = __ldg(ball_offsets + ball.zstart + j + kOriThreads);
-                int bin = -1;
-                float vote = 0.f;
-                if (j < ball.count) {
-                    const int ox = unpack_off(p, 0), oy = unpack_off(p, 1), oz = unpack_off(p, 2);
-                    const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
-                    if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
-                        ++inside_cnt;
-                        bin = ori_vote_fast(load_nb6(data, L.nx, L.ny, L.nz, x, y, z), win32,
-                                            ox * ox + oy * oy + oz * oz, sh.dirs, icp, K, vote);
-                    }
-                }
-                red_vote(hist, bin, vote);
-            }
+            inside_cnt = ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz)
+                             ? ori_walk<true>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, K, hist)
+                             : ori_walk<false>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, K, hist);
         } else {
             for (int j = tid; j < ball.count; j += kOriThreads) {
                 const int p = __ldg(ball_offsets + ball.start + j);
@@ -621,10 +640,7 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
         return VK_ERR_PARAMETER;
     }
     if (n_kp_max == 0) return VK_OK;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = n_kp_max < sms * kAccumCtasPerSm ? n_kp_max : sms * kAccumCtasPerSm;
+    const int grid = accum_grid(orient_kernel, kOriThreads, n_kp_max);
     IcoT ico{};
     if (ico_host && K == 42) {
         ico.valid = 1;

@@ -74,6 +74,8 @@ def to_device(arr: np.ndarray, stream=None):
     """numpy data[x, y, z] -> CUDA tensor (nz, ny, nx), x fastest (vk_transpose)."""
     t = _lib.torch()
     a = np.ascontiguousarray(arr, dtype=np.float32)
+    if not a.flags.writeable:
+        a = a.copy()
     nx, ny, nz = a.shape
     src = t.from_numpy(a).to("cuda", non_blocking=False)
     dst = t.empty((nz, ny, nx), dtype=t.float32, device="cuda")
