@@ -259,6 +259,13 @@ int vk_describe_patch(int kind, const vk_frame* frames, const double* rot, const
                       const vk_level* source, int side, const double* grid_host,
                       const float* taps_host, int radius, const double* pts, int npairs,
                       uint8_t* bits_out, uint16_t* ranks_out, void* stream);
+/* extract_patch (descriptor.py:96-111), optionally followed by preblur_patch
+ * (descriptor.py:196-202) when radius > 0: the side^3 reoriented fp32 patch of
+ * each frame, [x][y][z] (z fastest) like Patch.data, into patch_out
+ * (n_frames x side^3, device).  Same arguments as vk_describe_patch. */
+int vk_extract_patches(const vk_frame* frames, const double* rot, const int* n_frames_dev, int n_frames_max,
+                       const vk_kp* kps, const double* pos, const double* sigma, const vk_level* source, int side,
+                       const double* grid_host, const float* taps_host, int radius, float* patch_out, void* stream);
 
 /* --------------------------------------------------------------- matching */
 /* nearest_neighbor_matches (match.py:81-121).  metric 0 = hamming on packed

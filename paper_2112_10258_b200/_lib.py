@@ -51,6 +51,7 @@ SIGNATURES = {
     "vk_describe_siftrank": [P, P, P, P, P, I, I, P, P, P, P, P, I, P, P, P, P],
     "vk_gradient_volume": [P, P, P, I, I, I, I, P, P, P],
     "vk_describe_patch": [I, P, P, P, I, P, P, P, P, I, P, P, I, P, I, P, P, P],
+    "vk_extract_patches": [P, P, P, I, P, P, P, P, I, P, P, I, P, P],
     "vk_match": [I, P, I, P, I, I, D, P, P, P, P, P],
     "vk_match_excluding": [I, P, I, P, I, I, D, I, I, P, P, P, P, P],
     "vk_set_match_path": [I],

@@ -95,16 +95,21 @@ __device__ __noinline__ int sr_obits_exact(int ox, int oy, int oz, const double*
 // centre give exact zeros for axes with zero coordinates), gradient
 // components need the exact fp64 gradient (rare).
 //
-// Rc holds the frame's columns (R[0][j], R[1][j], R[2][j], 0) as fp32 in
-// shared memory, read with a volatile vector load per use: the compiler would
-// otherwise hoist 9 x F rotation floats into registers for the whole walk and
-// halve the resident warps of this latency-bound loop.
-VK_D float4 lds_col(const float4* p) {
-    float4 v;
+// Rc holds each frame column j = (R[0][j], R[1][j], R[2][j]) as fp32 pairs
+// (cx, cx, cy, cy), (cz, cz, -, -) in shared memory, read with volatile vector
+// loads per use: the compiler would otherwise hoist 9 x F rotation floats into
+// registers for the whole walk and halve the resident warps of this
+// latency-bound loop.  The offset and gradient components of one column are
+// evaluated together with packed fp32x2 multiply / FMA (same per-lane
+// rounding as the scalar chain fmaf(z, cz, fmaf(y, cy, x * cx))).
+constexpr int kRcPerFrame = 6;  // float4 slots per frame
+
+VK_D void lds_col(const float4* p, float2& xx, float2& yy, float2& zz) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "r"((unsigned)__cvta_generic_to_shared(p)));
-    return v;
+                 : "=f"(xx.x), "=f"(xx.y), "=f"(yy.x), "=f"(yy.y)
+                 : "r"(a));
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(zz.x), "=f"(zz.y) : "r"(a + 16u));
 }
 
 VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const double* R, const float4* Rc,
@@ -112,17 +117,18 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
     const float fx = (float)ox, fy = (float)oy, fz = (float)oz;
     const float eo = 1.0e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
     const float eg = 1.0e-6f * (fabsf(gx) + fabsf(gy) + fabsf(gz)) + 1.0e-40f;
+    const float2 vx = make_float2(fx, gx), vy = make_float2(fy, gy), vz = make_float2(fz, gz);
     int sp = 0, og = 0;
     bool osure = true, gsure = true;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        const float4 c = lds_col(Rc + j);
-        const float r = fmaf(fz, c.z, fmaf(fy, c.y, fx * c.x));
-        const float g = fmaf(gz, c.z, fmaf(gy, c.y, gx * c.x));
-        sp |= (int)(r > 0.f) << j;
-        og |= (int)(g > 0.f) << j;
-        osure = osure && fabsf(r) > eo;
-        gsure = gsure && fabsf(g) > eg;
+        float2 cxx, cyy, czz;
+        lds_col(Rc + 2 * j, cxx, cyy, czz);
+        const float2 t = __ffma2_rn(vz, czz, __ffma2_rn(vy, cyy, __fmul2_rn(vx, cxx)));  // (r_j, g_j)
+        sp |= (int)(t.x > 0.f) << j;
+        og |= (int)(t.y > 0.f) << j;
+        osure = osure && fabsf(t.x) > eo;
+        gsure = gsure && fabsf(t.y) > eg;
     }
     if (!osure) sp = sr_obits_exact(ox, oy, oz, R);
     if (!gsure) og = sr_gbits_exact(data, nx, ny, nz, x, y, z, R);
@@ -180,7 +186,7 @@ VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const fl
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
             if (f >= F) break;
-            const int bin = has ? sr_bin_fast(ox, oy, oz, gx, gy, gz, Rs + 9 * f, Rc + 3 * f, data, L.nx, L.ny, L.nz, x,
+            const int bin = has ? sr_bin_fast(ox, oy, oz, gx, gy, gz, Rs + 9 * f, Rc + kRcPerFrame * f, data, L.nx, L.ny, L.nz, x,
                                               y, z)
                                 : -1;
             red_vote(hist + f * kSrBins, bin, mag);
@@ -200,7 +206,7 @@ VK_D int sr_walk_frames(const vk_kp& kp, const vk_level& L, const float* data, c
         case 4: return sr_walk<4, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);
         default: {  // > 4 frames: two passes of up to 4 frames
             const int cnt = sr_walk<4, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, 4);
-            sr_walk<4, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs + 36, Rc + 12, hist + 4 * kSrBins, F - 4);
+            sr_walk<4, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs + 36, Rc + 4 * kRcPerFrame, hist + 4 * kSrBins, F - 4);
             return cnt;
         }
     }
@@ -273,7 +279,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
     __shared__ double w[kSrBins];
     __shared__ int order[kSrBins];
     __shared__ double Rs[VK_MAX_FRAMES * 9];
-    __shared__ float4 Rc[VK_MAX_FRAMES * 3];
+    __shared__ float4 Rc[VK_MAX_FRAMES * kRcPerFrame];
     __shared__ int xb[kSrThreads];
     __shared__ double xv[kSrThreads];
     __shared__ int n_inside;
@@ -295,7 +301,9 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
         for (int i = tid; i < F * 3; i += kSrThreads) {
             const double* R = Rs + 9 * (i / 3);
             const int j = i % 3;
-            Rc[i] = make_float4((float)R[j], (float)R[3 + j], (float)R[6 + j], 0.f);
+            const float cx = (float)R[j], cy = (float)R[3 + j], cz = (float)R[6 + j];
+            Rc[(i / 3) * kRcPerFrame + 2 * j] = make_float4(cx, cx, cy, cy);
+            Rc[(i / 3) * kRcPerFrame + 2 * j + 1] = make_float4(cz, cz, 0.f, 0.f);
         }
         zero_hist(hist, F * kSrBins);
         if (tid == 0) n_inside = 0;
@@ -365,7 +373,8 @@ __global__ void __launch_bounds__(kPatchThreads)
 patch_kernel(int kind, const vk_frame* __restrict__ frames, const double* __restrict__ rot, const int* __restrict__ n_dev,
              int n_max, const vk_kp* __restrict__ kps, const double* __restrict__ pos, const double* __restrict__ sigma,
              const vk_level* __restrict__ source, int side, PatchParams pp, int radius,
-             const double* __restrict__ pts, int npairs, uint8_t* __restrict__ bits_out, uint16_t* __restrict__ ranks_out) {
+             const double* __restrict__ pts, int npairs, uint8_t* __restrict__ bits_out, uint16_t* __restrict__ ranks_out,
+             float* __restrict__ patch_out) {
     extern __shared__ float pbuf[];  // 2 x side^3 floats, then npairs doubles
     const int n3 = side * side * side;
     float* p0 = pbuf;
@@ -417,6 +426,11 @@ patch_kernel(int kind, const vk_frame* __restrict__ frames, const double* __rest
                 cur = nxt;
                 nxt = t;
             }
+        }
+        if (kind == 0) {  // the (pre-blurred) patch itself, [x][y][z] like Patch.data
+            for (int i = tid; i < n3; i += kPatchThreads) patch_out[(long long)item * n3 + i] = cur[i];
+            __syncthreads();
+            continue;
         }
         // 3. pair samples (descriptor.py:205-212) and their differences
         for (int k = tid; k < npairs; k += kPatchThreads) {
@@ -506,7 +520,36 @@ extern "C" int vk_describe_patch(int kind, const vk_frame* frames, const double*
     }
     patch_kernel<<<grid_for(n_frames_max, 4), kPatchThreads, smem, as_stream(stream)>>>(
         kind, frames, rot, n_frames_dev, n_frames_max, kps, pos, sigma, source, side, pp, radius, pts, npairs, bits_out,
-        ranks_out);
+        ranks_out, nullptr);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "patch launch");
+}
+
+extern "C" int vk_extract_patches(const vk_frame* frames, const double* rot, const int* n_frames_dev, int n_frames_max,
+                                  const vk_kp* kps, const double* pos, const double* sigma, const vk_level* source,
+                                  int side, const double* grid_host, const float* taps_host, int radius,
+                                  float* patch_out, void* stream) {
+    if (!frames || !rot || n_frames_max < 0 || !kps || !pos || !sigma || !source || side < 1 || side > kMaxSide ||
+        (side % 2) == 0 || !grid_host || radius < 0 || 2 * radius + 1 > VK_MAX_TAPS || (radius > 0 && !taps_host) ||
+        !patch_out) {
+        set_error("vk_extract_patches: bad arguments (side=%d radius=%d)", side, radius);
+        return VK_ERR_PARAMETER;
+    }
+    if (n_frames_max == 0) return VK_OK;
+    PatchParams pp{};
+    for (int i = 0; i < side; ++i) pp.grid[i] = grid_host[i];
+    for (int i = 0; i < 2 * radius + 1 && radius > 0; ++i) pp.taps[i] = taps_host[i];
+    const int n3 = side * side * side;
+    const int smem = 2 * ((n3 + 1) & ~1) * 4;
+    static int configured = 0;
+    if (smem > 48 * 1024 && configured < smem) {
+        cudaError_t e = cudaFuncSetAttribute(patch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return cuda_status(e, "patch attribute");
+        configured = smem;
+    }
+    patch_kernel<<<grid_for(n_frames_max, 4), kPatchThreads, smem, as_stream(stream)>>>(
+        0, frames, rot, n_frames_dev, n_frames_max, kps, pos, sigma, source, side, pp, radius, nullptr, 0, nullptr,
+        nullptr, patch_out);
     count_launch();
     return cuda_status(cudaGetLastError(), "patch launch");
 }

@@ -3,8 +3,13 @@
 Same names and semantics as descriptor.py:30-316.  ``describe_all`` and
 ``sift_rank_descriptor`` run ``vk_describe_siftrank``; BRIEF / RRIEF run
 ``vk_describe_patch`` (patch extraction, pre-blur and pair sampling fused in
-one CTA per frame).  ``sample_point_pairs`` is the reference's host RNG draw
-(a per-run constant table, uploaded once).
+one CTA per frame).  The per-record building blocks the reference exposes
+(``extract_patch``, ``preblur_patch``, ``brief_descriptor``,
+``rrief_descriptor``) run the same device code one stage at a time
+(``vk_extract_patches``, the pyramid blur, ``vk_sample_trilinear``).
+``sample_point_pairs`` is the reference's host RNG draw (a per-run constant
+table, uploaded once); ``pack_bits`` / ``pack_ranks`` and their inverses are
+host byte helpers.
 """
 
 from __future__ import annotations
@@ -22,6 +27,14 @@ Kind = Literal["siftrank", "brief", "rrief"]
 KINDS = ("siftrank", "brief", "rrief")
 SIFT_RANK_LENGTH = 64
 PAIR_SUPPORT_RADIUS = T.PAIR_SUPPORT_RADIUS
+
+
+@dataclass(frozen=True)
+class Patch:
+    """descriptor.py:37-42: (side, side, side) fp32 resample, [x, y, z]."""
+
+    side: int
+    data: np.ndarray
 
 
 @dataclass(frozen=True)
@@ -131,6 +144,54 @@ def sample_point_pairs(method: int, n: int, sigma_unit: float = 1.0, seed: int =
     return PointPairSet(method, n, float(sigma_unit), int(seed), p1, p2)
 
 
+def extract_patch(pyr, kp, frame, side: int = 15) -> Patch:
+    """descriptor.py:96-111 on the GPU: side^3 fp64 trilinear samples of the
+    unblurred source spanning +-2 sigma along the frame axes, cast to fp32."""
+    from .stages import run_patches
+
+    if side < 1 or side % 2 == 0:
+        raise ParameterError(f"patch side must be odd and >= 1, got {side}")
+    if pyr.source is None:
+        raise ParameterError("pyramid carries no source volume for patch extraction")
+    data = run_patches(pyr, [kp], [(0, frame.rotation)], side)[0]
+    data.setflags(write=False)
+    return Patch(side, data)
+
+
+def preblur_patch(p: Patch, blur_sigma: float) -> Patch:
+    """descriptor.py:196-202: separable Gaussian blur of the patch (the
+    pyramid's blur kernels, replicate borders); 0 returns the patch."""
+    from .scalespace import convolve_array
+
+    if blur_sigma < 0:
+        raise ParameterError(f"blur_sigma must be >= 0, got {blur_sigma}")
+    if blur_sigma == 0:
+        return p
+    return Patch(p.side, convolve_array(p.data, T.gaussian_kernel(blur_sigma)))
+
+
+def _pair_samples(patch: Patch, pairs: PointPairSet) -> tuple[np.ndarray, np.ndarray]:
+    """descriptor.py:205-212: fp64 trilinear samples of the pair endpoints."""
+    from .volume import sample_trilinear_array
+
+    center = (patch.side - 1) / 2.0
+    scale = (patch.side - 1) / (2.0 * PAIR_SUPPORT_RADIUS) / pairs.sigma_unit
+    return (sample_trilinear_array(patch.data, center + pairs.p1 * scale),
+            sample_trilinear_array(patch.data, center + pairs.p2 * scale))
+
+
+def brief_descriptor(p: Patch, pairs: PointPairSet) -> BriefDescriptor:
+    """descriptor.py:215-218: bit k = sample(p1_k) - sample(p2_k) > 0."""
+    s1, s2 = _pair_samples(p, pairs)
+    return BriefDescriptor((s1 - s2 > 0).astype(np.uint8))
+
+
+def rrief_descriptor(p: Patch, pairs: PointPairSet) -> RriefDescriptor:
+    """descriptor.py:221-224: stable ranks of the pair differences."""
+    s1, s2 = _pair_samples(p, pairs)
+    return RriefDescriptor(rank_vector(s1 - s2))
+
+
 def sift_rank_descriptor(pyr, kp, frame, radius_factor: float = 4.0) -> SiftRankDescriptor:
     """descriptor.py:227-263 for one (keypoint, frame) on the GPU."""
     from .stages import run_descriptors
@@ -187,3 +248,33 @@ def descriptor_array(records: Sequence[DescriptorRecord], kind: Kind) -> np.ndar
     if kind == "brief":
         return np.packbits(np.stack([r.descriptor.bits for r in records]), axis=1, bitorder="big")
     return np.stack([r.descriptor.ranks for r in records])
+
+
+def pack_bits(bits: np.ndarray) -> bytes:
+    """descriptor.py:319-321: 0/1 bits MSB-first into bytes."""
+    return np.packbits(np.asarray(bits, dtype=np.uint8), bitorder="big").tobytes()
+
+
+def unpack_bits(blob: bytes, n: int) -> np.ndarray:
+    """descriptor.py:324-325."""
+    return np.unpackbits(np.frombuffer(blob, dtype=np.uint8), bitorder="big")[:n]
+
+
+def _bit_weights(bits_per_rank: int) -> np.ndarray:
+    return np.left_shift(1, np.arange(bits_per_rank - 1, -1, -1, dtype=np.int64))
+
+
+def pack_ranks(ranks: np.ndarray, bits_per_rank: int = 6) -> bytes:
+    """descriptor.py:328-334: each rank as ``bits_per_rank`` bits, MSB first,
+    concatenated and packed big-endian (64 ranks -> 48 bytes)."""
+    r = np.asarray(ranks, dtype=np.int64)
+    if r.min() < 0 or r.max() >= (1 << bits_per_rank):
+        raise ParameterError(f"ranks out of range for {bits_per_rank}-bit packing")
+    bits = (r[:, None] & _bit_weights(bits_per_rank)[None, :]) != 0
+    return np.packbits(bits.reshape(-1).astype(np.uint8), bitorder="big").tobytes()
+
+
+def unpack_ranks(blob: bytes, n: int, bits_per_rank: int = 6) -> np.ndarray:
+    """descriptor.py:337-340."""
+    bits = np.unpackbits(np.frombuffer(blob, dtype=np.uint8), bitorder="big")[: n * bits_per_rank]
+    return bits.reshape(n, bits_per_rank).astype(np.int64) @ _bit_weights(bits_per_rank)

@@ -171,3 +171,38 @@ def run_descriptors(pyr, keypoints, rotations, kind="siftrank", pairs=None, patc
                   taps.ctypes.data, radius, d_pts.data_ptr(), pairs.n, out.data_ptr() if code == 1 else None,
                   out.data_ptr() if code == 2 else None, s)
     return out[:m].cpu().numpy()
+
+
+def run_patches(pyr, keypoints, rotations, side=15, blur_sigma=0.0) -> np.ndarray:
+    """(m, side, side, side) fp32 patches for (keypoint index, rotation) pairs:
+    extract_patch (descriptor.py:96-111), pre-blurred when blur_sigma > 0."""
+    t = _lib.torch()
+    if side < 1 or side % 2 == 0:
+        raise ParameterError(f"patch side must be odd and >= 1, got {side}")
+    if blur_sigma < 0:
+        raise ParameterError(f"blur_sigma must be >= 0, got {blur_sigma}")
+    m = len(rotations)
+    view = PyramidView(pyr, need_source=True)
+    rec, pos, sig = keypoint_records(view, keypoints, 4.0, T.BallTable())
+    out = t.empty((max(m, 1), side, side, side), dtype=t.float32, device="cuda")
+    if m == 0:
+        return out[:0].cpu().numpy()
+    fr = np.zeros(m, dtype=_lib.FRAME_DTYPE)
+    rot = np.zeros((m, 9), dtype=np.float64)
+    for j, (ki, R) in enumerate(rotations):
+        fr[j] = (ki, -1, -1, 0)
+        rot[j] = np.asarray(R, dtype=np.float64).reshape(9)
+    grid = np.ascontiguousarray(T.patch_axis(side), dtype=np.float64)
+    if blur_sigma > 0:
+        k = T.gaussian_kernel(blur_sigma)
+        taps, radius = np.ascontiguousarray(k.weights), k.radius
+    else:
+        taps, radius = np.zeros(1, np.float32), 0
+    d_kps, d_fr = _lib.to_device_records(rec), _lib.to_device_records(fr)
+    d_rot = t.from_numpy(rot.reshape(-1).copy()).cuda()
+    d_pos = t.from_numpy(pos.reshape(-1).copy()).cuda()
+    d_sig = t.from_numpy(sig.copy()).cuda()
+    _lib.call("vk_extract_patches", d_fr.data_ptr(), d_rot.data_ptr(), None, m, d_kps.data_ptr(), d_pos.data_ptr(),
+              d_sig.data_ptr(), view.source.data_ptr(), side, grid.ctypes.data, taps.ctypes.data, radius,
+              out.data_ptr(), _lib.stream_ptr())
+    return out[:m].cpu().numpy()

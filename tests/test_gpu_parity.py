@@ -544,3 +544,37 @@ def test_point_samplers_match_oracle():
     assert gradients_at(data, np.zeros((0, 3), dtype=np.int64)).shape == (0, 3)
     with pytest.raises(IndexError):
         gradients_at(data, [[dims[0], 0, 0]])
+
+
+def test_patch_building_blocks_match_oracle():
+    """extract_patch / preblur_patch / brief_descriptor / rrief_descriptor
+    (descriptor.py:96-111,196-224) one stage at a time on the GPU == the
+    oracle, and composed == the fused describe_all records."""
+    from oracle import volkey_oracle as O
+    from paper_2112_10258_b200 import descriptor as D
+
+    g, vol, cfg = case_inputs("small0.npz")
+    res = vk.extract_features(vk.Volume(vol), cfg.model_copy(update={"descriptor": "brief"}))
+    pairs = D.sample_point_pairs(cfg.method, cfg.pairs, 1.0, cfg.seed)
+    opairs = (pairs.p1, pairs.p2)
+    recs_r, _ = D.describe_all(res.pyramid, res.oriented, "rrief", pairs, cfg.patch_side, cfg.blur_sigma)
+    assert len(res.records) >= 8
+    for i in range(0, len(res.records), max(1, len(res.records) // 8)):
+        rec = res.records[i]
+        kp, fr = rec.keypoint, rec.frame
+        okp = O.OKp(tuple(kp.position), kp.sigma, kp.octave, kp.level, kp.dog_value, kp.sign)
+        want = O.patch({"source": vol}, okp, np.asarray(fr.rotation), cfg.patch_side)
+        p = D.extract_patch(res.pyramid, kp, fr, cfg.patch_side)
+        assert isinstance(p, D.Patch) and p.side == cfg.patch_side and np.array_equal(p.data, want)
+        pb = D.preblur_patch(p, cfg.blur_sigma)
+        want_b = O.preblur(want, cfg.blur_sigma)
+        assert np.array_equal(pb.data, want_b)
+        diffs = O.pair_diffs(want_b, opairs)
+        bits = D.brief_descriptor(pb, pairs).bits
+        assert np.array_equal(bits, (diffs > 0).astype(np.uint8))
+        assert np.array_equal(bits, rec.descriptor.bits)
+        ranks = D.rrief_descriptor(pb, pairs).ranks
+        assert np.array_equal(ranks, O.ranks(diffs)) and np.array_equal(ranks, recs_r[i].descriptor.ranks)
+    assert D.preblur_patch(p, 0.0) is p
+    with pytest.raises(vk.ParameterError):
+        D.extract_patch(res.pyramid, kp, fr, 14)

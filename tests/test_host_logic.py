@@ -3,6 +3,7 @@
 import math
 
 import numpy as np
+import pytest
 
 from paper_2112_10258_b200 import tables as T
 from paper_2112_10258_b200.config import PipelineConfig
@@ -105,3 +106,27 @@ def test_ball_table_and_windows():
     ps = planes[balls[i0]["pstart"]: balls[i0]["pstart"] + 2 * r + 2]
     for oz in range(-r, r + 1):
         assert np.all(zo[ps[oz + r]: ps[oz + r + 1], 2] == oz)
+
+
+def test_pack_helpers_round_trip():
+    """pack_bits / unpack_bits / pack_ranks / unpack_ranks (descriptor.py:319-340):
+    MSB-first packing, 64 six-bit ranks -> 48 bytes, out-of-range ranks rejected."""
+    from paper_2112_10258_b200 import descriptor as D
+    from paper_2112_10258_b200.errors import ParameterError
+
+    rng = np.random.default_rng(3)
+    bits = rng.integers(0, 2, 64).astype(np.uint8)
+    blob = D.pack_bits(bits)
+    assert len(blob) == 8 and blob[0] == int("".join(map(str, bits[:8])), 2)
+    assert np.array_equal(D.unpack_bits(blob, 64), bits)
+    ranks = rng.permutation(64)
+    blob = D.pack_ranks(ranks)
+    assert len(blob) == 48
+    assert np.array_equal(D.unpack_ranks(blob, 64), ranks)
+    stream = "".join(format(int(r), "06b") for r in ranks)
+    assert blob == int(stream, 2).to_bytes(48, "big")
+    assert np.array_equal(D.unpack_ranks(D.pack_ranks([5, 1, 7], 3), 3, 3), [5, 1, 7])
+    with pytest.raises(ParameterError):
+        D.pack_ranks([64])
+    with pytest.raises(ParameterError):
+        D.pack_ranks([-1])
