@@ -103,6 +103,9 @@ __device__ __noinline__ int sr_obits_exact(int ox, int oy, int oz, const double*
 // evaluated together with packed fp32x2 multiply / FMA (same per-lane
 // rounding as the scalar chain fmaf(z, cz, fmaf(y, cy, x * cx))).
 constexpr int kRcPerFrame = 6;  // float4 slots per frame
+#ifndef VK_SR_PACKED
+#define VK_SR_PACKED 1
+#endif
 
 VK_D void lds_col(const float4* p, float2& xx, float2& yy, float2& zz) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(p);
@@ -124,7 +127,12 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
     for (int j = 0; j < 3; ++j) {
         float2 cxx, cyy, czz;
         lds_col(Rc + 2 * j, cxx, cyy, czz);
+#if VK_SR_PACKED
         const float2 t = __ffma2_rn(vz, czz, __ffma2_rn(vy, cyy, __fmul2_rn(vx, cxx)));  // (r_j, g_j)
+#else
+        const float2 t = make_float2(fmaf(fz, czz.x, fmaf(fy, cyy.x, fx * cxx.x)),
+                                     fmaf(gz, czz.x, fmaf(gy, cyy.x, gx * cxx.x)));
+#endif
         sp |= (int)(t.x > 0.f) << j;
         og |= (int)(t.y > 0.f) << j;
         osure = osure && fabsf(t.x) > eo;
@@ -195,10 +203,74 @@ VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const fl
     return cnt;
 }
 
+// Interior walk with the six neighbour loads of the thread's next voxel issued
+// before the current voxel's bins are computed (two voxels in flight per
+// thread): the walk is bound by L1 hit latency, not by issue.
+template <int NF>
+VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
+                      const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist, int F) {
+    const int tid = threadIdx.x;
+    const int step = blockDim.x;
+    const int nx = L.nx, plane = L.nx * L.ny;
+    const int kc = (kp.iz * L.ny + kp.iy) * nx + kp.ix;
+    const int zpf = L.nz - kPrefetchPlanes - kp.iz;  // prefetch plane exists while oz < zpf
+    const int* offs = ball_offsets + ball.zstart;
+    hist = vote_copy(hist);
+    auto issue = [&](int pk, Nb6& n) {
+        const int ox = unpack_off(pk, 0), oy = unpack_off(pk, 1), oz = unpack_off(pk, 2);
+        const int c = kc + oz * plane + oy * nx + ox;
+        if (oz < zpf) asm volatile("prefetch.global.L1 [%0];" ::"l"(data + c + kPrefetchPlanes * plane));
+        n = load_nb6_interior(data, (unsigned)nx, (unsigned)plane, (unsigned)c);
+    };
+    int p = tid < ball.count ? __ldg(offs + tid) : 0;
+    Nb6 nb{};
+    if (tid < ball.count) issue(p, nb);
+    int pn = tid + step < ball.count ? __ldg(offs + tid + step) : 0;
+    int cnt = 0;
+    for (int base = 0; base < ball.count; base += step) {
+        const int j = base + tid;
+        const int pc = p;
+        const Nb6 cur = nb;
+        p = pn;
+        if (j + step < ball.count) {
+            issue(p, nb);
+            if (j + 2 * step < ball.count) pn = __ldg(offs + j + 2 * step);
+        }
+        if (j < ball.count) {
+            ++cnt;
+            float gx, gy, gz;
+            grad32(cur, gx, gy, gz);
+            if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {  // zero vote: no bin changes
+                const float mag = norm3_f32(gx, gy, gz);
+                const int ox = unpack_off(pc, 0), oy = unpack_off(pc, 1), oz = unpack_off(pc, 2);
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    if (f >= F) break;
+                    const int bin = sr_bin_fast(ox, oy, oz, gx, gy, gz, Rs + 9 * f, Rc + kRcPerFrame * f, data, L.nx,
+                                                L.ny, L.nz, kp.ix + ox, kp.iy + oy, kp.iz + oz);
+                    red_vote(hist + f * kSrBins, bin, mag);
+                }
+            }
+        }
+    }
+    return cnt;
+}
+
 template <bool INTERIOR>
 VK_D int sr_walk_frames(const vk_kp& kp, const vk_level& L, const float* data, const float4* g4, const vk_ball& ball,
                         const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist,
                         int F) {
+#ifndef VK_SR_PIPE
+#define VK_SR_PIPE 1
+#endif
+    if (VK_SR_PIPE && INTERIOR && !g4 && F <= 4) {
+        switch (F) {
+            case 1: return sr_walk_pipe<1>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F);
+            case 2: return sr_walk_pipe<2>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F);
+            case 3: return sr_walk_pipe<3>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F);
+            default: return sr_walk_pipe<4>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F);
+        }
+    }
     switch (F) {
         case 1: return sr_walk<1, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);
         case 2: return sr_walk<2, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);

@@ -197,3 +197,23 @@ def build_dog_pyramid(g: GaussianPyramid, recorder=None) -> DoGPyramid:
             diffs.append(DeviceVolume(out, oc.levels[i].spacing))
         octaves.append(DoGOctave(diffs, list(oc.sigmas[:-1])))
     return DoGPyramid(octaves, g.kappa, g.levels_per_octave)
+
+
+_incremental_sigma = incremental_sigma  # scalespace.py:154-155
+
+
+def dump_pyramid(g: GaussianPyramid, directory) -> list[str]:
+    """scalespace.py:226-235: every level as ``oct{o}_lvl{i}_sigma{s:.4g}.f32``
+    (+ header sidecar); device levels are written straight from their
+    x-fastest layout.  Returns the data paths."""
+    import os
+
+    from .ingest import save_raw
+
+    os.makedirs(directory, exist_ok=True)
+    written = []
+    for o, oc in enumerate(g.octaves):
+        for i, (lv, sigma) in enumerate(zip(oc.levels, oc.sigmas)):
+            path, _ = save_raw(lv, os.path.join(str(directory), f"oct{o}_lvl{i}_sigma{sigma:.4g}"))
+            written.append(path)
+    return written

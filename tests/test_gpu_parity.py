@@ -578,3 +578,17 @@ def test_patch_building_blocks_match_oracle():
     assert D.preblur_patch(p, 0.0) is p
     with pytest.raises(vk.ParameterError):
         D.extract_patch(res.pyramid, kp, fr, 14)
+
+
+def test_dump_pyramid_round_trip(tmp_path):
+    """dump_pyramid (scalespace.py:226-235): one .f32 per level, named by
+    octave / level / sigma, reloading to the level's voxels."""
+    from paper_2112_10258_b200.scalespace import build_gaussian_pyramid, dump_pyramid
+
+    vol = synthetic.random_blob_phantom((20, 18, 16), np.random.default_rng(2), n_blobs=4, margin=3, noise=0.02)
+    g = build_gaussian_pyramid(vk.Volume(vol), num_octaves=2)
+    paths = dump_pyramid(g, tmp_path / "dump")
+    assert len(paths) == sum(len(o.levels) for o in g.octaves)
+    assert paths[0].endswith("oct0_lvl0_sigma%.4g.f32" % g.octaves[0].sigmas[0])
+    back = vk.load_volume(paths[-1])
+    assert np.array_equal(back.data, g.octaves[-1].levels[-1].data)
