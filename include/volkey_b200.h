@@ -197,7 +197,8 @@ long long vk_accum_work_bytes(int device);
  * only): int[132] = 12 icosahedron-vertex indices into dirs, 12x5 indices of
  * the edge midpoints around each vertex, and the same 12x5 midpoints ordered
  * by neighbour kind (tables.icosphere_structure), enabling the screened and
- * the fast argmax.
+ * the fast argmax.  ico_lut (nullable, device, with ico_host): uint8[128*128 +
+ * 42*24] exact-argmax lookup table (tables.icosphere_lut), tried first.
  * exact_only != 0 forces the reference accumulation order and the brute-force
  * argmax for every keypoint (weights then bit-identical to the reference).
  * grads (nullable, indexed like levels): precomputed gradient volumes
@@ -209,7 +210,8 @@ int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_leve
               const float* windows32, const double* dirs, int K, const uint8_t* pair_ok,
               double secondary_ratio, int max_frames,
               double* weights, int* nframes, int* prim, int* sec, int* status,
-              int exact_only, const int* ico_host, const vk_gradlevel* grads, double* work, void* stream);
+              int exact_only, const int* ico_host, const uint8_t* ico_lut, const vk_gradlevel* grads,
+              double* work, void* stream);
 
 /* dominant_orientations (orient.py:310-350) on n caller-supplied K-bin
  * weight vectors (exact comparisons). */

@@ -45,7 +45,7 @@ SIGNATURES = {
     "vk_detect_octave": [P, I, I, I, I, I, I, I, F, P, P, I, P],
     "vk_extrema_from_map": [P, P, I, I, I, I, I, F, P, P, I, P],
     "vk_order_keypoints": [P, P, I, I, P, P, I, P, P, P, P, P, P, P, P, I, P],
-    "vk_orient": [P, P, I, P, P, P, P, P, P, I, P, D, I, P, P, P, P, P, I, P, P, P, P],
+    "vk_orient": [P, P, I, P, P, P, P, P, P, I, P, D, I, P, P, P, P, P, I, P, P, P, P, P],
     "vk_frames_from_weights": [P, I, I, P, D, I, P, P, P, P],
     "vk_expand_frames": [P, P, P, P, I, I, P, I, P, P, P, P, I, P, P],
     "vk_describe_siftrank": [P, P, P, P, P, I, I, P, P, P, P, P, I, P, P, P, P],

@@ -162,9 +162,36 @@ VK_D int nearest_dir_fast(const IcoSh& ic, float gx, float gy, float gz, float a
     return ic.fk[6 * slot + kind];
 }
 
-VK_D int nearest_dir_ico(const double* dirs, const IcoSh& ic, float gx, float gy, float gz, const Nb6& nb) {
+// Table lookup of the exact argmax (tables.icosphere_lut): canonical face
+// point (p / r, q / r) of |g| -> cell -> canonical direction -> actual
+// direction by (permutation, sign bits).  -1 when the cell is crossed by a
+// Voronoi boundary (2.7% of cells) or |g| is too small for the division.
+constexpr int kLutN = 128;
+constexpr int kLutBytes = kLutN * kLutN + 42 * 24;
+
+VK_D int nearest_dir_lut(const uint8_t* lut, float gx, float gy, float gz, float ax, float ay, float az) {
+    float p, q, r;
+    int perm;
+    if (az >= ax && az >= ay) { p = ax; q = ay; r = az; perm = 0; }
+    else if (ax >= ay) { p = ay; q = az; r = ax; perm = 1; }
+    else { p = az; q = ax; r = ay; perm = 2; }
+    if (!(r > 1.0e-30f)) return -1;
+    const int iu = min(__float2int_rz(__fdividef(p, r) * (float)kLutN), kLutN - 1);
+    const int iv = min(__float2int_rz(__fdividef(q, r) * (float)kLutN), kLutN - 1);
+    const int c = lut[iv * kLutN + iu];
+    if (c == 255) return -1;
+    const int sb = (gx < 0.f) | ((gy < 0.f) << 1) | ((gz < 0.f) << 2);
+    return lut[kLutN * kLutN + c * 24 + perm * 8 + sb];
+}
+
+VK_D int nearest_dir_ico(const double* dirs, const IcoSh& ic, const uint8_t* lut, float gx, float gy, float gz,
+                         const Nb6& nb) {
     constexpr float PHI = 1.6180339887498949f;
     const float ax = fabsf(gx), ay = fabsf(gy), az = fabsf(gz);
+    if (lut) {
+        const int k = nearest_dir_lut(lut, gx, gy, gz, ax, ay, az);
+        if (k >= 0) return k;
+    }
     const float l1 = ax + ay + az;
     const float vA = fmaf(PHI, az, ay), vB = fmaf(PHI, ay, ax), vC = fmaf(PHI, ax, az);
     const float m = 1.0e-5f * 2.7f * l1;
@@ -218,12 +245,12 @@ VK_D int nearest_dir_ico(const double* dirs, const IcoSh& ic, float gx, float gy
 // <= kVoteRel against the reference vote) into the exactly determined nearest
 // direction.  Returns -1 for zero gradients (mag == 0 exactly in the reference).
 VK_D int ori_vote_fast(const Nb6& n, const float* __restrict__ win32, int d2, const double* dirs, const IcoSh* ic,
-                       int K, float& vote) {
+                       const uint8_t* lut, int K, float& vote) {
     float gx, gy, gz;
     grad32(n, gx, gy, gz);
     if (gx == 0.f && gy == 0.f && gz == 0.f) return -1;
     vote = fmul(norm3_f32(gx, gy, gz), __ldg(win32 + d2));
-    if (ic) return nearest_dir_ico(dirs, *ic, gx, gy, gz, n);
+    if (ic) return nearest_dir_ico(dirs, *ic, lut, gx, gy, gz, n);
     double x64, y64, z64;
     grad64(n, x64, y64, z64);
     return nearest_dir(dirs, K, x64, y64, z64);
@@ -235,7 +262,7 @@ VK_D int ori_vote_fast(const Nb6& n, const float* __restrict__ win32, int d2, co
 template <bool INTERIOR>
 VK_D int ori_walk(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
                   const int* __restrict__ ball_offsets, const float* __restrict__ win32, const double* dirs,
-                  const IcoSh* icp, int K, double* hist) {
+                  const IcoSh* icp, const uint8_t* lut, int K, double* hist) {
     const int tid = threadIdx.x;
     const unsigned plane = (unsigned)L.nx * (unsigned)L.ny;
     hist = vote_copy(hist);
@@ -256,7 +283,7 @@ VK_D int ori_walk(const vk_kp& kp, const vk_level& L, const float* data, const v
                                                             ((unsigned)z * (unsigned)L.ny + (unsigned)y) *
                                                                     (unsigned)L.nx + (unsigned)x)
                                         : load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
-                bin = ori_vote_fast(nb, win32, ox * ox + oy * oy + oz * oz, dirs, icp, K, vote);
+                bin = ori_vote_fast(nb, win32, ox * ox + oy * oy + oz * oz, dirs, icp, lut, K, vote);
             }
         }
         red_vote(hist, bin, vote);
@@ -300,7 +327,7 @@ gradient_volume_kernel(const float* __restrict__ level, float4* __restrict__ g4,
             double x64, y64, z64;
             grad64(n, x64, y64, z64);
             o.w = (float)norm3_numpy(x64, y64, z64);
-            bin = nearest_dir_ico(dirs, ic, gx, gy, gz, n);
+            bin = nearest_dir_ico(dirs, ic, nullptr, gx, gy, gz, n);
         }
         g4[i] = o;
         bins[i] = (uint8_t)bin;
@@ -379,9 +406,11 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
               const float* __restrict__ windows32, const double* __restrict__ dirs_g, int K,
               const uint8_t* __restrict__ pair_ok, double ratio, int max_frames, double* __restrict__ weights,
               int* __restrict__ nframes, int* __restrict__ prim, int* __restrict__ sec, int* __restrict__ status,
-              int exact_only, IcoT ico, const vk_gradlevel* __restrict__ grads, double* __restrict__ work) {
+              int exact_only, IcoT ico, const uint8_t* __restrict__ ico_lut, const vk_gradlevel* __restrict__ grads,
+              double* __restrict__ work) {
     __shared__ OriShared sh;
     __shared__ IcoSh ic;
+    __shared__ __align__(16) uint8_t lut[kLutBytes];
     double* hist = work + (long long)blockIdx.x * kAccumSlot;  // [K] fp64, L2-resident
     const int tid = threadIdx.x;
     for (int i = tid; i < 3 * K; i += kOriThreads) sh.dirs[i] = dirs_g[i];
@@ -395,6 +424,10 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
     for (int i = tid; i < K * K; i += kOriThreads) sh.ok[i] = pair_ok[i];
     const int n_kp = n_kp_dev ? min(*n_kp_dev, n_kp_max) : n_kp_max;
     const IcoSh* icp = ico.valid ? &ic : nullptr;
+    const uint8_t* lutp = ico.valid && ico_lut ? lut : nullptr;
+    if (lutp)
+        for (int i = tid; i < kLutBytes / 4; i += kOriThreads)
+            reinterpret_cast<uint32_t*>(lut)[i] = __ldg(reinterpret_cast<const uint32_t*>(ico_lut) + i);
     __syncthreads();
 
     for (int item = blockIdx.x; item < n_kp; item += gridDim.x) {
@@ -437,8 +470,8 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
             }
         } else if (!exact_only) {
             inside_cnt = ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz)
-                             ? ori_walk<true>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, K, hist)
-                             : ori_walk<false>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, K, hist);
+                             ? ori_walk<true>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, K, hist)
+                             : ori_walk<false>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, K, hist);
         } else {
             for (int j = tid; j < ball.count; j += kOriThreads) {
                 const int p = __ldg(ball_offsets + ball.start + j);
@@ -632,7 +665,8 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
                          const vk_ball* balls, const int* ball_offsets, const double* windows, const float* windows32,
                          const double* dirs, int K, const uint8_t* pair_ok, double secondary_ratio, int max_frames,
                          double* weights, int* nframes, int* prim, int* sec, int* status, int exact_only,
-                         const int* ico_host, const vk_gradlevel* grads, double* work, void* stream) {
+                         const int* ico_host, const uint8_t* ico_lut, const vk_gradlevel* grads, double* work,
+                         void* stream) {
     if (!kps || n_kp_max < 0 || !levels || !balls || !ball_offsets || !windows || !windows32 || !dirs || K < 1 || !work ||
         K > VK_MAX_DIRS || !pair_ok || !nframes || !prim || !sec || !status || max_frames < 1 ||
         max_frames > VK_MAX_FRAMES || !(secondary_ratio > 0.0 && secondary_ratio <= 1.0)) {
@@ -653,7 +687,7 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
     orient_kernel<<<grid, kOriThreads, 0, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
                                                                windows, windows32, dirs, K, pair_ok, secondary_ratio,
                                                                max_frames, weights, nframes, prim, sec, status,
-                                                               exact_only, ico, grads, work);
+                                                               exact_only, ico, ico_lut, grads, work);
     count_launch();
     return cuda_status(cudaGetLastError(), "orient launch");
 }

@@ -127,6 +127,7 @@ class DeviceTables:
         self.pair_ok = t.from_numpy(ok.copy()).cuda()
         self.rot_table = t.from_numpy(rot.reshape(-1).copy()).cuda()
         self.ico = np.ascontiguousarray(T.icosphere_structure())
+        self.ico_lut = t.from_numpy(T.icosphere_lut().copy()).cuda()
         balls, off, win, planes = plan.balls.arrays()
         self.balls = _lib.to_device_records(balls)
         self.ball_offsets = t.from_numpy(off.copy()).cuda()
@@ -318,7 +319,7 @@ class Extractor:
                   tb.dirs.data_ptr(), tb.K,
                   tb.pair_ok.data_ptr(), float(cfg.secondary_ratio), self.maxf, None, self.nframes.data_ptr(),
                   self.prim.data_ptr(), self.sec.data_ptr(), self.status.data_ptr(), self.exact_only,
-                  tb.ico.ctypes.data, self.grad_table.data_ptr(), self.accum.data_ptr(), s)
+                  tb.ico.ctypes.data, tb.ico_lut.data_ptr(), self.grad_table.data_ptr(), self.accum.data_ptr(), s)
         _lib.call("vk_expand_frames", self.nframes.data_ptr(), self.prim.data_ptr(), self.sec.data_ptr(),
                   self.total.data_ptr(), self.kp_cap, self.maxf, tb.rot_table.data_ptr(), tb.K,
                   self.frames.data_ptr(), self.rot.data_ptr(), self.n_frames.data_ptr(), self.dropped.data_ptr(),

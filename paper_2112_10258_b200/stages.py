@@ -66,6 +66,17 @@ def keypoint_records(view: PyramidView, keypoints, radius_factor: float, balls: 
     return rec, pos, sig
 
 
+_LUT = {}
+
+
+def _ico_lut(t):
+    """Device copy of tables.icosphere_lut (per device, built once)."""
+    dev = t.cuda.current_device()
+    if dev not in _LUT:
+        _LUT[dev] = t.from_numpy(T.icosphere_lut().copy()).cuda()
+    return _LUT[dev]
+
+
 def run_orientation(pyr, keypoints, radius_factor=4.0, secondary_ratio=0.8, max_frames=4, directions=None,
                     exact=False, want_weights=False):
     """Histograms (+ frames) for a list of keypoints.  Returns dict with
@@ -105,7 +116,8 @@ def run_orientation(pyr, keypoints, radius_factor=4.0, secondary_ratio=0.8, max_
     _lib.call("vk_orient", d_kps.data_ptr(), None, n, view.table.data_ptr(), d_balls.data_ptr(), d_off.data_ptr(),
               d_win.data_ptr(), d_win32.data_ptr(), d_dirs.data_ptr(), K, d_ok.data_ptr(), float(secondary_ratio), mf, _lib.ptr(weights),
               nframes.data_ptr(), prim.data_ptr(), sec.data_ptr(), status.data_ptr(), int(bool(exact)),
-              None if ico is None else ico.ctypes.data, None, _lib.accum_work().data_ptr(), _lib.stream_ptr())
+              None if ico is None else ico.ctypes.data, None if ico is None else _ico_lut(t).data_ptr(), None,
+              _lib.accum_work().data_ptr(), _lib.stream_ptr())
     if int(status[0].item()) & 1:
         raise DataError("orientation neighborhood lies entirely outside the volume")
     out = dict(nframes=nframes.cpu().numpy(), prim=prim.cpu().numpy().reshape(n, mf),

@@ -130,6 +130,67 @@ def icosphere_structure() -> np.ndarray:
     return out
 
 
+ICO_LUT_N = 128          # cells per axis of the canonical face
+ICO_LUT_DILATE = 2.0 ** -14  # cell dilation in (u, v): >> fp32 gradient / division error (~1e-6)
+ICO_LUT_MARGIN = 1e-9    # required dot lead at every dilated corner: >> fp64 dot error (~1e-15)
+
+
+def _ico_canonical(a: np.ndarray):
+    """Canonical (p, q, r) of |g| components (r the largest; cyclic order
+    kept) and the permutation id, exactly as csrc/vk_orient.cu computes them."""
+    ax, ay, az = a[..., 0], a[..., 1], a[..., 2]
+    perm = np.where((az >= ax) & (az >= ay), 0, np.where(ax >= ay, 1, 2))
+    p = np.choose(perm, [ax, ay, az])
+    q = np.choose(perm, [ay, az, ax])
+    r = np.choose(perm, [az, ax, ay])
+    return p, q, r, perm
+
+
+def icosphere_lut() -> np.ndarray:
+    """uint8[N*N + 42*24]: exact-argmax lookup for orientation binning.
+
+    The 42 icosphere directions are invariant under axis sign flips and cyclic
+    axis permutations, so np.argmax(g @ dirs.T) follows from the canonical
+    point (u, v) = (p / r, q / r) in [0, 1]^2 of |g| (gnomonic projection onto
+    the face of its largest component).  Voronoi boundaries are great circles,
+    i.e. straight lines in (u, v), so a cell whose four corners, dilated by
+    ICO_LUT_DILATE, all have the same nearest direction with a lead above
+    ICO_LUT_MARGIN has that direction at every point within the dilation --
+    including every gradient whose fp32 canonical coordinates land in it.
+    Table entry = canonical direction index, or 255 for the ~2.7% of cells a
+    boundary crosses (the kernel then takes its screened path).  The trailing
+    42 x 3 x 8 map turns (canonical index, permutation, sign bits of g) into
+    the index of the actual direction."""
+    dirs = icosphere_directions()
+    N, d = ICO_LUT_N, ICO_LUT_DILATE
+    i = np.arange(N)
+    lo, hi = i / N - d, (i + 1) / N + d
+    best, pure = None, np.ones((N, N), bool)
+    for uu, vv in ((lo[None, :], lo[:, None]), (hi[None, :], lo[:, None]), (lo[None, :], hi[:, None]),
+                   (hi[None, :], hi[:, None])):
+        uu, vv = np.broadcast_arrays(uu, vv)
+        x = np.stack([uu, vv, np.ones_like(uu)], -1)  # (iv, iu) rows
+        dots = x @ dirs.T
+        top2 = np.sort(dots, -1)[..., -2:]
+        a = np.argmax(dots, -1)
+        pure &= (top2[..., 1] - top2[..., 0]) > ICO_LUT_MARGIN
+        pure &= a == (a if best is None else best)
+        best = a if best is None else best
+    table = np.where(pure, best, 255).astype(np.uint8).reshape(-1)
+    lmap = np.zeros(42 * 24, dtype=np.uint8)
+    for c in range(42):
+        C = dirs[c]
+        for perm, A in enumerate(((C[0], C[1], C[2]), (C[2], C[0], C[1]), (C[1], C[2], C[0]))):
+            for sb in range(8):
+                D = np.array([-A[k] if (sb >> k) & 1 else A[k] for k in range(3)])
+                k = int(np.argmin(np.linalg.norm(dirs - D, axis=1)))
+                assert np.linalg.norm(dirs[k] - D) < 1e-12
+                lmap[c * 24 + perm * 8 + sb] = k
+    out = np.concatenate([table, lmap])
+    out.setflags(write=False)
+    return out
+
+
 def frame_tables(dirs: np.ndarray):
     """For every (primary p, candidate secondary q): whether q's projection
     orthogonal to p is usable (norm > 1e-6) and the resulting right-handed
