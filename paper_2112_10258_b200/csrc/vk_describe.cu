@@ -333,6 +333,65 @@ __device__ __noinline__ void sr_exact_frame(const float* data, const vk_level& L
     __syncthreads();
 }
 
+// Cheap exact repair of an uncertain rank vector: only the bins in unc[]
+// (members of an adjacent sorted pair whose separation was not certified) are
+// re-accumulated, in the reference's ball order (x-major, np.add.at), with the
+// reference's fp64 votes; every other bin keeps its fast sum.  The ranks of
+// the repaired vector equal the reference's: a certified gap separates the
+// true values as well, and inside an uncertain run the comparisons are now
+// between exact values.  Bins come from the exact fast binning; a vote is
+// computed in fp64 only for voxels in an uncertain bin, and the ordered sums
+// take one thread a few additions per 256-voxel chunk (warp ballots of the
+// contributing entries).
+__device__ __noinline__ void sr_exact_subset(const float* data, const vk_level& L, const vk_kp& kp,
+                                             const vk_ball& ball, const int* __restrict__ ball_offsets,
+                                             const double* Rsm, const float4* Rc, const int* unc, double* w, int* xb,
+                                             double* xv, unsigned* wmask) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid < kSrBins && unc[tid]) w[tid] = 0.0;
+    for (int base = 0; base < ball.count; base += blockDim.x) {
+        const int j = base + tid;
+        int bin = -1;
+        double v = 0.0;
+        if (j < ball.count) {
+            const int p = __ldg(ball_offsets + ball.start + j);
+            const int ox = unpack_off(p, 0), oy = unpack_off(p, 1), oz = unpack_off(p, 2);
+            const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
+            if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
+                const Nb6 nb = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
+                float gx, gy, gz;
+                grad32(nb, gx, gy, gz);
+                if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {
+                    const int b = sr_bin_fast(ox, oy, oz, gx, gy, gz, Rsm, Rc, data, L.nx, L.ny, L.nz, x, y, z);
+                    if (unc[b]) {
+                        double x64, y64, z64;
+                        grad64(nb, x64, y64, z64);
+                        const double g0 = dot3_blas(x64, y64, z64, Rsm[0], Rsm[3], Rsm[6]);
+                        const double g1 = dot3_blas(x64, y64, z64, Rsm[1], Rsm[4], Rsm[7]);
+                        const double g2 = dot3_blas(x64, y64, z64, Rsm[2], Rsm[5], Rsm[8]);
+                        v = norm3_numpy(g0, g1, g2);
+                        bin = b;
+                    }
+                }
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, bin >= 0);
+        if (lane == 0) wmask[wid] = m;
+        xb[tid] = bin;
+        xv[tid] = v;
+        __syncthreads();
+        if (tid == 0) {
+            for (int g = 0; g < (int)(blockDim.x >> 5); ++g)
+                for (unsigned t = wmask[g]; t; t &= t - 1) {
+                    const int q = 32 * g + __ffs(t) - 1;
+                    w[xb[q]] = dadd(w[xb[q]], xv[q]);
+                }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+}
+
 // One CTA per work item = one keypoint and its F frames (contiguous in the
 // frame list).  The ball is walked in z-major order (coalesced gathers);
 // each voxel's gradient is computed once and voted into all F frames.
@@ -355,6 +414,8 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
     __shared__ int xb[kSrThreads];
     __shared__ double xv[kSrThreads];
     __shared__ int n_inside;
+    __shared__ int unc[kSrBins];
+    __shared__ unsigned wmask[kSrThreads / 32];
     const int tid = threadIdx.x;
     const int n = n_items_dev ? min(*n_items_dev, n_items_max) : n_items_max;
     for (int item = blockIdx.x; item < n; item += gridDim.x) {
@@ -413,13 +474,12 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                 order[myrank] = tid;
             }
             __syncthreads();
-            int go_exact = 1;
+            int go_exact = 1, bad = 0;
             if (fast) {
                 // every adjacent pair of the sorted bins must be separated by more than
                 // the bound between our summation and the reference's sequential one
                 const double epsrel = 2.0 * (kVoteRel + gamma_k((double)n_inside + 64.0));
                 const double epsabs = kVoteAbs * n_inside;
-                int bad = 0;
                 if (tid + 1 < kSrBins) {
                     const double a = w[order[tid]], b = w[order[tid + 1]];
                     if (!(a == 0.0 && b == 0.0)) {  // exact empty-bin ties are order-independent
@@ -429,9 +489,21 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                     }
                 }
                 go_exact = __syncthreads_or(bad);
+#ifdef VK_EXP_NO_FALLBACK
+                go_exact = 0;  // timing experiment only: wrong ranks on near ties
+#endif
                 if (go_exact && tid == 0 && stats) atomicAdd(stats, 1);  // fallback counter (diagnostics)
             }
-            if (go_exact) {
+            if (go_exact && fast) {
+                if (tid < kSrBins) unc[tid] = 0;
+                __syncthreads();
+                if (bad) unc[order[tid]] = unc[order[tid + 1]] = 1;
+                __syncthreads();
+                sr_exact_subset(data, L, kp, ball, ball_offsets, Rs + 9 * f, Rc + kRcPerFrame * f, unc, w, xb, xv,
+                                wmask);
+                if (tid < kSrBins) myrank = stable_rank(w, kSrBins, tid);
+                __syncthreads();
+            } else if (go_exact) {
                 sr_exact_frame(data, L, kp, ball, ball_offsets, Rs + 9 * f, w, xb, xv);
                 if (tid < kSrBins) myrank = stable_rank(w, kSrBins, tid);
                 __syncthreads();

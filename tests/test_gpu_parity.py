@@ -592,3 +592,24 @@ def test_dump_pyramid_round_trip(tmp_path):
     assert paths[0].endswith("oct0_lvl0_sigma%.4g.f32" % g.octaves[0].sigmas[0])
     back = vk.load_volume(paths[-1])
     assert np.array_equal(back.data, g.octaves[-1].levels[-1].data)
+
+
+def test_uncertain_bin_repair_on_brain_batch():
+    """configs[0]-style volumes hit near-tied SIFT-Rank bins (a few frames per
+    volume): the uncertain-bin repair (sr_exact_subset) must give the same
+    ranks as the full reference-order accumulation of every frame."""
+    dims = (145, 174, 145)
+    host = synthetic.batch_from(synthetic.brain_volume(), 2, seed=3)
+    outs, fallbacks = [], 0
+    for exact in (False, True):
+        ex = vk.Extractor(dims, PipelineConfig(), batch=2, exact_only=exact)
+        for i, v in enumerate(host):
+            ex.input[i].copy_(vk.volume.to_device(v))
+        ex.enqueue()
+        outs.append(ex.results())
+        if not exact:
+            fallbacks = ex.counts()["siftrank_fallbacks"]
+    a, b = outs
+    assert fallbacks > 0
+    assert len(a["desc"]) == len(b["desc"]) > 5000
+    assert np.array_equal(a["desc"], b["desc"])
