@@ -28,8 +28,11 @@ struct OriShared {
     double w[VK_MAX_DIRS];
     int order[VK_MAX_DIRS];
     uint8_t ok[VK_MAX_DIRS * VK_MAX_DIRS];
+    int unc[VK_MAX_DIRS];
+    unsigned wmask[kOriThreads / 32];
     int n_inside;
     int exact;
+    int repair;
 };
 
 // Nearest direction: first index of the maximum fp64 dot (np.argmax).
@@ -371,32 +374,89 @@ VK_D void sort_desc(const double* w, int K, int* order) {
 }
 
 // Are all decisions of frames_from() the same for every weight vector within
-// +-eps of w?  (adjacent-order separation + threshold margins)
-// Only the top of the order matters: primaries are the first max_frames bins
-// above the threshold and each secondary is the first usable bin of the
-// order, so positions 0..m (m = max_frames + 2) and the gap below them decide
-// every frame.
-VK_D bool frames_certain(const double* w, const int* order, int K, double epsrel, double epsabs, double ratio,
-                         int max_frames) {
+// +-eps of w?  Only the top of the order matters: primaries are the first
+// max_frames bins above the threshold and each secondary is the first usable
+// bin of the order, so positions 0..m (m = max_frames + 2) and the gap below
+// them decide every frame.  Marks the bins whose exact value could change a
+// decision: both members of every unseparated adjacent pair among those
+// positions, and a bin with an undecided threshold test together with the top
+// bin (the threshold is ratio x top).  Returns whether any bin was marked.
+VK_D bool frames_mark_uncertain(const double* w, const int* order, int K, double epsrel, double epsabs, double ratio,
+                                int max_frames, int* unc) {
     auto lo = [&](double v) { return v == 0.0 ? 0.0 : dsub(v, v * epsrel + epsabs); };
     auto hi = [&](double v) { return v == 0.0 ? 0.0 : dadd(v, v * epsrel + epsabs); };
+    bool any = false;
     const int m = min(K - 1, max_frames + 2);
     for (int r = 0; r < m; ++r) {
         const double a = w[order[r]], b = w[order[r + 1]];
-        if (b == 0.0) continue;  // exact zero (no votes) ties are order-independent
-        if (!(lo(a) > hi(b))) return false;
+        if (b == 0.0) continue;
+        if (!(lo(a) > hi(b))) {
+            unc[order[r]] = unc[order[r + 1]] = 1;
+            any = true;
+        }
     }
     const double top = w[order[0]];
-    if (!(top > 0.0)) return true;
+    if (!(top > 0.0)) return any;
     const double thr_lo = dmul(ratio, lo(top));
     const double thr_hi = dmul(ratio, hi(top));
     for (int r = 0; r <= m; ++r) {
         const double v = w[order[r]];
-        const bool yes = lo(v) >= thr_hi;
-        const bool no = hi(v) < thr_lo;
-        if (!yes && !no) return false;
+        if (!(lo(v) >= thr_hi) && !(hi(v) < thr_lo)) {
+            unc[order[r]] = unc[order[0]] = 1;
+            any = true;
+        }
     }
-    return true;
+    return any;
+}
+
+// Reference-order re-accumulation of the uncertain bins only (see
+// sr_exact_subset in vk_describe.cu): exact fast binning, the reference's
+// fp64 vote |g| x window for voxels of an uncertain bin, ordered sums by one
+// thread over ballot-compacted entries.  Certified bins keep their fast sums.
+__device__ __noinline__ void ori_exact_subset(const float* data, const vk_level& L, const vk_kp& kp,
+                                              const vk_ball& ball, const int* __restrict__ ball_offsets,
+                                              const double* __restrict__ win, const double* dirs, const IcoSh* icp,
+                                              const uint8_t* lut, int K, OriShared& sh) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid < K && sh.unc[tid]) sh.w[tid] = 0.0;
+    for (int base = 0; base < ball.count; base += kOriThreads) {
+        const int j = base + tid;
+        int bin = -1;
+        double v = 0.0;
+        if (j < ball.count) {
+            const int p = __ldg(ball_offsets + ball.start + j);
+            const int ox = unpack_off(p, 0), oy = unpack_off(p, 1), oz = unpack_off(p, 2);
+            const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
+            if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
+                const Nb6 nb = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
+                float gx, gy, gz;
+                grad32(nb, gx, gy, gz);
+                if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {
+                    double x64, y64, z64;
+                    grad64(nb, x64, y64, z64);
+                    const int b = icp ? nearest_dir_ico(dirs, *icp, lut, gx, gy, gz, nb) : nearest_dir(dirs, K, x64, y64, z64);
+                    if (sh.unc[b]) {
+                        v = dmul(norm3_numpy(x64, y64, z64), __ldg(win + (ox * ox + oy * oy + oz * oz)));
+                        bin = b;
+                    }
+                }
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, bin >= 0);
+        if (lane == 0) sh.wmask[wid] = m;
+        sh.xb[tid] = bin;
+        sh.xv[tid] = v;
+        __syncthreads();
+        if (tid == 0) {
+            for (int g = 0; g < kOriThreads / 32; ++g)
+                for (unsigned t = sh.wmask[g]; t; t &= t - 1) {
+                    const int q = 32 * g + __ffs(t) - 1;
+                    sh.w[sh.xb[q]] = dadd(sh.w[sh.xb[q]], sh.xv[q]);
+                }
+        }
+        __syncthreads();
+    }
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(kOriThreads, 4)
@@ -438,7 +498,7 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         const double* win = windows + ball.window_start;
         const float* win32 = windows32 + ball.window_start;
         zero_hist(hist, K);
-        if (tid == 0) { sh.n_inside = 0; sh.exact = exact_only; }
+        if (tid == 0) { sh.n_inside = 0; sh.exact = exact_only; sh.repair = 0; }
         __syncthreads();
         int inside_cnt = 0;
         const vk_gradlevel GL = grads ? grads[kp.lvl] : vk_gradlevel{};
@@ -494,17 +554,23 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
             for (int b = tid; b < K; b += kOriThreads) sh.w[b] = read_hist(hist, b);
             __syncthreads();
             sort_desc(sh.w, K, sh.order);
+            for (int b = tid; b < K; b += kOriThreads) sh.unc[b] = 0;
             __syncthreads();
             if (tid == 0) {
                 // fp32 votes (kVoteRel) summed in fp64 in some order vs the reference's
                 const double epsrel = 2.0 * (kVoteRel + gamma_k((double)sh.n_inside + 64.0));
                 const double epsabs = kVoteAbs * sh.n_inside;
-                if (!frames_certain(sh.w, sh.order, K, epsrel, epsabs, ratio, max_frames)) {
-                    sh.exact = 1;
+                if (frames_mark_uncertain(sh.w, sh.order, K, epsrel, epsabs, ratio, max_frames, sh.unc)) {
+                    sh.repair = 1;
                     atomicAdd(status + 1, 1);  // fallback counter (diagnostics)
                 }
             }
             __syncthreads();
+            if (sh.repair) {
+                ori_exact_subset(data, L, kp, ball, ball_offsets, win, sh.dirs, icp, lutp, K, sh);
+                sort_desc(sh.w, K, sh.order);
+                __syncthreads();
+            }
         }
         if (sh.exact) {
             // Exact reference order: all threads compute a chunk of exact votes,

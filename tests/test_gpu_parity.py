@@ -596,20 +596,22 @@ def test_dump_pyramid_round_trip(tmp_path):
 
 def test_uncertain_bin_repair_on_brain_batch():
     """configs[0]-style volumes hit near-tied SIFT-Rank bins (a few frames per
-    volume): the uncertain-bin repair (sr_exact_subset) must give the same
-    ranks as the full reference-order accumulation of every frame."""
+    volume) and near-tied orientation decisions (rarer): the uncertain-bin
+    repairs (sr_exact_subset, ori_exact_subset) must give the same frames and
+    ranks as the full reference-order accumulation of every keypoint."""
     dims = (145, 174, 145)
-    host = synthetic.batch_from(synthetic.brain_volume(), 2, seed=3)
-    outs, fallbacks = [], 0
+    host = synthetic.batch_from(synthetic.brain_volume(), 4, seed=3)
+    outs, fallbacks = [], {}
     for exact in (False, True):
-        ex = vk.Extractor(dims, PipelineConfig(), batch=2, exact_only=exact)
+        ex = vk.Extractor(dims, PipelineConfig(), batch=4, exact_only=exact)
         for i, v in enumerate(host):
             ex.input[i].copy_(vk.volume.to_device(v))
         ex.enqueue()
         outs.append(ex.results())
         if not exact:
-            fallbacks = ex.counts()["siftrank_fallbacks"]
+            fallbacks = ex.counts()
     a, b = outs
-    assert fallbacks > 0
-    assert len(a["desc"]) == len(b["desc"]) > 5000
+    assert fallbacks["siftrank_fallbacks"] > 0 and fallbacks["orient_fallbacks"] > 0, fallbacks
+    assert np.array_equal(a["frame_prim"], b["frame_prim"]) and np.array_equal(a["frame_sec"], b["frame_sec"])
+    assert len(a["desc"]) == len(b["desc"]) > 10000
     assert np.array_equal(a["desc"], b["desc"])
