@@ -20,6 +20,9 @@
 namespace vk {
 
 constexpr int kOriThreads = 256;
+#ifndef VK_ORI_PREFETCH
+#define VK_ORI_PREFETCH 0  // z-plane lead of an L1 prefetch in the ball walk (0: none)
+#endif
 
 struct OriShared {
     double xv[kOriThreads];
@@ -282,6 +285,9 @@ VK_D int ori_walk(const vk_kp& kp, const vk_level& L, const float* data, const v
             const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
             if (INTERIOR || (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz)) {
                 ++inside_cnt;
+#if VK_ORI_PREFETCH
+                prefetch_plane_ahead(data, L.nx, L.ny, L.nz, x, y, z, VK_ORI_PREFETCH);
+#endif
                 const Nb6 nb = INTERIOR ? load_nb6_interior(data, (unsigned)L.nx, plane,
                                                             ((unsigned)z * (unsigned)L.ny + (unsigned)y) *
                                                                     (unsigned)L.nx + (unsigned)x)

@@ -25,6 +25,7 @@ namespace vk {
 
 struct Taps {
     float w[VK_MAX_TAPS];
+    float mz;  // -0.0f, a launch-time value (see prod2)
 };
 
 constexpr int kTX = 32;       // output tile width in x
@@ -53,13 +54,31 @@ struct BlurGeom {
     static constexpr int SMEM = (2 * IN_F2 * 2 + 2 * ROWS * XS + ROWS) * 4;
 };
 
-// Two taps' products with one packed FMUL2 (two IEEE-rounded products); sums
-// stay scalar FADDs in tap order.  ptxas contracts FMUL2 + FADD2 into FFMA2
-// even with --fmad=false (verified in SASS), so packed adds are not used.
-VK_D float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+// Two taps' products with one packed op and two running sums with one packed
+// FADD2, each lane rounded exactly like the scalar fmul / fadd sequence.
+// ptxas contracts a packed multiply feeding a packed add into FFMA2 even with
+// --fmad=false and explicit .rn (scripts/micro: PTX mul.rn.f32x2 +
+// add.rn.f32x2 -> SASS FFMA2), which would drop the product's rounding.  The
+// product is therefore formed as FFMA2(w, v, mz) with mz = -0.0 passed at
+// launch: w*v + (-0) rounds to exactly round(w*v) (also for +-0 products), and
+// an FMA result feeding an add cannot be contracted further.
+#ifndef VK_PACKED_SUMS
+#define VK_PACKED_SUMS 0  // measured: no gain on B200 (the blur is FP-pipe bound, not issue bound)
+#endif
+VK_D float2 prod2(const Taps& taps, float w, float2 v) {
+#if VK_PACKED_SUMS
+    return __ffma2_rn(make_float2(w, w), v, make_float2(taps.mz, taps.mz));
+#else
+    return __fmul2_rn(make_float2(w, w), v);
+#endif
+}
 VK_D void acc2(float2& a, float2 p) {
+#if VK_PACKED_SUMS
+    a = __fadd2_rn(a, p);
+#else
     a.x = fadd(a.x, p.x);
     a.y = fadd(a.y, p.y);
+#endif
 }
 
 // One arriving y-blurred plane (z') in the z-pass.  The accumulator ring holds
@@ -76,7 +95,7 @@ VK_D void z_arrive(float2 (&r0)[2 * R + 1], float2 (&r1)[2 * R + 1], float2 v0, 
 #pragma unroll
     for (int d = 0; d <= R; ++d) {
         const float w = taps.w[R + d];
-        const float2 p0 = fmul2(make_float2(w, w), v0), p1 = fmul2(make_float2(w, w), v1);
+        const float2 p0 = prod2(taps, w, v0), p1 = prod2(taps, w, v1);
         if (d == 0) {
             acc2(r0[C], p0);
             acc2(r1[C], p1);
@@ -118,7 +137,7 @@ VK_D float2 z_arrive1(float2 (&r0)[2 * R + 1], float2 v0, const Taps& taps) {
 #pragma unroll
     for (int d = 0; d <= R; ++d) {
         const float w = taps.w[R + d];
-        const float2 p0 = fmul2(make_float2(w, w), v0);
+        const float2 p0 = prod2(taps, w, v0);
         if (d == 0) {
             acc2(r0[C], p0);
         } else {
@@ -269,7 +288,7 @@ blur3d_stream_kernel(const float* __restrict__ src, float* __restrict__ dst, flo
                     if (t < 0 || t > 2 * R) continue;
                     const int dd = t < R ? R - t : t - R;
                     const float w = taps.w[R + dd];
-                    const float2 p = fmul2(make_float2(w, w), v);
+                    const float2 p = prod2(taps, w, v);
                     if (t == 0) acc[k] = p;
                     else acc2(acc[k], p);
                 }
@@ -290,7 +309,7 @@ blur3d_stream_kernel(const float* __restrict__ src, float* __restrict__ dst, flo
                 if (i <= 2 * R) {
                     const int dd = i < R ? R - i : i - R;
                     const float w = taps.w[R + dd];
-                    const float2 p = fmul2(make_float2(w, w), v);
+                    const float2 p = prod2(taps, w, v);
                     if (i == 0) v0 = p;
                     else acc2(v0, p);
                 }
@@ -298,7 +317,7 @@ blur3d_stream_kernel(const float* __restrict__ src, float* __restrict__ dst, flo
                     const int t = i - 1;
                     const int dd = t < R ? R - t : t - R;
                     const float w = taps.w[R + dd];
-                    const float2 p = fmul2(make_float2(w, w), v);
+                    const float2 p = prod2(taps, w, v);
                     if (t == 0) v1 = p;
                     else acc2(v1, p);
                 }
@@ -438,7 +457,7 @@ blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, i
                 if (t < 0 || t > 2 * R) continue;
                 const int dd = t < R ? R - t : t - R;
                 const float w = taps.w[R + dd];
-                const float2 pr = fmul2(make_float2(w, w), v);
+                const float2 pr = prod2(taps, w, v);
                 if (t == 0) acc[k] = pr;
                 else acc2(acc[k], pr);
             }
@@ -465,7 +484,7 @@ blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, i
             if (t < 0 || t > 2 * R) continue;
             const int dd = t < R ? R - t : t - R;
             const float w = taps.w[R + dd];
-            const float2 pr = fmul2(make_float2(w, w), v);
+            const float2 pr = prod2(taps, w, v);
             if (t == 0) o[k] = pr;
             else acc2(o[k], pr);
         }
@@ -901,6 +920,7 @@ extern "C" int vk_blur3d_ws(const float* src, float* dst, float* dog_out, float*
     if (nb == 0) return VK_OK;
     Taps taps{};
     for (int i = 0; i < 2 * radius + 1; ++i) taps.w[i] = taps_host[i];
+    taps.mz = -0.0f;
     cudaStream_t st = as_stream(stream);
     if (half_out && (nx < 2 || ny < 2 || nz < 2)) half_out = nullptr;
     // Both kernels share each product between the two taps at the same
