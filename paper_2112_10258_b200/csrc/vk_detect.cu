@@ -124,6 +124,16 @@ detect_band0_rb_kernel(DogPtrs dogs, int nlev, int nx, int ny, int nz, int seg_b
     const bool xout = lane >= 1 && lane <= 30 && x <= nx - 2;
     int* cnt = counts + b;
     unsigned long long* kb = keys + (long long)b * cap;
+    // this lane's two adjacent-level neighbours (o = lane, lane + 32 of the 54,
+    // level-major then z, y, x like detect.py:65-76) as pointer offsets
+    auto nb_ptr = [&](int o) {
+        const int r = o % 27;
+        return dogs.p[o < 27 ? lev - 1 : lev + 1] + (long long)b * vol + (long long)(r / 9 - 1) * plane +
+               (long long)((r / 3) % 3 - 1) * nx + (r % 3 - 1);
+    };
+    const float* nb1 = nb_ptr(lane);
+    const bool has2 = lane + 32 < 54;
+    const float* nb2 = nb_ptr(has2 ? lane + 32 : lane);
 
     // per-plane stats for the kDetRows outputs: M9/m9 (3x3 incl. centre), M8/m8 (8-neighbourhood), c
     auto stats = [&](const float (&r)[kDetRows + 2], float (&M9)[kDetRows], float (&m9)[kDetRows],
@@ -170,27 +180,32 @@ detect_band0_rb_kernel(DogPtrs dogs, int nlev, int nx, int ny, int nz, int seg_b
         if (z + 2 <= z_hi + 1) load(rn, z + 2);
 #pragma unroll
         for (int k = 0; k < kDetRows; ++k) {
-            const int y = y0 + k;
-            bool hit = false, valley = false;
+            const int y = y0 + k;  // warp-uniform
+            bool pk = false, vl = false;
             if (xout && y <= ny - 2 && fabsf(cc[k]) >= cmin) {
-                const bool pk = cc[k] > fmaxf(fmaxf(Mp[k], Mc[k]), Mn9[k]);
-                const bool vl = cc[k] < fminf(fminf(mp[k], mc[k]), mn9[k]);
-                if (pk || vl) {
-                    // confirm against the 54 neighbours of the adjacent DoG levels
-                    const float* lo = dogs.p[lev - 1] + (long long)b * vol + (long long)z * plane + (long long)y * nx + x;
-                    const float* hi = dogs.p[lev + 1] + (long long)b * vol + (long long)z * plane + (long long)y * nx + x;
-                    bool ok = true;
-#pragma unroll 1
-                    for (int o = 0; o < 54 && ok; ++o) {
-                        const int l = o / 27, r = o % 27;
-                        const float n = __ldg((l == 0 ? lo : hi) + (long long)(r / 9 - 1) * plane +
-                                              (long long)((r / 3) % 3 - 1) * nx + (r % 3 - 1));
-                        ok = pk ? (cc[k] > n) : (cc[k] < n);
-                    }
-                    hit = ok;
-                    valley = vl;
-                }
+                pk = cc[k] > fmaxf(fmaxf(Mp[k], Mc[k]), Mn9[k]);
+                vl = cc[k] < fminf(fminf(mp[k], mc[k]), mn9[k]);
             }
+            // Confirm every surviving candidate against its 54 neighbours in the
+            // adjacent DoG levels with the whole warp (lane l checks neighbours l
+            // and l + 32): no divergent per-lane loops.
+            bool hit = false;
+            const long long cpos = (long long)z * plane + (long long)y * nx;
+            for (unsigned cm = __ballot_sync(0xffffffffu, pk || vl); cm; cm &= cm - 1) {
+                const int src = __ffs(cm) - 1;
+                const float cv = __shfl_sync(0xffffffffu, cc[k], src);
+                const bool cpk = __shfl_sync(0xffffffffu, pk, src);
+                const long long at = cpos + (blockIdx.x * 30 + src);
+                const float n1 = __ldg(nb1 + at);
+                bool ok = cpk ? (cv > n1) : (cv < n1);
+                if (has2) {
+                    const float n2 = __ldg(nb2 + at);
+                    ok = ok && (cpk ? (cv > n2) : (cv < n2));
+                }
+                const bool all = __all_sync(0xffffffffu, ok);
+                if (lane == src) hit = all;
+            }
+            const bool valley = vl;
             const unsigned mask = __ballot_sync(0xffffffffu, hit);
             if (mask) {
                 const int leader = __ffs(mask) - 1;
