@@ -103,7 +103,10 @@ detect_kernel(DogPtrs dogs, int nlev, int nx, int ny, int nz, int seg_base, int 
 // one plane ahead), the x neighbours come from the adjacent lanes (shuffles),
 // so the 3x3 in-plane max / min costs ~1.6 loads per voxel instead of 9.
 // Same prefilter + exact 54-neighbour confirmation as detect_band0_kernel.
-constexpr int kDetRows = 2;  // output rows per thread
+#ifndef VK_DET_ROWS
+#define VK_DET_ROWS 2
+#endif
+constexpr int kDetRows = VK_DET_ROWS;  // output rows per thread
 __global__ void __launch_bounds__(128)
 detect_band0_rb_kernel(DogPtrs dogs, int nlev, int nx, int ny, int nz, int seg_base, float cmin,
                        unsigned long long* __restrict__ keys, int* __restrict__ counts, int cap, int tz, int nzc) {
