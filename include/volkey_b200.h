@@ -56,11 +56,11 @@ typedef struct vk_level {
  * g4[v] = (gx, gy, gz, |g|) in fp32 (|g| from fp64), bin[v] = nearest of the
  * 42 icosphere directions (exact np.argmax semantics) or 255 for g == 0. */
 typedef struct vk_gradlevel {
-    const void* g4;
+    const void* g4;       /* kind 0: float4 (gx, gy, gz, |g|); kind 1: float |g| (vk_orient_field) */
     const uint8_t* bin;
     long long vol_stride;
     int nx, ny, nz;
-    int pad_;
+    int kind;             /* 0: gradient volume (orientation + SIFT-Rank), 1: orientation field */
 } vk_gradlevel;
 
 /* One keypoint (device record). */
@@ -221,6 +221,13 @@ int vk_frames_from_weights(const double* weights, int n, int K, const uint8_t* p
 /* Dense gradient volume of a batched level for the orientation / SIFT-Rank
  * fast paths (volume.py:244-264 gradients, orient.py:305 nearest direction
  * with the default icosphere; ico_host as in vk_orient). */
+/* Orientation field of a batched level (nb x nz x ny x nx, x fastest): mag[v]
+ * = fp32 |g| of the fp32 central-difference gradient (the orientation fast
+ * path's vote before the window), bin[v] = exact nearest of the 42 icosphere
+ * directions (np.argmax semantics) or 255 for g == 0.  ico_lut nullable.
+ * vk_orient walks it when the level's vk_gradlevel has kind 1. */
+int vk_orient_field(const float* level, float* mag, uint8_t* bin, int nb, int nx, int ny, int nz, const double* dirs,
+                    const int* ico_host, const uint8_t* ico_lut, void* stream);
 int vk_gradient_volume(const float* level, void* g4, uint8_t* bin, int nb, int nx, int ny, int nz,
                        const double* dirs, const int* ico_host, void* stream);
 

@@ -52,6 +52,7 @@ SIGNATURES = {
     "vk_gradient_volume": [P, P, P, I, I, I, I, P, P, P],
     "vk_describe_patch": [I, P, P, P, I, P, P, P, P, I, P, P, I, P, I, P, P, P],
     "vk_extract_patches": [P, P, P, I, P, P, P, P, I, P, P, I, P, P],
+    "vk_orient_field": [P, P, P, I, I, I, I, P, P, P, P],
     "vk_match": [I, P, I, P, I, I, D, P, P, P, P, P],
     "vk_match_excluding": [I, P, I, P, I, I, D, I, I, P, P, P, P, P],
     "vk_set_match_path": [I],
@@ -69,7 +70,7 @@ LEVEL_DTYPE = np.dtype([("base", "<u8"), ("vol_stride", "<i8"), ("nx", "<i4"), (
 KP_DTYPE = np.dtype([(n, "<i4") for n in ("vol", "lvl", "ix", "iy", "iz", "ball", "octave", "level")])
 BALL_DTYPE = np.dtype([(n, "<i4") for n in ("start", "count", "window_start", "max_d2", "zstart", "pstart", "r", "pad")])
 GRADLEVEL_DTYPE = np.dtype([("g4", "<u8"), ("bin", "<u8"), ("vol_stride", "<i8"), ("nx", "<i4"), ("ny", "<i4"),
-                            ("nz", "<i4"), ("pad", "<i4")])
+                            ("nz", "<i4"), ("kind", "<i4")])
 FRAME_DTYPE = np.dtype([(n, "<i4") for n in ("kp", "prim", "sec", "pad")])
 
 _lock = threading.Lock()

@@ -448,7 +448,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
             const float4* g4 = nullptr;
             if (grads) {
                 const vk_gradlevel GL = grads[kp.lvl];
-                if (GL.g4) g4 = reinterpret_cast<const float4*>(GL.g4) + (long long)kp.vol * GL.vol_stride;
+                if (GL.g4 && GL.kind == 0) g4 = reinterpret_cast<const float4*>(GL.g4) + (long long)kp.vol * GL.vol_stride;
             }
             if (ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz))
                 cnt = sr_walk_frames<true>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);

@@ -343,6 +343,109 @@ gradient_volume_kernel(const float* __restrict__ level, float4* __restrict__ g4,
     }
 }
 
+// Orientation field of a batched level: per voxel the fp32 magnitude of the
+// fp32 gradient (norm3_f32: the fast path's vote before the window) and the
+// exact nearest icosphere direction (255 for g == 0).  Keypoint-independent,
+// so the ball walks of all keypoints on this level gather 5 bytes per visit
+// instead of recomputing a 6-neighbour gradient and an argmax.
+constexpr int kFieldPlanes = 16;  // z planes per CTA of orient_field_kernel
+
+__global__ void __launch_bounds__(256)
+orient_field_kernel(const float* __restrict__ level, float* __restrict__ mag, uint8_t* __restrict__ bins, int nx,
+                    int ny, int nz, int nzc, const double* __restrict__ dirs_g, IcoT ico,
+                    const uint8_t* __restrict__ ico_lut) {
+    __shared__ double dirs[42 * 3];
+    __shared__ IcoSh ic;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int i = tid; i < 42 * 3; i += 256) dirs[i] = dirs_g[i];
+    if (tid < 72) {
+        const int v = tid / 6, c = tid % 6;
+        const int k = c == 0 ? ico.vert[v] : ico.adj[v][c - 1];
+        ic.ci[tid] = k;
+        ic.cd[tid] = make_float4((float)dirs_g[3 * k], (float)dirs_g[3 * k + 1], (float)dirs_g[3 * k + 2], 0.f);
+        ic.fk[tid] = c == 0 ? ico.vert[v] : ico.kind[v][c - 1];
+    }
+    __syncthreads();
+    // block = 32 x-columns x 8 rows x kFieldPlanes planes (blockIdx.z = volume * nzc + z chunk);
+    // the lookup table is read through L1 (16 KB, hot)
+    const int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 8 + threadIdx.y;
+    if (x >= nx || y >= ny) return;
+    const int b = blockIdx.z / nzc, z0 = (blockIdx.z - b * nzc) * kFieldPlanes;
+    const long long vol = (long long)nx * ny * nz;
+    const float* lv = level + b * vol;
+    const int z1 = min(nz, z0 + kFieldPlanes);
+    for (int z = z0; z < z1; ++z) {
+        const long long i = b * vol + ((long long)z * ny + y) * nx + x;
+        const Nb6 n = load_nb6(lv, nx, ny, nz, x, y, z);
+        float gx, gy, gz;
+        grad32(n, gx, gy, gz);
+        float m = 0.f;
+        int bin = 255;
+        if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {
+            m = norm3_f32(gx, gy, gz);
+            bin = nearest_dir_ico(dirs, ic, ico_lut, gx, gy, gz, n);
+        }
+        mag[i] = m;
+        bins[i] = (uint8_t)bin;
+    }
+}
+
+// Ball walk over an orientation field: U voxels per thread per step with all
+// their gathers in flight, packed offsets of the next step prefetched.
+// INTERIOR: ball inside the volume (no bounds tests).  Votes are the fast
+// path's fp32 |g| x window, bit for bit.
+template <bool INTERIOR>
+VK_D int field_walk(const vk_kp& kp, const vk_level& L, const float* __restrict__ mag,
+                    const uint8_t* __restrict__ bins, const vk_ball& ball, const int* __restrict__ ball_offsets,
+                    const float* __restrict__ win32, double* hist) {
+    constexpr int U = 4;
+    const int tid = threadIdx.x;
+    const int* offs = ball_offsets + ball.zstart;
+    const int nx = L.nx, plane = L.nx * L.ny;
+    const int kc = (kp.iz * L.ny + kp.iy) * nx + kp.ix;
+    hist = vote_copy(hist);
+    int cnt = 0;
+    int pn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int j = u * kOriThreads + tid;
+        pn[u] = j < ball.count ? __ldg(offs + j) : 0;
+    }
+    for (int base = 0; base < ball.count; base += U * kOriThreads) {
+        int idx[U], d2[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = base + u * kOriThreads + tid;
+            const int p = pn[u];
+            const int jn = j + U * kOriThreads;
+            pn[u] = jn < ball.count ? __ldg(offs + jn) : 0;
+            const int ox = unpack_off(p, 0), oy = unpack_off(p, 1), oz = unpack_off(p, 2);
+            ok[u] = j < ball.count;
+            if (!INTERIOR) {
+                const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
+                ok[u] = ok[u] && x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz;
+            }
+            idx[u] = ok[u] ? kc + oz * plane + oy * nx + ox : kc;
+            d2[u] = ok[u] ? ox * ox + oy * oy + oz * oz : 0;
+        }
+        int b[U];
+        float m[U], w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            b[u] = ok[u] ? (int)__ldg(bins + idx[u]) : 255;
+            m[u] = __ldg(mag + idx[u]);
+            w[u] = __ldg(win32 + d2[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            cnt += ok[u];
+            red_vote(hist, b[u] == 255 ? -1 : b[u], fmul(m[u], w[u]));
+        }
+    }
+    return cnt;
+}
+
 // Frames from a weight vector whose comparisons are exact (dominant_orientations).
 // order[] must hold the bins sorted by (-w, index).
 VK_D int frames_from(const double* w, const int* order, int K, const uint8_t* ok, double ratio, int max_frames,
@@ -508,7 +611,13 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         __syncthreads();
         int inside_cnt = 0;
         const vk_gradlevel GL = grads ? grads[kp.lvl] : vk_gradlevel{};
-        if (!exact_only && GL.bin != nullptr) {
+        if (!exact_only && GL.bin != nullptr && GL.kind == 1) {
+            const float* fm = reinterpret_cast<const float*>(GL.g4) + (long long)kp.vol * GL.vol_stride;
+            const uint8_t* fb = GL.bin + (long long)kp.vol * GL.vol_stride;
+            inside_cnt = ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz)
+                             ? field_walk<true>(kp, L, fm, fb, ball, ball_offsets, win32, hist)
+                             : field_walk<false>(kp, L, fm, fb, ball, ball_offsets, win32, hist);
+        } else if (!exact_only && GL.bin != nullptr) {
             // precomputed gradient volume: one coalesced (bin, |g|) pair per visit
             const uint8_t* bl = GL.bin + (long long)kp.vol * GL.vol_stride;
             const float4* gl = reinterpret_cast<const float4*>(GL.g4) + (long long)kp.vol * GL.vol_stride;
@@ -799,6 +908,29 @@ extern "C" int vk_expand_frames(const int* nframes, const int* prim, const int* 
         count_launch();
     }
     return cuda_status(cudaGetLastError(), "expand launch");
+}
+
+extern "C" int vk_orient_field(const float* level, float* mag, uint8_t* bin, int nb, int nx, int ny, int nz,
+                               const double* dirs, const int* ico_host, const uint8_t* ico_lut, void* stream) {
+    if (!level || !mag || !bin || nb < 0 || nx < 1 || ny < 1 || nz < 1 || !dirs || !ico_host) {
+        set_error("vk_orient_field: bad arguments");
+        return VK_ERR_PARAMETER;
+    }
+    const long long total = (long long)nb * nx * ny * nz;
+    if (total == 0) return VK_OK;
+    IcoT ico{};
+    ico.valid = 1;
+    for (int v = 0; v < 12; ++v) {
+        ico.vert[v] = ico_host[v];
+        for (int m = 0; m < 5; ++m) ico.adj[v][m] = ico_host[12 + 5 * v + m];
+        for (int m = 0; m < 5; ++m) ico.kind[v][m] = ico_host[72 + 5 * v + m];
+    }
+    const int nzc = (nz + kFieldPlanes - 1) / kFieldPlanes;
+    const dim3 grid((nx + 31) / 32, (ny + 7) / 8, (unsigned)(nb * nzc));
+    orient_field_kernel<<<grid, dim3(32, 8), 0, as_stream(stream)>>>(level, mag, bin, nx, ny, nz, nzc, dirs, ico,
+                                                                      ico_lut);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "orient field launch");
 }
 
 extern "C" int vk_gradient_volume(const float* level, void* g4, uint8_t* bin, int nb, int nx, int ny, int nz,

@@ -615,3 +615,21 @@ def test_uncertain_bin_repair_on_brain_batch():
     assert np.array_equal(a["frame_prim"], b["frame_prim"]) and np.array_equal(a["frame_sec"], b["frame_sec"])
     assert len(a["desc"]) == len(b["desc"]) > 10000
     assert np.array_equal(a["desc"], b["desc"])
+
+
+def test_orientation_field_walk_equals_gradient_walk():
+    """The orientation field (vk_orient_field: per-voxel fast |g| + exact
+    nearest direction, walked by every keypoint) gives the same frames and
+    descriptors as recomputing gradients in each ball walk."""
+    dims = (145, 174, 145)
+    host = synthetic.batch_from(synthetic.brain_volume(), 2, seed=9)
+    outs = []
+    for field in (True, False):  # field walk (opt-in) vs the default fused walk
+        ex = vk.Extractor(dims, PipelineConfig(), batch=2, orient_field=field)
+        for i, v in enumerate(host):
+            ex.input[i].copy_(vk.volume.to_device(v))
+        ex.enqueue()
+        outs.append(ex.results())
+    a, b = outs
+    assert np.array_equal(a["frame_prim"], b["frame_prim"]) and np.array_equal(a["frame_sec"], b["frame_sec"])
+    assert np.array_equal(a["desc"], b["desc"]) and len(a["desc"]) > 5000
