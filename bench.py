@@ -44,8 +44,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=32, help="volumes per GPU per step")
-    ap.add_argument("--streams", type=int, default=4, help="parallel sub-batches (streams) per GPU")
+    ap.add_argument("--batch", type=int, default=64, help="volumes per GPU per step")
+    ap.add_argument("--streams", type=int, default=8, help="parallel sub-batches (streams) per GPU")
     ap.add_argument("--slots", type=int, default=2, help="distinct input batches cycled over steps")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--descriptor", default="siftrank", choices=("siftrank", "brief", "rrief"))
