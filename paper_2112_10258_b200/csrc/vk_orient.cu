@@ -490,32 +490,70 @@ VK_D void sort_desc(const double* w, int K, int* order) {
 // decision: both members of every unseparated adjacent pair among those
 // positions, and a bin with an undecided threshold test together with the top
 // bin (the threshold is ratio x top).  Returns whether any bin was marked.
-VK_D bool frames_mark_uncertain(const double* w, const int* order, int K, double epsrel, double epsabs, double ratio,
-                                int max_frames, int* unc) {
+// With one warp: lane r tests the adjacent pair (r, r + 1) and the threshold
+// decision at position r (m <= VK_MAX_FRAMES + 2 < 32); returns the warp-wide
+// any.
+VK_D bool warp_mark_uncertain(const double* w, const int* order, int K, double epsrel, double epsabs, double ratio,
+                              int max_frames, int* unc) {
+    const int lane = threadIdx.x & 31;
     auto lo = [&](double v) { return v == 0.0 ? 0.0 : dsub(v, v * epsrel + epsabs); };
     auto hi = [&](double v) { return v == 0.0 ? 0.0 : dadd(v, v * epsrel + epsabs); };
     bool any = false;
     const int m = min(K - 1, max_frames + 2);
-    for (int r = 0; r < m; ++r) {
-        const double a = w[order[r]], b = w[order[r + 1]];
-        if (b == 0.0) continue;
-        if (!(lo(a) > hi(b))) {
-            unc[order[r]] = unc[order[r + 1]] = 1;
+    if (lane < m) {
+        const double a = w[order[lane]], b = w[order[lane + 1]];
+        if (b != 0.0 && !(lo(a) > hi(b))) {
+            unc[order[lane]] = unc[order[lane + 1]] = 1;
             any = true;
         }
     }
     const double top = w[order[0]];
-    if (!(top > 0.0)) return any;
-    const double thr_lo = dmul(ratio, lo(top));
-    const double thr_hi = dmul(ratio, hi(top));
-    for (int r = 0; r <= m; ++r) {
-        const double v = w[order[r]];
+    if (top > 0.0 && lane <= m) {
+        const double thr_lo = dmul(ratio, lo(top));
+        const double thr_hi = dmul(ratio, hi(top));
+        const double v = w[order[lane]];
         if (!(lo(v) >= thr_hi) && !(hi(v) < thr_lo)) {
-            unc[order[r]] = unc[order[0]] = 1;
+            unc[order[lane]] = unc[order[0]] = 1;
             any = true;
         }
     }
-    return any;
+    return __any_sync(0xffffffffu, any);
+}
+
+// frames_from with one warp (orient.py:310-350 semantics): primaries are the
+// positions of the (-w, index) order whose weight reaches ratio x top, at most
+// max_frames of them counted whether or not a secondary exists; each
+// secondary is the first bin of the order != primary with pair_ok, found with
+// a ballot over the order.  Writes nframes[0], prim[0..], sec[0..].
+VK_D void warp_frames_from(const double* w, const int* order, int K, const uint8_t* ok, double ratio, int max_frames,
+                           int* nframes, int* prim, int* sec) {
+    const int lane = threadIdx.x & 31;
+    int nf = 0;
+    const double top = w[order[0]];
+    if (top > 0.0) {
+        const double thr = dmul(ratio, top);
+        const unsigned q0 = __ballot_sync(0xffffffffu, lane < K && w[order[lane]] >= thr);
+        const unsigned q1 = __ballot_sync(0xffffffffu, lane + 32 < K && w[order[lane + 32]] >= thr);
+        int taken = 0;
+        for (int h = 0; h < 2; ++h) {
+            for (unsigned qm = h ? q1 : q0; qm && taken < max_frames; qm &= qm - 1) {
+                const int p = order[32 * h + __ffs(qm) - 1];
+                ++taken;
+                const int oa = order[lane], ob = lane + 32 < K ? order[lane + 32] : p;
+                const unsigned m0 = __ballot_sync(0xffffffffu, lane < K && oa != p && ok[p * K + oa]);
+                const unsigned m1 = __ballot_sync(0xffffffffu, ob != p && ok[p * K + ob]);
+                const int q2 = m0 ? __ffs(m0) - 1 : (m1 ? 32 + __ffs(m1) - 1 : -1);
+                if (q2 >= 0) {
+                    if (lane == 0) {
+                        prim[nf] = p;
+                        sec[nf] = order[q2];
+                    }
+                    ++nf;
+                }
+            }
+        }
+    }
+    if (lane == 0) *nframes = nf;
 }
 
 // Reference-order re-accumulation of the uncertain bins only (see
@@ -671,11 +709,11 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
             sort_desc(sh.w, K, sh.order);
             for (int b = tid; b < K; b += kOriThreads) sh.unc[b] = 0;
             __syncthreads();
-            if (tid == 0) {
+            if (tid < 32) {
                 // fp32 votes (kVoteRel) summed in fp64 in some order vs the reference's
                 const double epsrel = 2.0 * (kVoteRel + gamma_k((double)sh.n_inside + 64.0));
                 const double epsabs = kVoteAbs * sh.n_inside;
-                if (frames_mark_uncertain(sh.w, sh.order, K, epsrel, epsabs, ratio, max_frames, sh.unc)) {
+                if (warp_mark_uncertain(sh.w, sh.order, K, epsrel, epsabs, ratio, max_frames, sh.unc) && tid == 0) {
                     sh.repair = 1;
                     atomicAdd(status + 1, 1);  // fallback counter (diagnostics)
                 }
@@ -724,15 +762,8 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         }
         if (weights)
             for (int b = tid; b < K; b += kOriThreads) weights[(long long)item * K + b] = sh.w[b];
-        if (tid == 0) {
-            int pr[VK_MAX_FRAMES], se[VK_MAX_FRAMES];
-            const int nf = frames_from(sh.w, sh.order, K, sh.ok, ratio, max_frames, pr, se);
-            nframes[item] = nf;
-            for (int f = 0; f < nf; ++f) {
-                prim[item * max_frames + f] = pr[f];
-                sec[item * max_frames + f] = se[f];
-            }
-        }
+        if (tid < 32) warp_frames_from(sh.w, sh.order, K, sh.ok, ratio, max_frames, nframes + item,
+                                       prim + (long long)item * max_frames, sec + (long long)item * max_frames);
         __syncthreads();
     }
 }
