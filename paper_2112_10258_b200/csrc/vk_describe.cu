@@ -408,13 +408,15 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                 const vk_gradlevel* __restrict__ grads, double* __restrict__ work) {
     double* hist = work + (long long)blockIdx.x * kAccumSlot;  // [F][64] fp64, L2-resident
     __shared__ double w[kSrBins];
-    __shared__ int order[kSrBins];
     __shared__ double Rs[VK_MAX_FRAMES * 9];
     __shared__ float4 Rc[VK_MAX_FRAMES * kRcPerFrame];
     __shared__ int xb[kSrThreads];
     __shared__ double xv[kSrThreads];
     __shared__ int n_inside;
     __shared__ int unc[kSrBins];
+    __shared__ double w4[kSrThreads / kSrBins][kSrBins];
+    __shared__ int order4[kSrThreads / kSrBins][kSrBins];
+    __shared__ int badf[4];
     __shared__ unsigned wmask[kSrThreads / 32];
     const int tid = threadIdx.x;
     const int n = n_items_dev ? min(*n_items_dev, n_items_max) : n_items_max;
@@ -463,52 +465,65 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
         }
         if (cnt) atomicAdd(&n_inside, cnt);
         __syncthreads();
-        for (int f = 0; f < F; ++f) {
-            if (fast && tid < kSrBins) {
-                w[tid] = read_hist(hist, f * kSrBins + tid);
-            }
-            __syncthreads();
-            int myrank = 0;
-            if (tid < kSrBins) {
-                myrank = stable_rank(w, kSrBins, tid);
-                order[myrank] = tid;
-            }
-            __syncthreads();
-            int go_exact = 1, bad = 0;
-            if (fast) {
+        if (fast) {
+            // all frames of the item at once, up to 4 per pass: thread (f, b) = (tid / 64, tid % 64)
+            const double epsrel = 2.0 * (kVoteRel + gamma_k((double)n_inside + 64.0));
+            const double epsabs = kVoteAbs * n_inside;
+            const int fl = tid >> 6, b = tid & (kSrBins - 1);
+            for (int f0 = 0; f0 < F; f0 += kSrThreads / kSrBins) {
+                const int f = f0 + fl;
+                const bool mine = f < F;
+                if (mine) w4[fl][b] = read_hist(hist, f * kSrBins + b);
+                if (tid < 4) badf[tid] = 0;
+                __syncthreads();
+                int myrank = 0;
+                if (mine) {
+                    myrank = stable_rank(w4[fl], kSrBins, b);
+                    order4[fl][myrank] = b;
+                }
+                __syncthreads();
                 // every adjacent pair of the sorted bins must be separated by more than
                 // the bound between our summation and the reference's sequential one
-                const double epsrel = 2.0 * (kVoteRel + gamma_k((double)n_inside + 64.0));
-                const double epsabs = kVoteAbs * n_inside;
-                if (tid + 1 < kSrBins) {
-                    const double a = w[order[tid]], b = w[order[tid + 1]];
-                    if (!(a == 0.0 && b == 0.0)) {  // exact empty-bin ties are order-independent
-                        const double ahi = a == 0.0 ? 0.0 : dadd(a, a * epsrel + epsabs);
-                        const double blo = dsub(b, b * epsrel + epsabs);
-                        bad = !(ahi < blo);
+                int bad = 0;
+                if (mine && b + 1 < kSrBins) {
+                    const double x = w4[fl][order4[fl][b]], y = w4[fl][order4[fl][b + 1]];
+                    if (!(x == 0.0 && y == 0.0)) {  // exact empty-bin ties are order-independent
+                        const double xhi = x == 0.0 ? 0.0 : dadd(x, x * epsrel + epsabs);
+                        const double ylo = dsub(y, y * epsrel + epsabs);
+                        bad = !(xhi < ylo);
                     }
                 }
-                go_exact = __syncthreads_or(bad);
 #ifdef VK_EXP_NO_FALLBACK
-                go_exact = 0;  // timing experiment only: wrong ranks on near ties
+                bad = 0;  // timing experiment only: wrong ranks on near ties
 #endif
-                if (go_exact && tid == 0 && stats) atomicAdd(stats, 1);  // fallback counter (diagnostics)
+                if (bad) badf[fl] = 1;
+                if (__syncthreads_or(bad)) {
+                    // rare: repair the uncertain frames one at a time (whole CTA)
+                    for (int g = 0; g < 4 && f0 + g < F; ++g) {
+                        if (!badf[g]) continue;
+                        if (tid == 0 && stats) atomicAdd(stats, 1);  // fallback counter (diagnostics)
+                        if (tid < kSrBins) {
+                            unc[tid] = 0;
+                            w[tid] = w4[g][tid];
+                        }
+                        __syncthreads();
+                        if (fl == g && bad) unc[order4[g][b]] = unc[order4[g][b + 1]] = 1;
+                        __syncthreads();
+                        sr_exact_subset(data, L, kp, ball, ball_offsets, Rs + 9 * (f0 + g), Rc + kRcPerFrame * (f0 + g),
+                                        unc, w, xb, xv, wmask);
+                        if (fl == g) myrank = stable_rank(w, kSrBins, b);
+                        __syncthreads();
+                    }
+                }
+                if (mine) out[(long long)(first + f) * kSrBins + b] = (uint8_t)myrank;
+                __syncthreads();
             }
-            if (go_exact && fast) {
-                if (tid < kSrBins) unc[tid] = 0;
-                __syncthreads();
-                if (bad) unc[order[tid]] = unc[order[tid + 1]] = 1;
-                __syncthreads();
-                sr_exact_subset(data, L, kp, ball, ball_offsets, Rs + 9 * f, Rc + kRcPerFrame * f, unc, w, xb, xv,
-                                wmask);
-                if (tid < kSrBins) myrank = stable_rank(w, kSrBins, tid);
-                __syncthreads();
-            } else if (go_exact) {
+        } else {
+            for (int f = 0; f < F; ++f) {
                 sr_exact_frame(data, L, kp, ball, ball_offsets, Rs + 9 * f, w, xb, xv);
-                if (tid < kSrBins) myrank = stable_rank(w, kSrBins, tid);
+                if (tid < kSrBins) out[(long long)(first + f) * kSrBins + tid] = (uint8_t)stable_rank(w, kSrBins, tid);
                 __syncthreads();
             }
-            if (tid < kSrBins) out[(long long)(first + f) * kSrBins + tid] = (uint8_t)myrank;
         }
     }
 }
