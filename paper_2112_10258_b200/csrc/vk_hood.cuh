@@ -30,7 +30,10 @@ constexpr int kCopyStride = VK_MAX_FRAMES * 64;
 // Histogram slots per CTA in the accumulation workspace.
 constexpr int kAccumSlot = kCopyStride * kVoteCopies;
 // Persistent grids launch at most this many CTAs per SM.
-constexpr int kAccumCtasPerSm = 4;
+#ifndef VK_ACCUM_CTAS_PER_SM
+#define VK_ACCUM_CTAS_PER_SM 4
+#endif
+constexpr int kAccumCtasPerSm = VK_ACCUM_CTAS_PER_SM;
 
 // Grid of a persistent accumulation kernel: every CTA resident at once (the
 // occupancy the kernel's registers allow, at most kAccumCtasPerSm per SM), so

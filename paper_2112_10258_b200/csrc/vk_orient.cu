@@ -606,7 +606,10 @@ __device__ __noinline__ void ori_exact_subset(const float* data, const vk_level&
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kOriThreads, 4)
+#ifndef VK_ORI_MIN_BLOCKS
+#define VK_ORI_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kOriThreads, VK_ORI_MIN_BLOCKS)
 orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, int n_kp_max,
               const vk_level* __restrict__ levels, const vk_ball* __restrict__ balls,
               const int* __restrict__ ball_offsets, const double* __restrict__ windows,
