@@ -122,14 +122,29 @@ constexpr int kRcPerFrame = 6;  // float4 slots per frame
 #ifndef VK_SR_PACKED
 #define VK_SR_PACKED 1
 #endif
+#ifndef VK_SR_ZERO_RULE
+#define VK_SR_ZERO_RULE 0  // measured slower (extra per-frame work outweighs the avoided fallbacks)
+#endif
 
-VK_D void lds_col(const float4* p, float2& xx, float2& yy, float2& zz) {
+VK_D void lds_col(const float4* p, float2& xx, float2& yy, float2& zz, int& zmask) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(p);
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(xx.x), "=f"(xx.y), "=f"(yy.x), "=f"(yy.y)
                  : "r"(a));
+#if VK_SR_ZERO_RULE
+    float zm, pad;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(zz.x), "=f"(zz.y), "=f"(zm), "=f"(pad)
+                 : "r"(a + 16u));
+    zmask = __float_as_int(zm);
+#else
     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(zz.x), "=f"(zz.y) : "r"(a + 16u));
+    zmask = 0;
+#endif
 }
+
+// Bits k of the components that are exactly nonzero.
+VK_D int nonzero_bits(float a, float b, float c) { return (a != 0.f) | ((b != 0.f) << 1) | ((c != 0.f) << 2); }
 
 VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const double* R, const float4* Rc,
                      const float* data, int nx, int ny, int nz, int x, int y, int z) {
@@ -139,10 +154,17 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
     const float2 vx = make_float2(fx, gx), vy = make_float2(fy, gy), vz = make_float2(fz, gz);
     int sp = 0, og = 0;
     bool osure = true, gsure = true;
+#if VK_SR_ZERO_RULE
+    // exact-zero rule: when every nonzero component of the offset (gradient)
+    // meets an exactly-zero fp64 entry of column j, both our chain and the
+    // reference's give +-0, i.e. bit 0, whatever the bound test says
+    const int nzo = nonzero_bits(fx, fy, fz), nzg = nonzero_bits(gx, gy, gz);
+#endif
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
         float2 cxx, cyy, czz;
-        lds_col(Rc + 2 * j, cxx, cyy, czz);
+        int zmask;
+        lds_col(Rc + 2 * j, cxx, cyy, czz, zmask);
 #if VK_SR_PACKED
         const float2 t = __ffma2_rn(vz, czz, __ffma2_rn(vy, cyy, __fmul2_rn(vx, cxx)));  // (r_j, g_j)
 #else
@@ -151,8 +173,13 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
 #endif
         sp |= (int)(t.x > 0.f) << j;
         og |= (int)(t.y > 0.f) << j;
+#if VK_SR_ZERO_RULE
+        osure = osure && (fabsf(t.x) > eo || (nzo & ~zmask) == 0);
+        gsure = gsure && (fabsf(t.y) > eg || (nzg & ~zmask) == 0);
+#else
         osure = osure && fabsf(t.x) > eo;
         gsure = gsure && fabsf(t.y) > eg;
+#endif
     }
     if (!osure) sp = sr_obits_exact(ox, oy, oz, R);
     if (!gsure) og = sr_gbits_exact(data, nx, ny, nz, x, y, z, R);
@@ -453,8 +480,9 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
             const double* R = Rs + 9 * (i / 3);
             const int j = i % 3;
             const float cx = (float)R[j], cy = (float)R[3 + j], cz = (float)R[6 + j];
+            const int zmask = (R[j] == 0.0) | ((R[3 + j] == 0.0) << 1) | ((R[6 + j] == 0.0) << 2);  // exact fp64 zeros
             Rc[(i / 3) * kRcPerFrame + 2 * j] = make_float4(cx, cx, cy, cy);
-            Rc[(i / 3) * kRcPerFrame + 2 * j + 1] = make_float4(cz, cz, 0.f, 0.f);
+            Rc[(i / 3) * kRcPerFrame + 2 * j + 1] = make_float4(cz, cz, __int_as_float(zmask), 0.f);
         }
         zero_hist(hist, F * kSrBins);
         if (tid == 0) n_inside = 0;
