@@ -103,6 +103,19 @@ detect_kernel(DogPtrs dogs, int nlev, int nx, int ny, int nz, int seg_base, int 
 // one plane ahead), the x neighbours come from the adjacent lanes (shuffles),
 // so the 3x3 in-plane max / min costs ~1.6 loads per voxel instead of 9.
 // Same prefilter + exact 54-neighbour confirmation as detect_band0_kernel.
+// Three-input float max / min (FMNMX3 on sm_100a): exact, NaN operands ignored
+// like fmaxf / fminf chains.
+VK_D float max3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+VK_D float min3f(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 #ifndef VK_DET_ROWS
 #define VK_DET_ROWS 2
 #endif
@@ -146,14 +159,14 @@ detect_band0_rb_kernel(DogPtrs dogs, int nlev, int nx, int ny, int nz, int seg_b
         for (int i = 0; i < kDetRows + 2; ++i) {
             L[i] = __shfl_up_sync(0xffffffffu, r[i], 1);
             Rr[i] = __shfl_down_sync(0xffffffffu, r[i], 1);
-            hM[i] = fmaxf(fmaxf(L[i], r[i]), Rr[i]);
-            hm[i] = fminf(fminf(L[i], r[i]), Rr[i]);
+            hM[i] = max3f(L[i], r[i], Rr[i]);
+            hm[i] = min3f(L[i], r[i], Rr[i]);
         }
 #pragma unroll
         for (int k = 0; k < kDetRows; ++k) {
             const float a = fmaxf(hM[k], hM[k + 2]), am = fminf(hm[k], hm[k + 2]);
-            M8[k] = fmaxf(a, fmaxf(L[k + 1], Rr[k + 1]));
-            m8[k] = fminf(am, fminf(L[k + 1], Rr[k + 1]));
+            M8[k] = max3f(a, L[k + 1], Rr[k + 1]);
+            m8[k] = min3f(am, L[k + 1], Rr[k + 1]);
             M9[k] = fmaxf(a, hM[k + 1]);
             m9[k] = fminf(am, hm[k + 1]);
             c[k] = r[k + 1];
@@ -186,8 +199,8 @@ detect_band0_rb_kernel(DogPtrs dogs, int nlev, int nx, int ny, int nz, int seg_b
             const int y = y0 + k;  // warp-uniform
             bool pk = false, vl = false;
             if (xout && y <= ny - 2 && fabsf(cc[k]) >= cmin) {
-                pk = cc[k] > fmaxf(fmaxf(Mp[k], Mc[k]), Mn9[k]);
-                vl = cc[k] < fminf(fminf(mp[k], mc[k]), mn9[k]);
+                pk = cc[k] > max3f(Mp[k], Mc[k], Mn9[k]);
+                vl = cc[k] < min3f(mp[k], mc[k], mn9[k]);
             }
             // Confirm every surviving candidate against its 54 neighbours in the
             // adjacent DoG levels with the whole warp (lane l checks neighbours l
