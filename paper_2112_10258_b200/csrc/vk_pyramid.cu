@@ -817,7 +817,8 @@ static int launch_ring(const float* src, float* dst, float* dog, float* half, in
 }
 
 // Split path: (x, y) kernel into `work` (nb * volume floats), then the z kernel.
-static int kZWaves = 4, kZMinChunkR = 4;  // z chunking (tuned on B200; env-overridable for sweeps)
+static int kZWaves = 1, kZMinChunkR = 12;  // z chunking: long chunks measured best in the multi-stream bench -- the 2R warm-up
+                                          // arrivals per chunk cost more than the lost parallelism (env-overridable)
 template <int R, int TY>
 static int launch_xy(const float* src, float* work, int nb, int nx, int ny, int nz, const Taps& taps, cudaStream_t st) {
     using G = XyGeom<R, TY>;
