@@ -279,6 +279,15 @@ def run_ours(a):
         for k, (e0, e1) in zip(stage_ms, zip(ev[:-1], ev[1:])):
             stage_ms[k].append(e0.elapsed_time(e1))
     stage_ms = {k: statistics.median(v) for k, v in stage_ms.items()}
+    # ball-voxel visits of the timed sub-batch (orientation / SIFT-Rank work units)
+    r0 = exs[0].results()
+    bcount = exs[0].tables.balls.cpu().numpy().view(_lib.BALL_DTYPE)["count"].astype(np.int64)
+    kp_visits = bcount[r0["kp"]["ball"]]
+    frames_per_kp = np.bincount(r0["frame_kp"], minlength=len(kp_visits))
+    walk = {"orient_visits": int(kp_visits.sum()), "siftrank_visit_frames": int((kp_visits * frames_per_kp).sum()),
+            "note": "ball voxels per keypoint (incl. the few outside the volume) on the timed sub-batch"}
+    walk["orient_visits_per_s"] = round(walk["orient_visits"] / (stage_ms["orient"] / 1e3))
+    walk["siftrank_visit_frames_per_s"] = round(walk["siftrank_visit_frames"] / (stage_ms["describe"] / 1e3))
     # ---- graphs
     use_graph = not a.no_graph
     if use_graph:
@@ -408,6 +417,7 @@ def run_ours(a):
         "roofline": roofline,
         "stages_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
         "detect_gbs": round(det_gbs, 1),
+        "walks": walk,
         "keypoints_per_volume": counts["keypoints"] / B, "frames_per_volume": counts["frames"] / B,
         "roofline_note": "pyramid stage measured eagerly on one sub-batch of stage_timing_subbatch volumes",
         "gpu_launches": int(launches_per_step * a.steps),
