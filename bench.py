@@ -20,6 +20,7 @@ travel to the GPU box), one full volume per process, all cores concurrently.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -253,6 +254,23 @@ def run_ours(a):
     torch.cuda.synchronize()
     exs = [grp.members[0] for grp in groups]
     counts = {k: sum(m.counts()[k] for m in groups[0].members) for k in ("keypoints", "frames")}
+    # ---- cross-rank parity: every rank extracts the same fixed
+    # 2-volume batch; the digests of keypoints + descriptors must agree, so
+    # each GPU's outputs equal the single-GPU ones (which the tests pin to the oracle)
+    chk = Extractor(DIMS, cfg, batch=2)
+    chk.input.copy_(torch.from_numpy(np.ascontiguousarray(
+        synthetic.batch_from(base, 2, seed=7).transpose(0, 3, 2, 1))).cuda())
+    chk.enqueue()
+    rc = chk.results()
+    digest = hashlib.sha256(b"".join(np.ascontiguousarray(rc[k]).tobytes()
+                                     for k in ("pos", "sigma", "frame_prim", "frame_sec", "desc"))).hexdigest()
+    digests = [digest]
+    if world > 1:
+        digests = [None] * world
+        dist.all_gather_object(digests, digest)
+    rank_parity = {"checked_volumes": 2, "keypoints": int(rc["n_keypoints"]), "digest": digest[:16],
+                   "ranks": world, "all_ranks_equal": len(set(digests)) == 1}
+    del chk, rc
     launches0 = _lib.load().vk_launch_count()
     groups[0].enqueue()
     torch.cuda.synchronize()
@@ -418,6 +436,7 @@ def run_ours(a):
         "stages_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
         "detect_gbs": round(det_gbs, 1),
         "walks": walk,
+        "rank_parity": rank_parity,
         "keypoints_per_volume": counts["keypoints"] / B, "frames_per_volume": counts["frames"] / B,
         "roofline_note": "pyramid stage measured eagerly on one sub-batch of stage_timing_subbatch volumes",
         "gpu_launches": int(launches_per_step * a.steps),
