@@ -122,6 +122,9 @@ constexpr int kRcPerFrame = 6;  // float4 slots per frame
 #ifndef VK_SR_PACKED
 #define VK_SR_PACKED 1
 #endif
+#ifndef VK_SR_SIGNBITS
+#define VK_SR_SIGNBITS 1
+#endif
 #ifndef VK_SR_ZERO_RULE
 #define VK_SR_ZERO_RULE 0  // measured slower (extra per-frame work outweighs the avoided fallbacks)
 #endif
@@ -153,6 +156,7 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
     const float eg = 1.0e-6f * (fabsf(gx) + fabsf(gy) + fabsf(gz)) + 1.0e-40f;
     const float2 vx = make_float2(fx, gx), vy = make_float2(fy, gy), vz = make_float2(fz, gz);
     int sp = 0, og = 0;
+    unsigned sneg = 0u, gneg = 0u;
     bool osure = true, gsure = true;
 #if VK_SR_ZERO_RULE
     // exact-zero rule: when every nonzero component of the offset (gradient)
@@ -171,8 +175,14 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
         const float2 t = make_float2(fmaf(fz, czz.x, fmaf(fy, cyy.x, fx * cxx.x)),
                                      fmaf(gz, czz.x, fmaf(gy, cyy.x, gx * cxx.x)));
 #endif
+#if VK_SR_SIGNBITS
+        // bit j = (t > 0): wherever the bound test passes t != 0, so it is the inverted sign bit
+        sneg |= (__float_as_uint(t.x) >> 31) << j;
+        gneg |= (__float_as_uint(t.y) >> 31) << j;
+#else
         sp |= (int)(t.x > 0.f) << j;
         og |= (int)(t.y > 0.f) << j;
+#endif
 #if VK_SR_ZERO_RULE
         osure = osure && (fabsf(t.x) > eo || (nzo & ~zmask) == 0);
         gsure = gsure && (fabsf(t.y) > eg || (nzg & ~zmask) == 0);
@@ -181,6 +191,10 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
         gsure = gsure && fabsf(t.y) > eg;
 #endif
     }
+#if VK_SR_SIGNBITS
+    sp = (int)(~sneg & 7u);
+    og = (int)(~gneg & 7u);
+#endif
     if (!osure) sp = sr_obits_exact(ox, oy, oz, R);
     if (!gsure) og = sr_gbits_exact(data, nx, ny, nz, x, y, z, R);
     return 8 * sp + og;
