@@ -348,7 +348,12 @@ def run_ours(a):
         ev_in = [torch.cuda.Event() for _ in range(S)]
         ev_done = [torch.cuda.Event() for _ in range(S)]
 
+        diag = os.environ.get("VK_E2E_DIAG", "")  # diagnostics only: "no_h2d" / "no_rb" (not a bench value)
+
         def stage(slot):  # step data of `slot` -> that group's input buffers
+            if diag == "no_h2d":
+                ev_in[slot].record(copy)
+                return
             with torch.cuda.stream(copy):
                 copy.wait_event(ev_done[slot])
                 for g, m in enumerate(groups[slot].members):
@@ -361,6 +366,8 @@ def run_ours(a):
             # D2H on its own stream, ordered after that step only (not after the
             # step now running on the compute stream)
             nonlocal d2h_tot
+            if diag == "no_rb":
+                return
             with torch.cuda.stream(rb):
                 rb.wait_event(ev_done[slot])
                 for m in groups[slot].members:   # counts, then exactly the produced SoA to host
