@@ -551,9 +551,6 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                         bad = !(xhi < ylo);
                     }
                 }
-#ifdef VK_EXP_NO_FALLBACK
-                bad = 0;  // timing experiment only: wrong ranks on near ties
-#endif
                 if (bad) badf[fl] = 1;
                 if (__syncthreads_or(bad)) {
                     // rare: repair the uncertain frames one at a time (whole CTA)
