@@ -21,7 +21,10 @@
 
 namespace vk {
 
-constexpr int kSrThreads = 256;
+#ifndef VK_SR_THREADS
+#define VK_SR_THREADS 256
+#endif
+constexpr int kSrThreads = VK_SR_THREADS;
 constexpr int kPrefetchPlanes = 3;  // z-plane lead of the L1 prefetch in the ball walk
 constexpr int kSrBins = 64;
 constexpr int kPatchThreads = 256;
@@ -473,7 +476,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
     __shared__ int unc[kSrBins];
     __shared__ double w4[kSrThreads / kSrBins][kSrBins];
     __shared__ int order4[kSrThreads / kSrBins][kSrBins];
-    __shared__ int badf[4];
+    __shared__ int badf[kSrThreads / kSrBins];
     __shared__ unsigned wmask[kSrThreads / 32];
     const int tid = threadIdx.x;
     const int n = n_items_dev ? min(*n_items_dev, n_items_max) : n_items_max;
@@ -532,7 +535,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                 const int f = f0 + fl;
                 const bool mine = f < F;
                 if (mine) w4[fl][b] = read_hist(hist, f * kSrBins + b);
-                if (tid < 4) badf[tid] = 0;
+                if (tid < kSrThreads / kSrBins) badf[tid] = 0;
                 __syncthreads();
                 int myrank = 0;
                 if (mine) {
@@ -554,7 +557,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                 if (bad) badf[fl] = 1;
                 if (__syncthreads_or(bad)) {
                     // rare: repair the uncertain frames one at a time (whole CTA)
-                    for (int g = 0; g < 4 && f0 + g < F; ++g) {
+                    for (int g = 0; g < kSrThreads / kSrBins && f0 + g < F; ++g) {
                         if (!badf[g]) continue;
                         if (tid == 0 && stats) atomicAdd(stats, 1);  // fallback counter (diagnostics)
                         if (tid < kSrBins) {
