@@ -19,7 +19,10 @@
 
 namespace vk {
 
-constexpr int kOriThreads = 256;
+#ifndef VK_ORI_THREADS
+#define VK_ORI_THREADS 256
+#endif
+constexpr int kOriThreads = VK_ORI_THREADS;
 #ifndef VK_ORI_PREFETCH
 #define VK_ORI_PREFETCH 0  // z-plane lead of an L1 prefetch in the ball walk (0: none)
 #endif
