@@ -27,6 +27,8 @@ constexpr int kOriThreads = VK_ORI_THREADS;
 #define VK_ORI_PREFETCH 0  // z-plane lead of an L1 prefetch in the ball walk (0: none)
 #endif
 
+constexpr int kOriQueue = 64;  // per-warp deferred entries of the fast walk (flush at >= 32)
+
 struct OriShared {
     double xv[kOriThreads];
     int xb[kOriThreads];
@@ -36,6 +38,7 @@ struct OriShared {
     uint8_t ok[VK_MAX_DIRS * VK_MAX_DIRS];
     int unc[VK_MAX_DIRS];
     unsigned wmask[kOriThreads / 32];
+    int2 queue[kOriThreads / 32][kOriQueue];  // deferred boundary-cell voxels of the fast walk (ori_walk)
     int n_inside;
     int exact;
     int repair;
@@ -268,13 +271,30 @@ VK_D int ori_vote_fast(const Nb6& n, const float* __restrict__ win32, int d2, co
 // Fast z-major ball walk (consecutive lanes take consecutive x: coalesced
 // gathers); INTERIOR: ball and gradient stencil inside the volume.  Returns
 // this thread's count of in-volume voxels.
+//
+// With the lookup table, the ~3% of voxels whose canonical cell is crossed by
+// a Voronoi boundary are not resolved in place (their screened argmax would
+// run in more than half of all warp steps with a lane or two active): they go
+// to a per-warp queue of (voxel, vote) and are resolved 32 at a time with the
+// whole warp (neighbours reloaded, screened + exact argmax), then voted.
 template <bool INTERIOR>
 VK_D int ori_walk(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
                   const int* __restrict__ ball_offsets, const float* __restrict__ win32, const double* dirs,
-                  const IcoSh* icp, const uint8_t* lut, int K, double* hist) {
-    const int tid = threadIdx.x;
+                  const IcoSh* icp, const uint8_t* lut, int K, double* hist, int2* queue) {
+    const int tid = threadIdx.x, lane = tid & 31;
     const unsigned plane = (unsigned)L.nx * (unsigned)L.ny;
     hist = vote_copy(hist);
+    const bool defer = icp != nullptr && lut != nullptr;  // CTA-uniform
+    auto resolve = [&](int2 e) {
+        const unsigned c = (unsigned)e.x;
+        const int z = (int)(c / plane), rem = (int)(c - (unsigned)z * plane);
+        const int y = rem / L.nx, x = rem - y * L.nx;
+        const Nb6 nb = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
+        float gx, gy, gz;
+        grad32(nb, gx, gy, gz);
+        red_vote(hist, nearest_dir_ico(dirs, *icp, nullptr, gx, gy, gz, nb), __int_as_float(e.y));
+    };
+    int qn = 0;  // warp-uniform queue fill
     int inside_cnt = 0;
     int pn = tid < ball.count ? __ldg(ball_offsets + ball.zstart + tid) : 0;
     for (int base = 0; base < ball.count; base += kOriThreads) {
@@ -283,6 +303,8 @@ VK_D int ori_walk(const vk_kp& kp, const vk_level& L, const float* data, const v
         if (j + kOriThreads < ball.count) pn = __ldg(ball_offsets + ball.zstart + j + kOriThreads);
         int bin = -1;
         float vote = 0.f;
+        bool miss = false;
+        unsigned c = 0;
         if (j < ball.count) {
             const int ox = unpack_off(p, 0), oy = unpack_off(p, 1), oz = unpack_off(p, 2);
             const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
@@ -291,14 +313,41 @@ VK_D int ori_walk(const vk_kp& kp, const vk_level& L, const float* data, const v
 #if VK_ORI_PREFETCH
                 prefetch_plane_ahead(data, L.nx, L.ny, L.nz, x, y, z, VK_ORI_PREFETCH);
 #endif
-                const Nb6 nb = INTERIOR ? load_nb6_interior(data, (unsigned)L.nx, plane,
-                                                            ((unsigned)z * (unsigned)L.ny + (unsigned)y) *
-                                                                    (unsigned)L.nx + (unsigned)x)
+                c = ((unsigned)z * (unsigned)L.ny + (unsigned)y) * (unsigned)L.nx + (unsigned)x;
+                const Nb6 nb = INTERIOR ? load_nb6_interior(data, (unsigned)L.nx, plane, c)
                                         : load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
-                bin = ori_vote_fast(nb, win32, ox * ox + oy * oy + oz * oz, dirs, icp, lut, K, vote);
+                if (defer) {
+                    float gx, gy, gz;
+                    grad32(nb, gx, gy, gz);
+                    if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {
+                        vote = fmul(norm3_f32(gx, gy, gz), __ldg(win32 + (ox * ox + oy * oy + oz * oz)));
+                        bin = nearest_dir_lut(lut, gx, gy, gz, fabsf(gx), fabsf(gy), fabsf(gz));
+                        miss = bin < 0;
+                    }
+                } else {
+                    bin = ori_vote_fast(nb, win32, ox * ox + oy * oy + oz * oz, dirs, icp, lut, K, vote);
+                }
             }
         }
         red_vote(hist, bin, vote);
+        if (defer) {
+            const unsigned mm = __ballot_sync(0xffffffffu, miss);
+            if (mm) {
+                if (miss) queue[qn + __popc(mm & ((1u << lane) - 1u))] = make_int2((int)c, __float_as_int(vote));
+                qn += __popc(mm);
+                if (qn >= 32) {
+                    __syncwarp();
+                    resolve(queue[qn - 32 + lane]);
+                    qn -= 32;
+                    __syncwarp();
+                }
+            }
+        }
+    }
+    if (defer && qn > 0) {
+        __syncwarp();
+        if (lane < qn) resolve(queue[lane]);
+        __syncwarp();
     }
     return inside_cnt;
 }
@@ -689,8 +738,10 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
             }
         } else if (!exact_only) {
             inside_cnt = ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz)
-                             ? ori_walk<true>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, K, hist)
-                             : ori_walk<false>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, K, hist);
+                             ? ori_walk<true>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, K, hist,
+                                              sh.queue[tid >> 5])
+                             : ori_walk<false>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, K, hist,
+                                               sh.queue[tid >> 5]);
         } else {
             for (int j = tid; j < ball.count; j += kOriThreads) {
                 const int p = __ldg(ball_offsets + ball.start + j);
