@@ -203,6 +203,30 @@ VK_D int sr_bin_fast(int ox, int oy, int oz, float gx, float gy, float gz, const
     return 8 * sp + og;
 }
 
+// sr_bin_fast without the fallbacks: the fp32 bin and which halves are
+// certain (bit 0: offset octant, bit 1: gradient octant).
+VK_D int sr_bin_try(int ox, int oy, int oz, float gx, float gy, float gz, const float4* Rc, int& sure) {
+    const float fx = (float)ox, fy = (float)oy, fz = (float)oz;
+    const float eo = 1.0e-6f * (fabsf(fx) + fabsf(fy) + fabsf(fz));
+    const float eg = 1.0e-6f * (fabsf(gx) + fabsf(gy) + fabsf(gz)) + 1.0e-40f;
+    const float2 vx = make_float2(fx, gx), vy = make_float2(fy, gy), vz = make_float2(fz, gz);
+    unsigned sneg = 0u, gneg = 0u;
+    bool osure = true, gsure = true;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        float2 cxx, cyy, czz;
+        int zm;
+        lds_col(Rc + 2 * j, cxx, cyy, czz, zm);
+        const float2 t = __ffma2_rn(vz, czz, __ffma2_rn(vy, cyy, __fmul2_rn(vx, cxx)));  // (r_j, g_j)
+        sneg |= (__float_as_uint(t.x) >> 31) << j;
+        gneg |= (__float_as_uint(t.y) >> 31) << j;
+        osure = osure && fabsf(t.x) > eo;
+        gsure = gsure && fabsf(t.y) > eg;
+    }
+    sure = (int)osure | ((int)gsure << 1);
+    return 8 * (int)(~sneg & 7u) + (int)(~gneg & 7u);
+}
+
 // Fast walk of one keypoint's ball for NF frames; returns the number of
 // in-volume ball voxels seen by this thread.  INTERIOR: the whole ball and its
 // gradient stencil lie inside the volume (no bounds tests, no one-sided
@@ -266,9 +290,26 @@ VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const fl
 // Interior walk with the six neighbour loads of the thread's next voxel issued
 // before the current voxel's bins are computed (two voxels in flight per
 // thread): the walk is bound by L1 hit latency, not by issue.
+#ifndef VK_SR_DEFER
+#define VK_SR_DEFER 1
+#endif
+// A deferred (voxel, frame) vote: exact octant bits where the fp32 ones were
+// uncertain, then the vote.  e = (packed offset, f | fast bin << 2 | sure << 8, mag bits).
+VK_D void sr_resolve(int4 e, const vk_kp& kp, const vk_level& L, const float* data, const double* Rs,
+                     double* hist) {
+    const int ox = unpack_off(e.x, 0), oy = unpack_off(e.x, 1), oz = unpack_off(e.x, 2);
+    const int f = e.y & 3, bin = (e.y >> 2) & 63, sure = (e.y >> 8) & 3;
+    const int sp = (sure & 1) ? (bin >> 3) : sr_obits_exact(ox, oy, oz, Rs + 9 * f);
+    const int og = (sure & 2) ? (bin & 7) : sr_gbits_exact(data, L.nx, L.ny, L.nz, kp.ix + ox, kp.iy + oy, kp.iz + oz,
+                                                           Rs + 9 * f);
+    red_vote(hist + f * kSrBins, 8 * sp + og, __int_as_float(e.z));
+}
+constexpr int kSrQueue = 32 + 4 * 32;  // per-warp deferred (voxel, frame) entries: flush at >= 32, one step adds <= 128
+
 template <int NF>
 VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
-                      const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist, int F) {
+                      const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist, int F,
+                      int4* queue, int* qcount) {
     const int tid = threadIdx.x;
     const int step = blockDim.x;
     const int nx = L.nx, plane = L.nx * L.ny;
@@ -306,29 +347,63 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
 #pragma unroll
                 for (int f = 0; f < NF; ++f) {
                     if (f >= F) break;
+#if VK_SR_DEFER
+                    // uncertain octants (~1.5% of visit-frames) are deferred: resolved in place they
+                    // would stall the whole warp in ~40% of its steps
+                    int sure;
+                    const int bin = sr_bin_try(ox, oy, oz, gx, gy, gz, Rc + kRcPerFrame * f, sure);
+                    if (sure == 3) {
+                        red_vote(hist + f * kSrBins, bin, mag);
+                    } else {
+                        const int pos = atomicAdd(qcount, 1);
+                        queue[pos] = make_int4(pc, f | (bin << 2) | (sure << 8), __float_as_int(mag), 0);
+                    }
+#else
                     const int bin = sr_bin_fast(ox, oy, oz, gx, gy, gz, Rs + 9 * f, Rc + kRcPerFrame * f, data, L.nx,
                                                 L.ny, L.nz, kp.ix + ox, kp.iy + oy, kp.iz + oz);
                     red_vote(hist + f * kSrBins, bin, mag);
+#endif
                 }
             }
         }
+#if VK_SR_DEFER
+        __syncwarp();
+        int qn = *reinterpret_cast<volatile int*>(qcount);
+        if (qn >= 32) {
+            do {
+                sr_resolve(queue[qn - 32 + (tid & 31)], kp, L, data, Rs, hist);
+                qn -= 32;
+            } while (qn >= 32);
+            __syncwarp();
+            if ((tid & 31) == 0) *qcount = qn;
+            __syncwarp();
+        }
+#endif
     }
+#if VK_SR_DEFER
+    __syncwarp();
+    const int qn = *reinterpret_cast<volatile int*>(qcount);
+    if ((tid & 31) < qn) sr_resolve(queue[tid & 31], kp, L, data, Rs, hist);
+    __syncwarp();
+    if ((tid & 31) == 0) *qcount = 0;
+    __syncwarp();
+#endif
     return cnt;
 }
 
 template <bool INTERIOR>
 VK_D int sr_walk_frames(const vk_kp& kp, const vk_level& L, const float* data, const float4* g4, const vk_ball& ball,
                         const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist,
-                        int F) {
+                        int F, int4* queue, int* qcount) {
 #ifndef VK_SR_PIPE
 #define VK_SR_PIPE 1
 #endif
     if (VK_SR_PIPE && INTERIOR && !g4 && F <= 4) {
         switch (F) {
-            case 1: return sr_walk_pipe<1>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F);
-            case 2: return sr_walk_pipe<2>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F);
-            case 3: return sr_walk_pipe<3>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F);
-            default: return sr_walk_pipe<4>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F);
+            case 1: return sr_walk_pipe<1>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
+            case 2: return sr_walk_pipe<2>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
+            case 3: return sr_walk_pipe<3>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
+            default: return sr_walk_pipe<4>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
         }
     }
     switch (F) {
@@ -477,9 +552,12 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
     __shared__ double w4[kSrThreads / kSrBins][kSrBins];
     __shared__ int order4[kSrThreads / kSrBins][kSrBins];
     __shared__ int badf[kSrThreads / kSrBins];
+    __shared__ int4 sq[kSrThreads / 32][kSrQueue];  // deferred uncertain votes, per warp
+    __shared__ int sqn[kSrThreads / 32];
     __shared__ unsigned wmask[kSrThreads / 32];
     const int tid = threadIdx.x;
     const int n = n_items_dev ? min(*n_items_dev, n_items_max) : n_items_max;
+    if (tid < kSrThreads / 32) sqn[tid] = 0;  // (first use is after the item's __syncthreads)
     for (int item = blockIdx.x; item < n; item += gridDim.x) {
         const int F = min(item_count[item], max_f);
         if (F <= 0) continue;
@@ -514,9 +592,11 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                 if (GL.g4 && GL.kind == 0) g4 = reinterpret_cast<const float4*>(GL.g4) + (long long)kp.vol * GL.vol_stride;
             }
             if (ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz))
-                cnt = sr_walk_frames<true>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);
+                cnt = sr_walk_frames<true>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F, sq[tid >> 5],
+                                           sqn + (tid >> 5));
             else
-                cnt = sr_walk_frames<false>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);
+                cnt = sr_walk_frames<false>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F, sq[tid >> 5],
+                                            sqn + (tid >> 5));
         } else {
             for (int j = tid; j < ball.count; j += kSrThreads) {
                 const int p = __ldg(ball_offsets + ball.start + j);
