@@ -182,9 +182,22 @@ VK_D void grad32(const Nb6& n, float& gx, float& gy, float& gz) {
     gz = fmul(__fsub_rn(n.zh, n.zl), n.sz);
 }
 
-// |v| in fp32, within 4 u32 relative of the exact Euclidean norm.
+// |v| in fp32, within 4 u32 relative of the exact Euclidean norm: the sum of
+// squares carries <= 3.5 u32, halved by the square root, plus the hardware
+// sqrt.approx.f32 (MUFU.SQRT) error -- measured <= 1.67 x 2^-24 relative over
+// 1.3e9 random finite inputs incl. subnormals (scripts/micro/sqrt_approx_err.cu).
+#ifndef VK_APPROX_SQRT
+#define VK_APPROX_SQRT 1
+#endif
 VK_D float norm3_f32(float x, float y, float z) {
-    return __fsqrt_rn(fadd(fadd(fmul(x, x), fmul(y, y)), fmul(z, z)));
+    const float s = fadd(fadd(fmul(x, x), fmul(y, y)), fmul(z, z));
+#if VK_APPROX_SQRT
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(s));
+    return r;
+#else
+    return __fsqrt_rn(s);
+#endif
 }
 
 // Relative error bound of fp32 votes against the reference's fp64 votes
