@@ -12,9 +12,10 @@ process per GPU (torchrun), each rank its own volumes, no collective in the
 data path (weak scaling); timing is CUDA events on the pipeline stream, max
 over ranks.  Rank 0 prints one JSON line.
 
-``--impl reference`` times the reference algorithm on the host cores instead:
-the oracle restatement (oracle/volkey_oracle.py -- the Python reference cannot
-travel to the GPU box), one full volume per process, all cores concurrently.
+``--impl reference`` times the reference on the host cores instead: the
+unmodified volkey package staged into oracle/_ref by oracle/make_ref.py (it
+travels to the GPU box with the snapshot), one full volume per
+single-threaded process, all cores concurrently.
 """
 
 from __future__ import annotations
@@ -54,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-matching", action="store_true", help="skip the descriptor-matching side measurement")
+    ap.add_argument("--no-extras", action="store_true", help="skip the drop-in API latency and configs[3] lines")
     ap.add_argument("--ref-steps", type=int, default=2, help="cap on timed reference steps (each ~30 s)")
     return ap.parse_args()
 
@@ -162,42 +164,66 @@ def detect_bytes(plan) -> int:
     return sum((L - 1) * 4 * int(np.prod(d)) for d in plan.octave_dims)
 
 
-# ------------------------------------------------------------ CPU oracle
-def _oracle_worker(args):
-    seed, kind, barrier = args
+# ------------------------------------------------------------ CPU reference
+REF_DIR = os.path.join(REPO, "oracle", "_ref")  # staged by oracle/make_ref.py (unmodified reference copy)
+
+
+def ref_available() -> bool:
+    return os.path.isfile(os.path.join(REF_DIR, "volkey", "pipeline.py"))
+
+
+def _cpu_worker(args):
+    """One full volume through the CPU path in this (spawned) process:
+    impl "reference" = the unmodified volkey.extract_features (pipeline.py:70-102)
+    from oracle/_ref with PipelineConfig(workers=1); impl "port" = the numpy
+    restatement oracle/volkey_oracle.py."""
+    seed, kind, barrier, impl = args
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     import threadpoolctl
 
-    from oracle import volkey_oracle as O
     from paper_2112_10258_b200 import synthetic
 
     with threadpoolctl.threadpool_limits(1):
         base = synthetic.brain_volume()
         vol = synthetic.batch_from(base, 1, seed=seed)[0] if seed else base
-        O.extract(np.ones((24, 24, 24), np.float32) * np.arange(24, dtype=np.float32), descriptor=kind)  # warm
+        warm = np.ones((24, 24, 24), np.float32) * np.arange(24, dtype=np.float32)
+        if impl == "reference":
+            sys.path.insert(0, REF_DIR)
+            import volkey
+
+            cfg = volkey.PipelineConfig(descriptor=kind, workers=1)
+            run = lambda v: volkey.extract_features(volkey.Volume(v), cfg)  # noqa: E731
+            count = lambda r: (len(r.keypoints), len(r.records))  # noqa: E731
+        else:
+            from oracle import volkey_oracle as O
+
+            run = lambda v: O.extract(v, descriptor=kind)  # noqa: E731
+            count = lambda r: (len(r["keypoints"]), len(r["records"]))  # noqa: E731
+        run(warm)
         if barrier is not None:
             barrier.wait()
         t0 = time.time()
-        res = O.extract(vol, descriptor=kind)
+        res = run(vol)
         t1 = time.time()
-    return t0, t1, len(res["keypoints"]), len(res["records"])
+    nk, nr = count(res)
+    return t0, t1, nk, nr
 
 
-def cpu_oracle_volumes_per_s(kind: str, procs: int, steps: int):
-    """Reference algorithm on the host cores: `procs` concurrent processes,
-    one full volume each per step.  Returns (volumes/s, details)."""
+def cpu_volumes_per_s(kind: str, procs: int, steps: int, impl: str):
+    """CPU path on the host cores: `procs` concurrent single-threaded
+    processes, one full volume each per step.  Returns (volumes/s, details)."""
     import multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     times, kps = [], []
     for s in range(steps):
         if procs == 1:
-            r = [_oracle_worker((s, kind, None))]
+            r = [_cpu_worker((s, kind, None, impl))]
         else:
             with ctx.Manager() as mgr:
                 bar = mgr.Barrier(procs)
                 with ctx.Pool(procs) as pool:
-                    r = pool.map(_oracle_worker, [(s * procs + i, kind, bar) for i in range(procs)])
+                    r = pool.map(_cpu_worker, [(s * procs + i, kind, bar, impl) for i in range(procs)])
         start, end = min(x[0] for x in r), max(x[1] for x in r)
         times.append(end - start)
         kps += [x[2] for x in r]
@@ -453,14 +479,111 @@ def run_ours(a):
         out["e2e"] = e2e
     if not a.no_matching:
         out["matching"] = bench_matching()
+    if not a.no_extras:
+        out["dropin"] = bench_dropin()
+        out["configs3"] = bench_configs3()
     if world == 1 and not a.no_cpu_baseline:
-        vps, det = cpu_oracle_volumes_per_s(a.descriptor, 1, 1)
-        out["cpu_baseline"] = {"value": round(vps, 5), "unit": UNIT, "cores": 1, "kind": "port",
-                               "sample": "1 full 145x174x145 volume through oracle/volkey_oracle.py (numpy "
-                                         "restatement of the reference), 1 thread", "seconds": det["step_s"]}
+        impl = "reference" if ref_available() else "port"
+        vps, det = cpu_volumes_per_s(a.descriptor, 1, 1, impl)
+        src = ("the unmodified reference volkey.extract_features (oracle/_ref, staged by oracle/make_ref.py), "
+               "PipelineConfig(workers=1)" if impl == "reference" else
+               "oracle/volkey_oracle.py (numpy restatement; oracle/_ref not staged)")
+        out["cpu_baseline"] = {"value": round(vps, 5), "unit": UNIT, "cores": 1, "kind": impl,
+                               "sample": f"1 full 145x174x145 volume through {src}, 1 thread, OPENBLAS_NUM_THREADS=1",
+                               "seconds": det["step_s"]}
+        if impl == "reference" and os.environ.get("VK_BENCH_PORT", "1") != "0":
+            pv, pd = cpu_volumes_per_s(a.descriptor, 1, 1, "port")
+            out["cpu_baseline"]["port_note"] = {"value": round(pv, 5), "seconds": pd["step_s"],
+                                                "what": "the oracle restatement on the same volume (not the baseline)"}
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_dropin(reps: int = 5) -> dict:
+    """Per-call latency of the reference-facing drop-in API on a host numpy
+    volume: extract_features(Volume(ndarray)) (cached Extractor, H2D of the
+    volume, the whole pipeline, SoA read-back) plus materialising the
+    reference's Python objects (keypoints, oriented frames, descriptor
+    records), wall clock, median of `reps` calls after 2 warm-up calls."""
+    import paper_2112_10258_b200 as vk
+    from paper_2112_10258_b200 import synthetic
+
+    vol = vk.Volume(synthetic.brain_volume())
+    cfg = vk.PipelineConfig()
+
+    def call(materialise):
+        t0 = time.perf_counter()
+        r = vk.extract_features(vol, cfg)
+        t1 = time.perf_counter()
+        if materialise:
+            _ = (r.keypoints, r.oriented, r.records)
+        return t1 - t0, time.perf_counter() - t0, len(r.soa["desc"])
+
+    for _ in range(2):
+        call(True)
+    soa_only = [call(False)[0] for _ in range(reps)]
+    full = [call(True) for _ in range(reps)]
+    med_full = statistics.median(f[1] for f in full)
+    return {"api": "extract_features(Volume(numpy 145x174x145), PipelineConfig()) + .keypoints/.oriented/.records",
+            "ms_per_call": round(1e3 * med_full, 2), "volumes_per_s": round(1.0 / med_full, 2),
+            "ms_per_call_soa_only": round(1e3 * statistics.median(soa_only), 2),
+            "descriptors": full[0][2], "reps": reps, "timing": "host wall clock (perf_counter), median"}
+
+
+def bench_configs3(steps: int = 5) -> dict:
+    """configs[3]: 256^3 synthetic volumes, num_octaves=4,
+    detect + describe, as 4 parallel-stream sub-batches of 2 volumes in one
+    CUDA graph; device time with CUDA events; pyramid roofline on one
+    sub-batch."""
+    import torch
+
+    import paper_2112_10258_b200 as vk
+    from paper_2112_10258_b200 import _lib, synthetic
+    from paper_2112_10258_b200.engine import Extractor, ExtractorGroup
+
+    dims = (256, 256, 256)
+    cfg = vk.PipelineConfig(num_octaves=4)
+    base = synthetic.soup_volume(dims, np.random.default_rng(20240817), noise=0.01)
+    host = synthetic.batch_from(base, 8, seed=31)
+    dev = torch.stack([vk.volume.to_device(v) for v in host])
+    members = [Extractor(dims, cfg, batch=2, input=dev[2 * m: 2 * m + 2]) for m in range(4)]
+    for ex in members:
+        ex.enqueue()
+    torch.cuda.synchronize()
+    grp = ExtractorGroup(members)
+    grp.capture()
+    for _ in range(2):
+        grp.run()
+    st = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        grp.run()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    ex = members[0]
+    pt = []
+    for _ in range(3):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(st)
+        ex.enqueue_pyramid(st.cuda_stream)
+        a1.record(st)
+        torch.cuda.synchronize()
+        pt.append(a0.elapsed_time(a1))
+    with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+        peak = json.load(fh).get("hbm_gbs")
+    pb = pyramid_bytes(ex.plan) * ex.B
+    ach = pb / (statistics.median(pt) / 1e3) / 1e9
+    c = {k: sum(m.counts()[k] for m in members) for k in ("keypoints", "frames")}
+    return {"workload": "configs[3]: 8 x 256^3 volumes per step, num_octaves=4, detect + describe (siftrank)",
+            "volumes_per_s": round(8 / (ms / 1e3), 2), "ms_per_step": round(ms, 3),
+            "keypoints_per_volume": c["keypoints"] / 8, "frames_per_volume": c["frames"] / 8,
+            "pyramid_ms_per_subbatch_of_2": round(statistics.median(pt), 4),
+            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(ach / peak, 4) if peak else None, "algorithmic_bytes": pb}}
 
 
 def bench_matching() -> dict:
@@ -516,12 +639,18 @@ def bench_matching() -> dict:
 
 
 def run_reference(a):
+    """The reference arm: the unmodified volkey (oracle/_ref) on every host
+    core, one single-threaded process per core, one full volume each per step
+    (falls back to the oracle port, kind "port", if oracle/_ref is not staged)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     procs = os.cpu_count() or 1
     steps = max(1, min(a.steps, a.ref_steps))
-    vps, det = cpu_oracle_volumes_per_s(a.descriptor, procs, steps)
+    impl = "reference" if ref_available() else "port"
+    vps, det = cpu_volumes_per_s(a.descriptor, procs, steps, impl)
+    what = ("the unmodified reference volkey.extract_features(Volume, PipelineConfig(workers=1)) from oracle/_ref"
+            if impl == "reference" else "oracle/volkey_oracle.py (oracle/_ref not staged)")
     out = {
         "impl": "reference", "metric": METRIC, "value": round(vps, 5), "unit": UNIT, "n_gpus": world,
         "steps": steps, "steps_requested": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * statistics.mean(det["step_s"]),
@@ -529,9 +658,9 @@ def run_reference(a):
         "data": "synthetic (same phantom family as the GPU arm)",
         "config": {"workload": f"1 x 145x174x145 volume per process per step, {procs} processes, detect + describe "
                                f"({a.descriptor})", "volume": list(DIMS), "descriptor": a.descriptor},
-        "cpu_baseline": {"value": round(vps, 5), "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": f"{procs} concurrent single-threaded processes x {steps} step(s), one full volume "
-                                   "each, oracle/volkey_oracle.py (the Python reference cannot travel to the box)"},
+        "cpu_baseline": {"value": round(vps, 5), "unit": UNIT, "cores": procs, "kind": impl,
+                         "sample": f"{procs} concurrent single-threaded processes (OPENBLAS_NUM_THREADS=1) x {steps} "
+                                   f"step(s), one full volume each, {what}"},
         "e2e": {"value": round(vps, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "step_seconds": det["step_s"],
     }

@@ -182,15 +182,38 @@ VK_D void grad32(const Nb6& n, float& gx, float& gy, float& gz) {
     gz = fmul(__fsub_rn(n.zh, n.zl), n.sz);
 }
 
-// |v| in fp32, within 4 u32 relative of the exact Euclidean norm: the sum of
-// squares carries <= 3.5 u32, halved by the square root, plus the hardware
-// sqrt.approx.f32 (MUFU.SQRT) error -- measured <= 1.67 x 2^-24 relative over
-// 1.3e9 random finite inputs incl. subnormals (scripts/micro/sqrt_approx_err.cu).
+// Does the reference vote for this voxel?  Its fp64 gradient is nonzero
+// exactly when some neighbour pair differs (volume.py:244-264) -- also when the
+// fp32 gradient rounds to zero (a one-subnormal-ulp difference halved).
+VK_D bool grad_nonzero(const Nb6& n) { return n.xh != n.xl || n.yh != n.yl || n.zh != n.zl; }
+
+constexpr float kMinSub = 1.40129846e-45f;  // 2^-149, the smallest positive fp32 subnormal
+constexpr float kFltMin = 1.17549435e-38f;  // 2^-126, the smallest normal fp32
+
+// Rare path of norm3_f32 (|v| < ~1.1e-19, where the fp32 squares underflow):
+// the components are scaled by 2^64 first (exact: they are < 2^-63 here, so
+// the scaled values are normal and small), the norm is taken with a correctly
+// rounded sqrt and scaled back (exact unless the result is subnormal, then
+// within 2^-150 absolute).
+static __device__ __noinline__ float norm3_f32_tiny(float x, float y, float z) {
+    const float k = 18446744073709551616.0f, ik = 5.42101086242752217e-20f;  // 2^64, 2^-64
+    const float a = fmul(x, k), b = fmul(y, k), c = fmul(z, k);
+    return fmul(__fsqrt_rn(fadd(fadd(fmul(a, a), fmul(b, b)), fmul(c, c))), ik);
+}
+
+// |v| in fp32: within 4 u32 relative of the exact Euclidean norm when the
+// fp32 sum of squares is normal (it carries <= 3.5 u32, halved by the square
+// root, plus the hardware sqrt.approx.f32 (MUFU.SQRT) error, <= 1.67 x 2^-24
+// relative over every positive finite fp32 input, scripts/micro/sqrt_approx_err.cu
+// exhaustive sweep); below that the squares would underflow (|v| ~ 1e-19 can
+// give s == 0), so the rescaled rare path above takes over: everywhere the
+// error is <= 4 u32 relative + 2^-150 absolute.
 #ifndef VK_APPROX_SQRT
 #define VK_APPROX_SQRT 1
 #endif
 VK_D float norm3_f32(float x, float y, float z) {
     const float s = fadd(fadd(fmul(x, x), fmul(y, y)), fmul(z, z));
+    if (s < kFltMin) return norm3_f32_tiny(x, y, z);
 #if VK_APPROX_SQRT
     float r;
     asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(s));
@@ -200,9 +223,18 @@ VK_D float norm3_f32(float x, float y, float z) {
 #endif
 }
 
-// Relative error bound of fp32 votes against the reference's fp64 votes
-// (4 u32 for the norm, 1 u32 for the window cast, 1 u32 for the product,
-// rounded up generously), and an absolute allowance for fp32 subnormals.
+// The fast path's vote of a voxel the reference votes for (grad_nonzero):
+// never 0, because the reference's fp64 vote of a nonzero gradient is
+// positive and the certifications treat bins that are 0 in the fast sums as
+// exactly empty in the reference too.  The clamp to 2^-149 (e.g. a tiny |g|
+// times the window underflowing) moves a vote by less than kVoteAbs.
+VK_D float nz_vote(float v) { return fmaxf(v, kMinSub); }
+
+// Error bound of a fast fp32 vote against the reference's fp64 vote:
+// relative 4 u32 for the norm (norm3_f32, valid for every |g| incl. tiny and
+// subnormal ones), 1 u32 for the window cast, 1 u32 for the product, rounded
+// up generously; absolute: subnormal rounding of the components, the norm, the
+// product and the nz_vote clamp (each <= 2^-149 ~ 1.4e-45).
 constexpr double kVoteRel = 1.0e-6;
 constexpr double kVoteAbs = 1.0e-43;
 

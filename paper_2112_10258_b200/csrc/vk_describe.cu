@@ -1,16 +1,22 @@
 // vk_describe.cu -- SIFT-Rank, BRIEF and RRIEF descriptors.
 //
 // Reference: descriptor.py:227-263 (sift_rank_descriptor), descriptor.py:77-83
-// (rank_vector), descriptor.py:96-111 (extract_patch), descriptor.py:196-224
-// (preblur_patch, _pair_samples, brief/rrief), descriptor.py:309-316 (packing).
+// (rank_vector), descriptor.py:86-111 (extract_patch), descriptor.py:196-224
+// (preblur_patch, _pair_samples, brief/rrief), descriptor.py:309-321 (packing).
 //
-// SIFT-Rank: one CTA per (keypoint, frame), persistent.  Votes (|R^T g| into
-// spatial-octant x gradient-octant bins) are bit-exact; the 64 bins are
-// summed in a parallel order with a rigorous bound against the reference's
-// sequential np.add.at order.  The output is only the stable rank vector, so
-// if every adjacent pair of the sorted bins is separated by more than the
-// bound the ranks are exact; otherwise the CTA re-accumulates in reference
-// order (one warp, lane-by-lane broadcast).
+// SIFT-Rank: one 256-thread CTA per keypoint (all of its frames at once),
+// persistent.  The ball is walked in z-major order; each voxel's fp32
+// gradient is computed once and voted (fp32 |g|, within kVoteRel + kVoteAbs of
+// the reference's fp64 |R^T g|) into the spatial-octant x gradient-octant bin
+// of every frame.  Octant bits come from fp32 rotated components where they
+// clear their error bound; uncertain (voxel, frame) pairs are deferred to a
+// per-warp queue and resolved with the reference's fp64 FMA chains.  Votes go
+// into a per-CTA fp64 histogram in L2 by fire-and-forget reductions (any
+// order).  The output is only the stable rank vector: if every adjacent pair
+// of the sorted bins is separated by more than the bound between that sum and
+// the reference's sequential np.add.at, the ranks are exact; otherwise only
+// the bins of the unseparated pairs are re-accumulated in reference order
+// with fp64 votes (sr_exact_subset).
 //
 // BRIEF / RRIEF: one CTA per frame.  The side^3 reoriented patch is sampled
 // from the source volume (fp64 trilinear, cast to fp32) straight into shared
@@ -264,14 +270,14 @@ VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const fl
                     gy = q.y;
                     gz = q.z;
                     mag = q.w;
-                    has = mag > 0.f;  // |g| > 0 exactly when g != 0 (fp64 norm, never underflows in fp32)
+                    has = mag > 0.f;  // gradient_volume_kernel: |g| >= 2^-149 exactly when the fp64 g != 0
                 } else {
                     prefetch_plane_ahead(data, L.nx, L.ny, L.nz, x, y, z, kPrefetchPlanes);
                     const Nb6 nb = INTERIOR ? load_nb6_interior(data, (unsigned)L.nx, plane, c)
                                             : load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
                     grad32(nb, gx, gy, gz);
-                    has = !(gx == 0.f && gy == 0.f && gz == 0.f);  // zero vote: no bin changes
-                    if (has) mag = norm3_f32(gx, gy, gz);
+                    has = grad_nonzero(nb);  // zero vote: no bin changes
+                    if (has) mag = nz_vote(norm3_f32(gx, gy, gz));
                 }
             }
         }
@@ -341,8 +347,8 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
             ++cnt;
             float gx, gy, gz;
             grad32(cur, gx, gy, gz);
-            if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {  // zero vote: no bin changes
-                const float mag = norm3_f32(gx, gy, gz);
+            if (grad_nonzero(cur)) {  // zero vote: no bin changes
+                const float mag = nz_vote(norm3_f32(gx, gy, gz));
                 const int ox = unpack_off(pc, 0), oy = unpack_off(pc, 1), oz = unpack_off(pc, 2);
 #pragma unroll
                 for (int f = 0; f < NF; ++f) {
@@ -496,7 +502,7 @@ __device__ __noinline__ void sr_exact_subset(const float* data, const vk_level& 
                 const Nb6 nb = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
                 float gx, gy, gz;
                 grad32(nb, gx, gy, gz);
-                if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {
+                if (grad_nonzero(nb)) {
                     const int b = sr_bin_fast(ox, oy, oz, gx, gy, gz, Rsm, Rc, data, L.nx, L.ny, L.nz, x, y, z);
                     if (unc[b]) {
                         double x64, y64, z64;
@@ -628,7 +634,10 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
                 int bad = 0;
                 if (mine && b + 1 < kSrBins) {
                     const double x = w4[fl][order4[fl][b]], y = w4[fl][order4[fl][b + 1]];
-                    if (!(x == 0.0 && y == 0.0)) {  // exact empty-bin ties are order-independent
+                    // exact empty-bin ties are order-independent: a fast bin is 0 exactly when
+                    // no voxel with a nonzero fp64 gradient voted into it (grad_nonzero, nz_vote),
+                    // i.e. exactly when the reference's bin is 0
+                    if (!(x == 0.0 && y == 0.0)) {
                         const double xhi = x == 0.0 ? 0.0 : dadd(x, x * epsrel + epsabs);
                         const double ylo = dsub(y, y * epsrel + epsabs);
                         bad = !(xhi < ylo);

@@ -1,20 +1,22 @@
 // vk_orient.cu -- spherical gradient histograms and orientation frames.
 //
-// Reference: orient.py:271-307 (gradient_histogram), orient.py:310-350
+// Reference: orient.py:89-125 (gradient_histogram), orient.py:128-168
 // (dominant_orientations), pipeline.py:41-67 (assign_orientations).
 //
-// One CTA (128 threads) per keypoint, persistent over the keypoint list (the
-// count lives in device memory so the whole pipeline can be graph-captured).
-// Every vote is computed bit-exactly (fp64 gradients, numpy's norm order,
-// OpenBLAS's FMA chain for the direction dots, host-numpy window table).  The
-// reference then accumulates votes strictly sequentially (np.add.at); we
-// accumulate them in a parallel order instead (private per-thread bins +
-// ordered tree), and carry a rigorous bound on the difference between the two
-// summation orders.  Every decision the frames depend on (the full weight
-// order, the secondary_ratio threshold) is checked against that bound; if any
-// decision is not certain, the CTA recomputes the histogram in the exact
-// reference order (one warp, votes broadcast lane by lane).  Either way the
-// frames are identical to the reference's.
+// orient_kernel: one 256-thread CTA per keypoint, persistent over the keypoint
+// list (the count lives in device memory so the whole pipeline can be
+// graph-captured).  Fast path: the ball is walked in z-major order (coalesced
+// gathers); each voxel's vote is the fp32 |g| x window (within kVoteRel +
+// kVoteAbs of the reference's fp64 vote) and its bin the exact nearest
+// icosphere direction (lookup table, boundary cells deferred to a per-warp
+// queue and resolved by a screened fp32 argmax with an fp64 fallback).  Votes
+// are added with fire-and-forget fp64 reductions into a per-CTA histogram in
+// L2 (any order).  Every decision the frames depend on (the top of the weight
+// order, the secondary_ratio threshold) is checked against a rigorous bound on
+// the difference between that sum and the reference's sequential np.add.at;
+// only the bins of an uncertain decision are re-accumulated in the reference's
+// order with fp64 votes (ori_exact_subset).  Either way the frames are the
+// reference's.
 #include "vk_hood.cuh"
 
 namespace vk {
@@ -196,6 +198,15 @@ VK_D int nearest_dir_lut(const uint8_t* lut, float gx, float gy, float gz, float
     return lut[kLutN * kLutN + c * 24 + perm * 8 + sb];
 }
 
+// Rare path: tiny gradients (|g|_1 < 1e-30, down to fp32 subnormals or an
+// fp32 gradient that rounded to 0), where the fp32 scores and margins below
+// lose their relative accuracy: the reference's 42 fp64 dots directly.
+__device__ __noinline__ int nearest_dir_tiny(const double* dirs, const Nb6& nb) {
+    double x64, y64, z64;
+    grad64(nb, x64, y64, z64);
+    return nearest_dir(dirs, 42, x64, y64, z64);
+}
+
 VK_D int nearest_dir_ico(const double* dirs, const IcoSh& ic, const uint8_t* lut, float gx, float gy, float gz,
                          const Nb6& nb) {
     constexpr float PHI = 1.6180339887498949f;
@@ -205,6 +216,7 @@ VK_D int nearest_dir_ico(const double* dirs, const IcoSh& ic, const uint8_t* lut
         if (k >= 0) return k;
     }
     const float l1 = ax + ay + az;
+    if (!(l1 >= 1.0e-30f)) return nearest_dir_tiny(dirs, nb);
     const float vA = fmaf(PHI, az, ay), vB = fmaf(PHI, ay, ax), vC = fmaf(PHI, ax, az);
     const float m = 1.0e-5f * 2.7f * l1;
     const int fast = nearest_dir_fast(ic, gx, gy, gz, ax, ay, az, l1, vA, vB, vC, m);
@@ -260,8 +272,8 @@ VK_D int ori_vote_fast(const Nb6& n, const float* __restrict__ win32, int d2, co
                        const uint8_t* lut, int K, float& vote) {
     float gx, gy, gz;
     grad32(n, gx, gy, gz);
-    if (gx == 0.f && gy == 0.f && gz == 0.f) return -1;
-    vote = fmul(norm3_f32(gx, gy, gz), __ldg(win32 + d2));
+    if (!grad_nonzero(n)) return -1;
+    vote = nz_vote(fmul(norm3_f32(gx, gy, gz), __ldg(win32 + d2)));
     if (ic) return nearest_dir_ico(dirs, *ic, lut, gx, gy, gz, n);
     double x64, y64, z64;
     grad64(n, x64, y64, z64);
@@ -319,8 +331,8 @@ VK_D int ori_walk(const vk_kp& kp, const vk_level& L, const float* data, const v
                 if (defer) {
                     float gx, gy, gz;
                     grad32(nb, gx, gy, gz);
-                    if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {
-                        vote = fmul(norm3_f32(gx, gy, gz), __ldg(win32 + (ox * ox + oy * oy + oz * oz)));
+                    if (grad_nonzero(nb)) {
+                        vote = nz_vote(fmul(norm3_f32(gx, gy, gz), __ldg(win32 + (ox * ox + oy * oy + oz * oz))));
                         bin = nearest_dir_lut(lut, gx, gy, gz, fabsf(gx), fabsf(gy), fabsf(gz));
                         miss = bin < 0;
                     }
@@ -384,10 +396,10 @@ gradient_volume_kernel(const float* __restrict__ level, float4* __restrict__ g4,
         grad32(n, gx, gy, gz);
         float4 o = make_float4(gx, gy, gz, 0.f);
         int bin = 255;
-        if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {
+        if (grad_nonzero(n)) {
             double x64, y64, z64;
             grad64(n, x64, y64, z64);
-            o.w = (float)norm3_numpy(x64, y64, z64);
+            o.w = nz_vote((float)norm3_numpy(x64, y64, z64));
             bin = nearest_dir_ico(dirs, ic, nullptr, gx, gy, gz, n);
         }
         g4[i] = o;
@@ -433,8 +445,8 @@ orient_field_kernel(const float* __restrict__ level, float* __restrict__ mag, ui
         grad32(n, gx, gy, gz);
         float m = 0.f;
         int bin = 255;
-        if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {
-            m = norm3_f32(gx, gy, gz);
+        if (grad_nonzero(n)) {
+            m = nz_vote(norm3_f32(gx, gy, gz));
             bin = nearest_dir_ico(dirs, ic, ico_lut, gx, gy, gz, n);
         }
         mag[i] = m;
@@ -492,7 +504,7 @@ VK_D int field_walk(const vk_kp& kp, const vk_level& L, const float* __restrict_
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             cnt += ok[u];
-            red_vote(hist, b[u] == 255 ? -1 : b[u], fmul(m[u], w[u]));
+            red_vote(hist, b[u] == 255 ? -1 : b[u], nz_vote(fmul(m[u], w[u])));
         }
     }
     return cnt;
@@ -630,7 +642,7 @@ __device__ __noinline__ void ori_exact_subset(const float* data, const vk_level&
                 const Nb6 nb = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
                 float gx, gy, gz;
                 grad32(nb, gx, gy, gz);
-                if (!(gx == 0.f && gy == 0.f && gz == 0.f)) {
+                if (grad_nonzero(nb)) {
                     double x64, y64, z64;
                     grad64(nb, x64, y64, z64);
                     const int b = icp ? nearest_dir_ico(dirs, *icp, lut, gx, gy, gz, nb) : nearest_dir(dirs, K, x64, y64, z64);
@@ -730,7 +742,7 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
                         const int b = __ldg(bl + idx);
                         if (b != 255) {
                             bin = b;
-                            vote = fmul(__ldg(&gl[idx].w), __ldg(win32 + (ox * ox + oy * oy + oz * oz)));
+                            vote = nz_vote(fmul(__ldg(&gl[idx].w), __ldg(win32 + (ox * ox + oy * oy + oz * oz))));
                         }
                     }
                 }

@@ -67,27 +67,47 @@ def gather_database(desc, subjects, group=None):
 def match_database(local: dict, ratio_max: float = 0.9, metric: str = "euclidean", group=None) -> dict:
     """{subject: descriptor array} for this rank's subjects -> {subject:
     (best_index, d1, d2, keep)} against all other subjects' descriptors (indices
-    into concat of the other subjects in id order).  Rank descriptors (int,
-    values in [-128, 127]) travel as int8; packed BRIEF bits as uint8."""
+    into concat of the other subjects in id order).  Rank descriptors whose
+    values all fit in int8 (every rank decides the same way: the min / max are
+    all-reduced) travel as int8 and run on the tensor-core kernel; any other
+    integer or float rows go through the fp64 kernel (nearest_neighbor_matches'
+    own choice, match.py _prepare).  Packed BRIEF bits travel as uint8.  A
+    subject with no descriptors gets empty arrays (the reference composition
+    returns no matches for an empty query)."""
     t = _lib.torch()
     ids = sorted(local)
     if metric not in ("hamming", "euclidean"):
         raise ParameterError(f"unknown metric {metric!r}")
     arrs = [np.asarray(local[i]) for i in ids]
+    width = next((a.shape[1] for a in arrs if a.ndim == 2 and a.size), None)
+    if width is None:
+        width = 8 if metric == "hamming" else 64
+    arrs = [a.reshape(len(a), width) if a.size else np.zeros((0, width), a.dtype if a.size else np.int64) for a in arrs]
     if metric == "hamming":
-        rows = np.concatenate([a.astype(np.uint8) for a in arrs]) if arrs else np.zeros((0, 8), np.uint8)
+        rows = np.concatenate([a.astype(np.uint8) for a in arrs]) if arrs else np.zeros((0, width), np.uint8)
         pad = (-rows.shape[1]) % 8
         code = 0
     else:
-        rows = np.concatenate([a.astype(np.int8) for a in arrs]) if arrs else np.zeros((0, 64), np.int8)
-        pad = (-rows.shape[1]) % 32 if rows.shape[1] <= 128 else (-rows.shape[1]) % 4
-        code = 1
+        allr = np.concatenate(arrs) if arrs else np.zeros((0, width), np.int64)
+        integral = allr.dtype.kind in "iub"
+        lo_hi = np.array([allr.min() if allr.size else 0, allr.max() if allr.size else 0, 0 if integral else 1],
+                         dtype=np.float64)
+        lo_hi = _allreduce_minmax(lo_hi, group)
+        if lo_hi[2] == 0 and lo_hi[0] >= -128 and lo_hi[1] <= 127:
+            rows = allr.astype(np.int8)
+            pad = (-rows.shape[1]) % 32 if rows.shape[1] <= 128 else (-rows.shape[1]) % 4
+            code = 1
+        else:
+            rows = np.ascontiguousarray(allr, dtype=np.float64)
+            pad = 0
+            code = 2
     rows = np.pad(rows, ((0, 0), (0, pad)))
     subj = np.concatenate([np.full(len(a), i, np.int32) for i, a in zip(ids, arrs)]) if arrs else np.zeros(0, np.int32)
     d_rows = t.from_numpy(np.ascontiguousarray(rows)).cuda()
     db, _, ranges = gather_database(d_rows, t.from_numpy(subj).cuda(), group)
     out = {}
     dim = db.shape[1]
+    empty = (np.zeros(0, np.int32), np.zeros(0), np.zeros(0), np.zeros(0, np.uint8))
     if code == 1 and dim % 32 == 0 and dim <= 128 and len(rows):
         # one tensor-core launch for every local query row, each excluding its
         # own subject's rows (vk_match_rows_excluding)
@@ -95,7 +115,7 @@ def match_database(local: dict, ratio_max: float = 0.9, metric: str = "euclidean
         ex = np.empty((n, 2), dtype=np.int32)
         off = 0
         for i, a in zip(ids, arrs):
-            ex[off: off + len(a)] = ranges[i]
+            ex[off: off + len(a)] = ranges.get(i, (0, 0))
             off += len(a)
         row_ex = t.from_numpy(ex).cuda()
         best = t.empty(n, dtype=t.int32, device="cuda")
@@ -113,17 +133,34 @@ def match_database(local: dict, ratio_max: float = 0.9, metric: str = "euclidean
         return out
     off = 0
     for i, a in zip(ids, arrs):
-        q = d_rows[off: off + len(a)]
-        off += len(a)
-        lo, hi = ranges[i]
         n = len(a)
-        best = t.empty(max(n, 1), dtype=t.int32, device="cuda")
-        d1 = t.empty(max(n, 1), dtype=t.float64, device="cuda")
-        d2 = t.empty(max(n, 1), dtype=t.float64, device="cuda")
-        keep = t.empty(max(n, 1), dtype=t.uint8, device="cuda")
-        if n:
-            _lib.call("vk_match_excluding", code, q.data_ptr(), n, db.data_ptr(), db.shape[0], db.shape[1],
-                      float(ratio_max), lo, hi, best.data_ptr(), d1.data_ptr(), d2.data_ptr(), keep.data_ptr(),
-                      _lib.stream_ptr())
-        out[i] = (best[:n].cpu().numpy(), d1[:n].cpu().numpy(), d2[:n].cpu().numpy(), keep[:n].cpu().numpy())
+        q = d_rows[off: off + n]
+        off += n
+        if n == 0:
+            out[i] = empty
+            continue
+        lo, hi = ranges[i]
+        best = t.empty(n, dtype=t.int32, device="cuda")
+        d1 = t.empty(n, dtype=t.float64, device="cuda")
+        d2 = t.empty(n, dtype=t.float64, device="cuda")
+        keep = t.empty(n, dtype=t.uint8, device="cuda")
+        _lib.call("vk_match_excluding", code, q.data_ptr(), n, db.data_ptr(), db.shape[0], db.shape[1],
+                  float(ratio_max), lo, hi, best.data_ptr(), d1.data_ptr(), d2.data_ptr(), keep.data_ptr(),
+                  _lib.stream_ptr())
+        out[i] = (best.cpu().numpy(), d1.cpu().numpy(), d2.cpu().numpy(), keep.cpu().numpy())
     return out
+
+
+def _allreduce_minmax(v: np.ndarray, group=None) -> np.ndarray:
+    """[min, max, any_float] reduced over the ranks (identity without a process group)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return v
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    lo = torch.tensor([v[0]], dtype=torch.float64, device=dev)
+    hi = torch.tensor([v[1], v[2]], dtype=torch.float64, device=dev)
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    return np.array([lo.item(), hi[0].item(), hi[1].item()])

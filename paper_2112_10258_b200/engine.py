@@ -155,7 +155,7 @@ class Extractor:
 
     def __init__(self, dims, cfg: PipelineConfig | None = None, batch: int = 1, kp_cap: int | None = None,
                  frame_cap: int | None = None, exact_only: bool = False, input=None, gradient_volumes: bool = False,
-                 orient_field: bool = False):
+                 orient_field: bool = False, cand_cap: int | None = None):
         t = _lib.torch()
         self.cfg = cfg or PipelineConfig()
         self.plan = Plan.build(dims, self.cfg)
@@ -164,7 +164,7 @@ class Extractor:
         self.exact_only = int(bool(exact_only))
         nx, ny, nz = self.plan.dims
         vox = nx * ny * nz
-        self.cand_cap = int(max(4096, vox // 128))
+        self.cand_cap = int(cand_cap or max(4096, vox // 128))
         self.kp_cap = int(kp_cap or self.B * max(2048, vox // 512))
         self.frame_cap = int(frame_cap or 2 * self.kp_cap)
         self.maxf = int(self.cfg.max_frames)

@@ -114,16 +114,55 @@ def _wrap_pyramids(ex: Extractor, volume: Volume):
     return pyr, DoGPyramid(dogs, P.kappa, L)
 
 
+class _ExtractorPool:
+    """Extractors cached per (dims, config) for the drop-in API: building one
+    (plan, host tables, every device buffer) costs far more than running it on
+    one volume.  A returned ExtractionResult keeps views of its Extractor's
+    pyramid levels, so an Extractor is reused only once the result of its
+    previous call is gone (weak reference); a loop that keeps the previous
+    result alive alternates between two.  At most ``cap`` per key."""
+
+    def __init__(self, cap: int = 3):
+        self.cap = cap
+        self.entries: dict = {}
+
+    def get(self, key, make):
+        import weakref
+
+        lst = self.entries.setdefault(key, [])
+        for e in lst:
+            if e[1] is None or e[1]() is None:
+                return e
+        e = [make(), None]
+        if len(lst) < self.cap:
+            lst.append(e)
+        return e
+
+    def clear(self):
+        self.entries.clear()
+
+
+_POOL = _ExtractorPool()
+
+
+def clear_extractor_cache() -> None:
+    """Drop the cached drop-in Extractors (frees their device memory)."""
+    _POOL.clear()
+
+
 def extract_features(volume: Volume, config: PipelineConfig | None = None, recorder=None) -> ExtractionResult:
-    """pipeline.py:70-102 on the GPU."""
+    """pipeline.py:70-102 on the GPU (Extractor cached per (dims, config))."""
+    import weakref
+
     cfg = config or PipelineConfig()
     if cfg.descriptor != "siftrank":
         from .descriptor import sample_point_pairs
 
         sample_point_pairs(cfg.method, cfg.pairs, 1.0, cfg.seed)  # validation order of pipeline.py:86-88
-    kp_cap = frame_cap = None
+    key = (tuple(volume.dims), cfg.model_dump_json())
+    entry = _POOL.get(key, lambda: Extractor(volume.dims, cfg, batch=1))
+    ex = entry[0]
     while True:
-        ex = Extractor(volume.dims, cfg, batch=1, kp_cap=kp_cap, frame_cap=frame_cap)
         ex.input[0].copy_(device_of(volume))
         ex.enqueue(rec=_stage(recorder) if recorder is not None else None)
         c = ex.check_capacity()
@@ -131,14 +170,20 @@ def extract_features(volume: Volume, config: PipelineConfig | None = None, recor
             break
         kp_cap = max(ex.kp_cap, c["keypoints"] + 1)
         frame_cap = max(ex.frame_cap, c["frames"] + 1)
+        cand_cap = None
         if c["cand_overflow"]:
-            ex.cand_cap = int(c["cand"].max()) + 1
-            kp_cap = max(kp_cap, ex.cand_cap)
+            cand_cap = int(c["cand"].max()) + 1
+            kp_cap = max(kp_cap, cand_cap)
             frame_cap = max(frame_cap, kp_cap * cfg.max_frames)
+        ex = Extractor(volume.dims, cfg, batch=1, kp_cap=kp_cap, frame_cap=frame_cap,
+                       cand_cap=max(ex.cand_cap, cand_cap or 0))
+        entry[0] = ex  # the grown Extractor replaces the cached one
     soa = ex.results()
     pyr, dog = _wrap_pyramids(ex, volume)
-    return ExtractionResult(pyr, dog, dropped_orientation=soa["dropped_orientation"], _soa=soa, _kind=cfg.descriptor,
-                            _npairs=cfg.pairs)
+    res = ExtractionResult(pyr, dog, dropped_orientation=soa["dropped_orientation"], _soa=soa, _kind=cfg.descriptor,
+                           _npairs=cfg.pairs)
+    entry[1] = weakref.ref(res)
+    return res
 
 
 def extract_batch(volumes, config: PipelineConfig | None = None, extractor: Extractor | None = None):

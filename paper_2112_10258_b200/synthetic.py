@@ -127,3 +127,16 @@ def batch_from(base: np.ndarray, count: int, seed: int = 0, noise: float = 0.01)
         v = np.roll(v, tuple(int(s) for s in rng.integers(0, 16, size=3)), axis=(0, 1, 2))
         out[i] = v + rng.normal(0.0, noise, size=base.shape).astype(np.float32)
     return out
+
+
+def zero_background_volume(dims, seed: int, radius_frac: float = 0.42, scale: float = 1.0) -> np.ndarray:
+    """Soup phantom + N(0, 0.01) set to exactly 0 outside a centred sphere of
+    radius ``radius_frac * min(dims)`` (a skull-stripped-MRI-like background),
+    then multiplied by ``scale`` in float32 (scale = 1e-22 makes every fp32 sum
+    of squared gradient components underflow).  Golden: tests/golden/zeroback.npz."""
+    v = soup_volume(dims, np.random.default_rng(seed), noise=0.01)
+    c = (np.array(dims) - 1) / 2.0
+    g = np.meshgrid(*[np.arange(d) for d in dims], indexing="ij")
+    r2 = sum((gi - ci) ** 2 for gi, ci in zip(g, c))
+    v = np.where(r2 <= (radius_frac * min(dims)) ** 2, v, 0.0).astype(np.float32)
+    return (v * np.float32(scale)).astype(np.float32)

@@ -12,6 +12,6 @@ name, defs = sys.argv[1], sys.argv[2:]
 out_dir = os.path.join(B.REPO, "variants")
 os.makedirs(out_dir, exist_ok=True)
 out = os.path.join(out_dir, f"libvolkey_{name}.so")
-cmd = [B.NVCC, *B.ARCH, *B.FLAGS, *defs, "-I", os.path.join(B.REPO, "include"), *B.sources(), "-o", out]
+cmd = [B.NVCC, *B.ARCH, *B.FLAGS_C, "-shared", "-cudart", "shared", *defs, "-I", os.path.join(B.REPO, "include"), *B.sources(), "-o", out]
 subprocess.run(cmd, check=True)
 print(out)
