@@ -128,10 +128,22 @@ int vk_blur3d(const float* src, float* dst, float* dog_out, float* half_out,
 int vk_blur3d_ws(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny, int nz,
                  const float* taps_host, int radius, float* work, long long work_floats, void* stream);
 
+/* vk_blur3d with a caller-chosen work granularity: the z pass runs in chunks
+ * of `zchunk` output planes per CTA (each chunk re-reads 2R warm-up planes),
+ * the analogue of the reference's chunk (scalespace.py convolve_separable,
+ * parallel.py task size).  Output is independent of zchunk. */
+int vk_blur3d_chunked(const float* src, float* dst, int nb, int nx, int ny, int nz, const float* taps_host,
+                      int radius, int zchunk, void* stream);
+
 /* Blur kernel selection: 0 = split (x, y) kernel + z kernel through an
  * intermediate level (default), 1 = fused single-pass streaming kernel.
  * Results are bit-identical. */
 int vk_set_blur_path(int path);
+
+/* (x, y) kernel of the split path: 0 = whole-plane register-ring kernel
+ * (bulk-copy staged plane, thread per row / column; default wherever the
+ * plane fits two CTAs per SM), 1 = tiled kernel.  Results are bit-identical. */
+int vk_set_xy_kernel(int k);
 
 /* The tail of the pyramid in one launch (scalespace.py:186-251 for octaves
  * whose levels hold <= 16384 voxels): one CTA per volume runs every level of

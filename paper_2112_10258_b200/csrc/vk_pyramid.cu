@@ -501,6 +501,141 @@ blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, i
     }
 }
 
+// ---------------------------------------------------------------------------
+// Whole-plane (x, y) pass with register rings (default split path).
+//
+// One CTA = one (volume, z) plane.  The plane is staged into shared memory
+// with ONE bulk asynchronous copy (cp.async.bulk, TMA engine, completion on an
+// mbarrier) of its 16-byte-aligned byte superset: rows keep the global pitch
+// nx, no pitched level layout needed.  Then
+//  * x-pass: thread t walks row t along x with a ring of 2R+1 accumulators in
+//    registers (outputs x-R .. x+R in flight): each arriving value is
+//    multiplied once per tap distance (R+1 products, shared by the symmetric
+//    taps) and added into the 2R outputs that use it, in tap order -- the
+//    minimum fp32 work for bit parity (R+1 products + 2R adds per output, vs
+//    ~19.5 + 20 at R = 10 for the register-blocked tile kernel).  Results are
+//    written back in place (an output is complete R arrivals after its input
+//    position was read, and no later arrival reads it).
+//  * y-pass: thread t walks column t along y with the same ring and writes the
+//    (x, y)-blurred values straight to the intermediate (lanes = consecutive
+//    x: coalesced stores, conflict-free shared reads).
+// Ring indices are compile-time constants: arrivals run in chunks of 2R+1
+// with the phase unrolled, the tail by a uniform compile-time chain.
+template <int R, int C>
+VK_D float ring_arrive(float (&r)[2 * R + 1], float v, const Taps& taps) {
+    constexpr int P = 2 * R + 1;
+#pragma unroll
+    for (int d = 0; d <= R; ++d) {
+        const float p = fmul(taps.w[R + d], v);
+        if (d == 0) {
+            r[C] = fadd(r[C], p);
+        } else {
+            const int up = (C + d) % P, dn = (C - d + P) % P;
+            if (d == R) r[up] = p;
+            else r[up] = fadd(r[up], p);
+            r[dn] = fadd(r[dn], p);
+        }
+    }
+    return r[(C - R + P) % P];
+}
+
+// Arrivals k0 + C, k0 + C + 1, ... up to the chunk end (P) or `left` arrivals.
+template <int R, int C, bool FULL, class Ld, class St>
+VK_D void ring_steps(float (&r)[2 * R + 1], int k0, int left, Ld& ld, St& st, const Taps& taps, float (&pf)[2]) {
+    constexpr int P = 2 * R + 1;
+    if constexpr (C < P) {
+        if (FULL || C < left) {
+            const int k = k0 + C;
+            const float v = pf[C & 1];
+            pf[C & 1] = ld(k + 2);  // two arrivals of load lead
+            const float o = ring_arrive<R, C>(r, v, taps);
+            if (k >= 2 * R) st(k - 2 * R, o);
+            ring_steps<R, C + 1, FULL>(r, k0, left, ld, st, taps, pf);
+        }
+    }
+}
+
+// One line of n values: arrival k (k = 0 .. n+2R-1) brings the value at
+// position clamp(k - R, 0, n - 1) (replicate padding, scalespace.py:45-92);
+// output o = k - 2R is complete after arrival k.
+template <int R, class Ld, class St>
+VK_D void ring_line(int n, Ld ld, St st, const Taps& taps) {
+    constexpr int P = 2 * R + 1;
+    float r[P];
+#pragma unroll
+    for (int t = 0; t < P; ++t) r[t] = 0.f;
+    const int A = n + 2 * R;
+    float pf[2] = {ld(0), ld(1)};
+    int k0 = 0;
+    for (; k0 + P <= A; k0 += P) ring_steps<R, 0, true>(r, k0, P, ld, st, taps, pf);
+    if (k0 < A) ring_steps<R, 0, false>(r, k0, A - k0, ld, st, taps, pf);
+}
+
+constexpr int kPlaneThreads = 192;
+
+VK_D void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+VK_D void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+VK_D void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+VK_D void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (unsigned)__cvta_generic_to_shared(smem)),
+        "l"(gmem), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+
+template <int R>
+__global__ void __launch_bounds__(kPlaneThreads, 2)
+blur_xy_plane_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, int ny, Taps taps) {
+    extern __shared__ float4 smem4[];
+    __shared__ uint64_t bar;
+    const int tid = threadIdx.x;
+    const unsigned plane = (unsigned)nx * (unsigned)ny;
+    const float* g = src + (size_t)blockIdx.x * plane;  // plane (b * nz + z)
+    const uintptr_t ga = reinterpret_cast<uintptr_t>(g);
+    const uintptr_t a0 = ga & ~(uintptr_t)15;
+    const unsigned bytes = (unsigned)(((ga + 4ull * plane) - a0 + 15) & ~(uintptr_t)15);
+    float* s = reinterpret_cast<float*>(smem4) + (ga - a0) / 4;  // element (0, 0) of the staged plane
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        mbar_expect_tx(&bar, bytes);
+        bulk_g2s(smem4, reinterpret_cast<const void*>(a0), bytes, &bar);
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(&bar, 0);
+    if (tid < ny) {
+        float* row = s + tid * nx;
+        ring_line<R>(
+            nx, [&](int k) { return row[clampi(k - R, 0, nx - 1)]; }, [&](int o, float v) { row[o] = v; }, taps);
+    }
+    __syncthreads();
+    if (tid < nx) {
+        const float* col = s + tid;
+        float* out = tmp + (size_t)blockIdx.x * plane + tid;
+        ring_line<R>(
+            ny, [&](int k) { return col[clampi(k - R, 0, ny - 1) * nx]; },
+            [&](int o, float v) { out[(unsigned)o * (unsigned)nx] = v; }, taps);
+    }
+}
+
 // z pass over the (x, y)-blurred intermediate: thread = column pair
 // (gx, gx+1) of row gy; warp = 16 column pairs x rows (y, y+1) so the 2x2x2
 // subsample block of a thread is completed by lane ^ 16.  Planes outside
@@ -834,9 +969,33 @@ static int launch_xy(const float* src, float* work, int nb, int nx, int ny, int 
     return cuda_status(cudaGetLastError(), "blur xy launch");
 }
 
+// Whole-plane (x, y) kernel: planes up to kPlaneThreads rows and columns and
+// small enough for two CTAs per SM.
+static bool plane_kernel_fits(int nx, int ny) {
+    return nx <= kPlaneThreads && ny <= kPlaneThreads && (long long)nx * ny * 4 + 32 <= 110 * 1024;
+}
+
+template <int R>
+static int launch_xy_plane(const float* src, float* work, int nb, int nx, int ny, int nz, const Taps& taps,
+                           cudaStream_t st) {
+    const int smem = nx * ny * 4 + 32;
+    static int configured = 0;
+    if (configured < smem) {
+        cudaError_t e = cudaFuncSetAttribute(blur_xy_plane_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             110 * 1024);
+        if (e != cudaSuccess) return cuda_status(e, "blur xy plane attribute");
+        configured = 110 * 1024;
+    }
+    blur_xy_plane_kernel<R><<<nb * nz, kPlaneThreads, smem, st>>>(src, work, nx, ny, taps);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "blur xy plane launch");
+}
+
+static int g_xy_kernel = 0;  // 0: whole-plane ring kernel where it fits, 1: tile kernel (A/B)
+
 template <int R>
 static int launch_split(const float* src, float* dst, float* dog, float* half, int nb, int nx, int ny, int nz,
-                        const Taps& taps, float* work, cudaStream_t st) {
+                        const Taps& taps, float* work, cudaStream_t st, int zchunk) {
     static bool env_read = false;
     if (!env_read) {
         if (const char* e = getenv("VK_Z_WAVES")) kZWaves = atoi(e) > 0 ? atoi(e) : kZWaves;
@@ -847,7 +1006,8 @@ static int launch_split(const float* src, float* dst, float* dog, float* half, i
     const bool tall = ((ny + 95) / 96) * 96 <= ((ny + 63) / 64) * 64;
     // 97..176 rows: one tile spans the whole y extent (no recomputed x-pass halo rows between y tiles;
     // measured 3.6% faster pyramid on 145x174x145 despite 2 CTAs/SM instead of 4)
-    const int rc1 = ny <= 176 && ny > 96 ? launch_xy<R, 176>(src, work, nb, nx, ny, nz, taps, st)
+    const int rc1 = g_xy_kernel == 0 && plane_kernel_fits(nx, ny) ? launch_xy_plane<R>(src, work, nb, nx, ny, nz, taps, st)
+                    : ny <= 176 && ny > 96 ? launch_xy<R, 176>(src, work, nb, nx, ny, nz, taps, st)
                     : tall               ? launch_xy<R, 96>(src, work, nb, nx, ny, nz, taps, st)
                                          : launch_xy<R, 64>(src, work, nb, nx, ny, nz, taps, st);
     if (rc1 != VK_OK) return rc1;
@@ -859,6 +1019,7 @@ static int launch_split(const float* src, float* dst, float* dog, float* half, i
     const long long cols = (long long)((nx + 31) / 32) * ((ny + 15) / 16) * nb;
     int nzc = 1;
     while (cols * nzc < (long long)kZWaves * 8 * sms && (nz + nzc) / (nzc + 1) >= kZMinChunkR * R && nzc < 64) ++nzc;
+    if (zchunk > 0) nzc = (nz + zchunk - 1) / zchunk;  // caller-chosen granularity (convolve_separable's chunk)
     int tz = (nz + nzc - 1) / nzc;
     tz += tz & 1;
     nzc = (nz + tz - 1) / tz;
@@ -913,9 +1074,37 @@ extern "C" int vk_set_blur_path(int path) {
     return VK_OK;
 }
 
+extern "C" int vk_set_xy_kernel(int k) {
+    if (k < 0 || k > 1) {
+        set_error("vk_set_xy_kernel: 0 (whole-plane ring kernel) or 1 (tile kernel)");
+        return VK_ERR_PARAMETER;
+    }
+    g_xy_kernel = k;
+    return VK_OK;
+}
+
+static int blur3d_impl(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny, int nz,
+                       const float* taps_host, int radius, float* work, long long work_floats, int zchunk,
+                       void* stream);
+
 extern "C" int vk_blur3d_ws(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny,
                             int nz, const float* taps_host, int radius, float* work, long long work_floats,
                             void* stream) {
+    return blur3d_impl(src, dst, dog_out, half_out, nb, nx, ny, nz, taps_host, radius, work, work_floats, 0, stream);
+}
+
+extern "C" int vk_blur3d_chunked(const float* src, float* dst, int nb, int nx, int ny, int nz, const float* taps_host,
+                                 int radius, int zchunk, void* stream) {
+    if (zchunk < 1) {
+        set_error("vk_blur3d_chunked: chunk must be >= 1, got %d", zchunk);
+        return VK_ERR_PARAMETER;
+    }
+    return blur3d_impl(src, dst, nullptr, nullptr, nb, nx, ny, nz, taps_host, radius, nullptr, 0, zchunk, stream);
+}
+
+static int blur3d_impl(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny, int nz,
+                       const float* taps_host, int radius, float* work, long long work_floats, int zchunk,
+                       void* stream) {
     if (!src || !dst || !taps_host || nb < 0 || nx < 1 || ny < 1 || nz < 1 || radius < 1 ||
         2 * radius + 1 > VK_MAX_TAPS || work_floats < 0) {
         set_error("vk_blur3d: bad arguments (nb=%d dims=%d,%d,%d radius=%d)", nb, nx, ny, nz, radius);
@@ -945,16 +1134,16 @@ extern "C" int vk_blur3d_ws(const float* src, float* dst, float* dog_out, float*
         }
         int rc;
         switch (radius) {
-            case 1: rc = launch_split<1>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
-            case 2: rc = launch_split<2>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
-            case 3: rc = launch_split<3>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
-            case 4: rc = launch_split<4>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
-            case 5: rc = launch_split<5>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
-            case 6: rc = launch_split<6>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
-            case 7: rc = launch_split<7>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
-            case 8: rc = launch_split<8>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
-            case 9: rc = launch_split<9>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
-            default: rc = launch_split<10>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st); break;
+            case 1: rc = launch_split<1>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
+            case 2: rc = launch_split<2>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
+            case 3: rc = launch_split<3>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
+            case 4: rc = launch_split<4>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
+            case 5: rc = launch_split<5>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
+            case 6: rc = launch_split<6>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
+            case 7: rc = launch_split<7>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
+            case 8: rc = launch_split<8>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
+            case 9: rc = launch_split<9>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
+            default: rc = launch_split<10>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
         }
         if (own) cudaFreeAsync(w, st);
         return rc;

@@ -278,6 +278,14 @@ class Extractor:
                     _lib.call("vk_blur3d_ws", lv[i - 1].data_ptr(), lv[i].data_ptr(),
                               dg[i - 1].data_ptr() if with_dog else None, half, B, nx, ny, nz,
                               k.weights.ctypes.data, k.radius, self.blur_work.data_ptr(), self.blur_work.numel(), s)
+                # DoG and the handoff subsample are epilogues of that blur launch: their stage
+                # rows (bench.py STAGES) carry only what is left outside it, i.e. ~0
+                if with_dog:
+                    with rec("dog", o, i - 1):
+                        pass
+                if half is not None:
+                    with rec("subsample", o, i):
+                        pass
         if small < P.n_octaves:
             import ctypes as C
 
@@ -294,6 +302,11 @@ class Extractor:
             with rec("convolution", small, -1):
                 _lib.call("vk_small_octaves", n, L, handoff, dims.ctypes.data, C.cast(lp, C.c_void_p),
                           C.cast(dp, C.c_void_p), rad.ctypes.data, taps.ctypes.data, B, s)
+            with rec("dog", small, -1):  # fused into vk_small_octaves
+                pass
+            if n > 1:
+                with rec("subsample", small, handoff):
+                    pass
 
     def enqueue_detect(self, s: int, rec=None) -> None:
         """detect_keypoints (detect.py:149-182) for the whole batch."""
