@@ -539,18 +539,23 @@ VK_D float ring_arrive(float (&r)[2 * R + 1], float v, const Taps& taps) {
     return r[(C - R + P) % P];
 }
 
-// Arrivals k0 + C, k0 + C + 1, ... up to the chunk end (P) or `left` arrivals.
-template <int R, int C, bool FULL, class Ld, class St>
-VK_D void ring_steps(float (&r)[2 * R + 1], int k0, int left, Ld& ld, St& st, const Taps& taps, float (&pf)[2]) {
+// Arrivals k0 + C, ... up to the chunk end (FULL) or `left` arrivals.  SAFE:
+// every arrival of the chunk has an unclamped prefetch position and a valid
+// output (no clamps, no store predicate).  The line accessor provides
+// at(k0, j) = value at position k0 + j - R (clamped unless SAFE) and
+// put(k0, j, v) = store of output k0 + j - 2R; with a per-chunk base and a
+// compile-time j both become one shared-memory / global access.
+template <int R, int C, bool FULL, bool SAFE, class Line>
+VK_D void ring_steps(float (&r)[2 * R + 1], int k0, int left, Line& ln, const Taps& taps, float (&pf)[2]) {
     constexpr int P = 2 * R + 1;
     if constexpr (C < P) {
         if (FULL || C < left) {
-            const int k = k0 + C;
-            const float v = pf[C & 1];
-            pf[C & 1] = ld(k + 2);  // two arrivals of load lead
+            const float v = pf[0];  // two arrivals of load lead (a shifting pair: P is odd)
+            pf[0] = pf[1];
+            pf[1] = ln.template at<SAFE>(k0, C + 2);
             const float o = ring_arrive<R, C>(r, v, taps);
-            if (k >= 2 * R) st(k - 2 * R, o);
-            ring_steps<R, C + 1, FULL>(r, k0, left, ld, st, taps, pf);
+            if (SAFE || k0 + C >= 2 * R) ln.put(k0, C, o);
+            ring_steps<R, C + 1, FULL, SAFE>(r, k0, left, ln, taps, pf);
         }
     }
 }
@@ -558,18 +563,46 @@ VK_D void ring_steps(float (&r)[2 * R + 1], int k0, int left, Ld& ld, St& st, co
 // One line of n values: arrival k (k = 0 .. n+2R-1) brings the value at
 // position clamp(k - R, 0, n - 1) (replicate padding, scalespace.py:45-92);
 // output o = k - 2R is complete after arrival k.
-template <int R, class Ld, class St>
-VK_D void ring_line(int n, Ld ld, St st, const Taps& taps) {
+template <int R, class Line>
+VK_D void ring_line(int n, Line& ln, const Taps& taps) {
     constexpr int P = 2 * R + 1;
     float r[P];
 #pragma unroll
     for (int t = 0; t < P; ++t) r[t] = 0.f;
     const int A = n + 2 * R;
-    float pf[2] = {ld(0), ld(1)};
+    float pf[2] = {ln.template at<false>(0, 0), ln.template at<false>(0, 1)};
     int k0 = 0;
-    for (; k0 + P <= A; k0 += P) ring_steps<R, 0, true>(r, k0, P, ld, st, taps, pf);
-    if (k0 < A) ring_steps<R, 0, false>(r, k0, A - k0, ld, st, taps, pf);
+    // a chunk is SAFE when k0 >= 2R and its last prefetch position k0 + P + 1 - R <= n - 1
+    for (; k0 + P <= A; k0 += P) {
+        if (k0 >= 2 * R && k0 + P + 1 - R <= n - 1) ring_steps<R, 0, true, true>(r, k0, P, ln, taps, pf);
+        else ring_steps<R, 0, true, false>(r, k0, P, ln, taps, pf);
+    }
+    if (k0 < A) ring_steps<R, 0, false, false>(r, k0, A - k0, ln, taps, pf);
 }
+
+// x-pass line: a row in shared memory, blurred in place.
+struct RowLine {
+    float* row;
+    int n, R;
+    template <bool SAFE>
+    VK_D float at(int k0, int j) const {
+        return SAFE ? row[k0 - R + j] : row[clampi(k0 + j - R, 0, n - 1)];
+    }
+    VK_D void put(int k0, int j, float v) const { row[k0 + j - 2 * R] = v; }
+};
+
+// y-pass line: a column of the shared plane (stride nx) -> the intermediate.
+struct ColLine {
+    const float* col;
+    float* out;
+    int n, R;
+    unsigned nx;
+    template <bool SAFE>
+    VK_D float at(int k0, int j) const {
+        return SAFE ? col[(unsigned)(k0 - R + j) * nx] : col[(unsigned)clampi(k0 + j - R, 0, n - 1) * nx];
+    }
+    VK_D void put(int k0, int j, float v) const { out[(unsigned)(k0 + j - 2 * R) * nx] = v; }
+};
 
 constexpr int kPlaneThreads = 192;
 
@@ -622,17 +655,13 @@ blur_xy_plane_kernel(const float* __restrict__ src, float* __restrict__ tmp, int
     __syncthreads();  // barrier initialised before anyone waits on it
     mbar_wait(&bar, 0);
     if (tid < ny) {
-        float* row = s + tid * nx;
-        ring_line<R>(
-            nx, [&](int k) { return row[clampi(k - R, 0, nx - 1)]; }, [&](int o, float v) { row[o] = v; }, taps);
+        RowLine ln{s + tid * nx, nx, R};
+        ring_line<R>(nx, ln, taps);
     }
     __syncthreads();
     if (tid < nx) {
-        const float* col = s + tid;
-        float* out = tmp + (size_t)blockIdx.x * plane + tid;
-        ring_line<R>(
-            ny, [&](int k) { return col[clampi(k - R, 0, ny - 1) * nx]; },
-            [&](int o, float v) { out[(unsigned)o * (unsigned)nx] = v; }, taps);
+        ColLine ln{s + tid, tmp + (size_t)blockIdx.x * plane + tid, ny, R, (unsigned)nx};
+        ring_line<R>(ny, ln, taps);
     }
 }
 

@@ -19,6 +19,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--dims", default="145,174,145")
 ap.add_argument("--octaves", type=int, default=6)
+ap.add_argument("--variants", default="1,0")
+ap.add_argument("--reps", type=int, default=7)
 a = ap.parse_args()
 dims = tuple(int(x) for x in a.dims.split(","))
 cfg = vk.PipelineConfig(num_octaves=a.octaves)
@@ -35,7 +37,7 @@ def run(variant):
     ex.enqueue_pyramid(st.cuda_stream)
     torch.cuda.synchronize()
     ts = []
-    for _ in range(7):
+    for _ in range(a.reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
         ex.enqueue_pyramid(st.cuda_stream)
@@ -52,12 +54,13 @@ import json  # noqa: E402
 
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
 res = {}
-for v in (1, 0):
+for v in [int(x) for x in a.variants.split(',')]:
     ms, snap = run(v)
     res[v] = snap
     gbs = pyramid_bytes(ex.plan) * a.batch / (ms / 1e3) / 1e9
     print(f"xy kernel {v}: pyramid {ms:.4f} ms / {a.batch} volumes = {1e3 * ms / a.batch:.1f} us/volume, "
           f"{gbs:.0f} GB/s = {gbs / peak:.3f} of peak", flush=True)
-same = all(torch.equal(x, y) for x, y in zip(res[0], res[1]))
-print("levels + DoG bit-identical between variants:", same)
+if len(res) == 2:
+    same = all(torch.equal(x, y) for x, y in zip(res[0], res[1]))
+    print("levels + DoG bit-identical between variants:", same)
 lib.vk_set_xy_kernel(0)
