@@ -123,10 +123,20 @@ int vk_blur3d(const float* src, float* dst, float* dog_out, float* half_out,
               int nb, int nx, int ny, int nz, const float* taps_host, int radius, void* stream);
 
 /* vk_blur3d with caller-owned scratch for the split (x, y) + z path: work
- * holds work_floats floats (>= nb*nx*ny*nz, else the call allocates its own,
- * stream-ordered). */
+ * holds work_floats floats (>= nb*nz*ny*tp with tp = nx rounded up to a
+ * multiple of 4: the intermediate's rows are pitched; 16-byte aligned; else
+ * the call allocates its own, stream-ordered). */
 int vk_blur3d_ws(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny, int nz,
                  const float* taps_host, int radius, float* work, long long work_floats, void* stream);
+
+/* vk_blur3d_ws that also writes the PREVIOUS pair's difference
+ * prev_dog = prev - src (the DoG level one below dog_out) from the (x, y)
+ * pass's staged copy of src, so each pyramid level is read from HBM by one
+ * kernel only.  prev and prev_dog: both NULL or both volumes of src's shape.
+ * Results are bit-identical to separate vk_difference calls. */
+int vk_blur3d_ws2(const float* src, float* dst, float* dog_out, float* half_out, const float* prev, float* prev_dog,
+                  int nb, int nx, int ny, int nz, const float* taps_host, int radius, float* work,
+                  long long work_floats, void* stream);
 
 /* vk_blur3d with a caller-chosen work granularity: the z pass runs in chunks
  * of `zchunk` output planes per CTA (each chunk re-reads 2R warm-up planes),
@@ -144,6 +154,12 @@ int vk_set_blur_path(int path);
  * (bulk-copy staged plane, thread per row / column; default wherever the
  * plane fits two CTAs per SM), 1 = tiled kernel.  Results are bit-identical. */
 int vk_set_xy_kernel(int k);
+
+/* z-pass kernel selection (A/B; results are bit-identical): 0 = TMA-fed
+ * four-column kernel (default), 1 = register-fed four columns per thread with
+ * packed FFMA2/FADD2 arithmetic, 2 = four columns with scalar sums,
+ * 3 = column-pair kernel. */
+int vk_set_z_kernel(int k);
 
 /* The tail of the pyramid in one launch (scalespace.py:186-251 for octaves
  * whose levels hold <= 16384 voxels): one CTA per volume runs every level of

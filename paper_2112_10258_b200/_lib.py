@@ -37,8 +37,10 @@ SIGNATURES = {
     "vk_transpose_xfast_to_zfast": [P, P, I, I, I, I, P],
     "vk_blur3d": [P, P, P, P, I, I, I, I, P, I, P],
     "vk_blur3d_ws": [P, P, P, P, I, I, I, I, P, I, P, LL, P],
+    "vk_blur3d_ws2": [P, P, P, P, P, P, I, I, I, I, P, I, P, LL, P],
     "vk_set_blur_path": [I],
     "vk_set_xy_kernel": [I],
+    "vk_set_z_kernel": [I],
     "vk_blur3d_chunked": [P, P, I, I, I, I, P, I, I, P],
     "vk_subsample_half": [P, P, I, I, I, I, P],
     "vk_small_octaves": [I, I, I, P, P, P, P, P, I, P],

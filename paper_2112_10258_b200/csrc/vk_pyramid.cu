@@ -16,6 +16,8 @@
 //  * Epilogues on the freshly produced plane: DoG = src - dst (the finer level
 //    minus the coarser one), and the ordered 2x2x2 mean of the handoff level
 //    for the next octave (needs even tile origins and an even z start).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -408,7 +410,8 @@ struct XyGeom {
 
 template <int R, int TY>
 __global__ void __launch_bounds__(kThreads, 4)
-blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, int ny, int nz, Taps taps) {
+blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int tp, int nx, int ny, int nz, Taps taps,
+               const float* __restrict__ prev, float* __restrict__ pdog) {
     using G = XyGeom<R, TY>;
     extern __shared__ float4 smem4[];
     float2* in2 = reinterpret_cast<float2*>(smem4);
@@ -443,6 +446,18 @@ blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, i
         cp_async_wait<0>();
     }
     __syncthreads();
+    if (prev != nullptr) {  // DoG of the previous pair on the tile core: prev - src (staged, intact)
+        const float* inf = reinterpret_cast<const float*>(in2);
+        for (int e = tid; e < kXyTX * TY; e += kThreads) {
+            const int cx = e & (kXyTX - 1), cy = e / kXyTX;
+            const int x = x0 + cx, y = y0 + cy;
+            if (x < nx && y < ny) {
+                const int r = cy + R, col = cx + R;
+                const unsigned gi = pbase + (unsigned)y * (unsigned)nx + (unsigned)x;
+                pdog[gi] = __fsub_rn(__ldg(prev + gi), inf[((r >> 1) * G::COLSP + col) * 2 + (r & 1)]);
+            }
+        }
+    }
     // x-pass: items (row pair, 8-output segment), 2 rows x 8 outputs each
     for (int it = tid; it < G::ITEMS; it += kThreads) {
         const int rp = it >> 2, sg = it & 3;
@@ -494,9 +509,9 @@ blur_xy_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, i
     for (int k = 0; k < YR; ++k) {
         const int gy = y0 + YR * yq + k;
         if (gy < ny) {
-            float* t = tmp + (pbase + (unsigned)gy * (unsigned)nx + (unsigned)gx);
-            if (gx < nx) t[0] = o[k].x;
-            if (gx + 1 < nx) t[1] = o[k].y;
+            float* t = tmp + ((unsigned)bz * (unsigned)tp * (unsigned)ny + (unsigned)gy * (unsigned)tp + (unsigned)gx);
+            if (gx < tp) t[0] = gx < nx ? o[k].x : 0.f;  // pad columns [nx, tp) hold zeros
+            if (gx + 1 < tp) t[1] = gx + 1 < nx ? o[k].y : 0.f;
         }
     }
 }
@@ -596,12 +611,12 @@ struct ColLine {
     const float* col;
     float* out;
     int n, R;
-    unsigned nx;
+    unsigned nx, tp;
     template <bool SAFE>
     VK_D float at(int k0, int j) const {
         return SAFE ? col[(unsigned)(k0 - R + j) * nx] : col[(unsigned)clampi(k0 + j - R, 0, n - 1) * nx];
     }
-    VK_D void put(int k0, int j, float v) const { out[(unsigned)(k0 + j - 2 * R) * nx] = v; }
+    VK_D void put(int k0, int j, float v) const { out[(unsigned)(k0 + j - 2 * R) * tp] = v; }
 };
 
 constexpr int kPlaneThreads = 192;
@@ -636,8 +651,9 @@ VK_D void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) 
 }
 
 template <int R>
-__global__ void __launch_bounds__(kPlaneThreads, 2)
-blur_xy_plane_kernel(const float* __restrict__ src, float* __restrict__ tmp, int nx, int ny, Taps taps) {
+__global__ void __launch_bounds__(kPlaneThreads + 64, 2)
+blur_xy_plane_kernel(const float* __restrict__ src, float* __restrict__ tmp, int tp, int nx, int ny, Taps taps,
+                     const float* __restrict__ prev, float* __restrict__ pdog) {
     extern __shared__ float4 smem4[];
     __shared__ uint64_t bar;
     const int tid = threadIdx.x;
@@ -653,15 +669,52 @@ blur_xy_plane_kernel(const float* __restrict__ src, float* __restrict__ tmp, int
         bulk_g2s(smem4, reinterpret_cast<const void*>(a0), bytes, &bar);
     }
     __syncthreads();  // barrier initialised before anyone waits on it
+    if (tid >= kPlaneThreads) {
+        // two DoG warps (launched only with prev): the previous pair's difference prev - src over the
+        // contiguous plane, read from global (src is L2-hot: the bulk copy just streamed it), concurrent
+        // with the x / y passes of the other six warps
+        const size_t pb = (size_t)blockIdx.x * plane;
+        const int w = tid - kPlaneThreads;
+        constexpr int NW = 64, U = 8;
+        if (((plane & 1) | ((reinterpret_cast<uintptr_t>(prev + pb) | reinterpret_cast<uintptr_t>(pdog + pb) |
+                             reinterpret_cast<uintptr_t>(g)) & 7)) == 0) {
+            const float2* pv2 = reinterpret_cast<const float2*>(prev + pb);
+            const float2* sv2 = reinterpret_cast<const float2*>(g);
+            float2* pd2 = reinterpret_cast<float2*>(pdog + pb);
+            const unsigned n2 = plane / 2;
+            for (unsigned i0 = w; i0 < n2; i0 += NW * U) {
+                float2 a[U], c[U];
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const unsigned i = i0 + j * NW;
+                    if (i < n2) {
+                        a[j] = __ldg(pv2 + i);
+                        c[j] = __ldg(sv2 + i);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const unsigned i = i0 + j * NW;
+                    if (i < n2) pd2[i] = make_float2(__fsub_rn(a[j].x, c[j].x), __fsub_rn(a[j].y, c[j].y));
+                }
+            }
+        } else {
+            for (unsigned i = w; i < plane; i += NW) pdog[pb + i] = __fsub_rn(__ldg(prev + pb + i), __ldg(g + i));
+        }
+        return;
+    }
     mbar_wait(&bar, 0);
     if (tid < ny) {
         RowLine ln{s + tid * nx, nx, R};
         ring_line<R>(nx, ln, taps);
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"n"(kPlaneThreads) : "memory");  // the pass warps only
+    float* out = tmp + (size_t)blockIdx.x * (unsigned)tp * (unsigned)ny + tid;
     if (tid < nx) {
-        ColLine ln{s + tid, tmp + (size_t)blockIdx.x * plane + tid, ny, R, (unsigned)nx};
+        ColLine ln{s + tid, out, ny, R, (unsigned)nx, (unsigned)tp};
         ring_line<R>(ny, ln, taps);
+    } else if (tid < tp) {  // pad columns [nx, tp) of the pitched intermediate hold zeros
+        for (int y = 0; y < ny; ++y) out[(unsigned)y * (unsigned)tp] = 0.f;
     }
 }
 
@@ -671,7 +724,7 @@ blur_xy_plane_kernel(const float* __restrict__ src, float* __restrict__ tmp, int
 // [0, nz) are the clamped border plane (re-read, L1-resident).
 template <int R>
 __global__ void __launch_bounds__(kThreads, 3)
-blur_z_kernel(const float* __restrict__ tmp, const float* __restrict__ src, float* __restrict__ dst,
+blur_z_kernel(const float* __restrict__ tmp, int tp, const float* __restrict__ src, float* __restrict__ dst,
               float* __restrict__ dog, float* __restrict__ half, int nx, int ny, int nz, int tz, int nzc, Taps taps) {
     constexpr int P = 2 * R + 1;
     const int b = blockIdx.z / nzc;
@@ -686,6 +739,9 @@ blur_z_kernel(const float* __restrict__ tmp, const float* __restrict__ src, floa
     const unsigned vbase = (unsigned)b * plane * (unsigned)nz;
     const unsigned e0 = vbase + (unsigned)min(gy, ny - 1) * (unsigned)nx + (unsigned)min(gx, nx - 1);
     const unsigned cst = okx1 ? 1u : 0u;
+    const unsigned tplane = (unsigned)tp * (unsigned)ny;
+    const unsigned t0 = (unsigned)b * tplane * (unsigned)nz + (unsigned)min(gy, ny - 1) * (unsigned)tp +
+                        (unsigned)min(gx, nx - 1);
     float2 r0[P];
 #pragma unroll
     for (int t = 0; t < P; ++t) r0[t] = make_float2(0.f, 0.f);
@@ -695,9 +751,13 @@ blur_z_kernel(const float* __restrict__ tmp, const float* __restrict__ src, floa
         const float* t = base + (e0 + (unsigned)clampi(zp, 0, nz - 1) * plane);
         return make_float2(__ldg(t), __ldg(t + cst));
     };
+    auto ldt = [&](int zp) {
+        const float* t = tmp + (t0 + (unsigned)clampi(zp, 0, nz - 1) * tplane);
+        return make_float2(__ldg(t), __ldg(t + cst));
+    };
     // Two arrivals per step (the arrival count tz + 2R is even); loads run two
     // steps ahead for the intermediate and one step ahead for the DoG source.
-    float2 q0 = ld(tmp, za), q1 = ld(tmp, za + 1), q2 = ld(tmp, za + 2), q3 = ld(tmp, za + 3);
+    float2 q0 = ldt(za), q1 = ldt(za + 1), q2 = ldt(za + 2), q3 = ldt(za + 3);
     const bool want_src = dog != nullptr;
     float2 s0 = want_src ? ld(src, z_start) : make_float2(0.f, 0.f);
     float2 s1 = want_src ? ld(src, z_start + 1) : make_float2(0.f, 0.f);
@@ -738,8 +798,8 @@ blur_z_kernel(const float* __restrict__ tmp, const float* __restrict__ src, floa
         const float2 v0 = q0, v1 = q1;
         q0 = q2;
         q1 = q3;
-        if (zp + 4 <= zb) q2 = ld(tmp, zp + 4);
-        if (zp + 5 <= zb) q3 = ld(tmp, zp + 5);
+        if (zp + 4 <= zb) q2 = ldt(zp + 4);
+        if (zp + 5 <= zb) q3 = ldt(zp + 5);
         const int zo = zp - R;  // outputs zo, zo + 1 (zo and z_start are even)
         const bool out = zo >= z_start;
         const float2 sv0 = s0, sv1 = s1;
@@ -749,6 +809,433 @@ blur_z_kernel(const float* __restrict__ tmp, const float* __restrict__ src, floa
         }
         float2 o0, o1;
         z_dispatch2<R, 0, P>(c, r0, v0, v1, taps, o0, o1);
+        c += 2;
+        if (c >= P) c -= P;
+        if (!out) continue;
+        epilogue(zo, o0, sv0);
+        if (zo + 1 < z_end) epilogue(zo + 1, o1, sv1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// z pass, four columns per thread (default).  The (x, y)-blurred intermediate
+// is PITCHED (row pitch tp = nx rounded up to 4 floats, pad columns zero), so
+// a thread's columns x0..x0+3 (x0 = 4 k) are one aligned 16-byte load per
+// plane.  A warp is 8 such float4 columns x 4 rows: one plane of a warp is
+// 4 x 128 contiguous bytes, and the y partner of the handoff subsample is
+// lane ^ 8.  Same arithmetic as blur_z_kernel (accumulator ring, one rounded
+// product per tap distance, adds in tap order); with PK the products are
+// FFMA2(w, v, -0) and the sums FADD2 -- bit-identical per lane to the scalar
+// fmul / fadd sequence, half the issue slots (the z pass is issue-bound, not
+// FP-pipe bound: loads, addresses and epilogue stores are amortised over four
+// columns as well).
+constexpr int kZ4Threads = 128;
+
+template <bool PK>
+VK_D float2 prodk(const Taps& taps, float w, float2 v) {
+    if constexpr (PK) return __ffma2_rn(make_float2(w, w), v, make_float2(taps.mz, taps.mz));
+    else return __fmul2_rn(make_float2(w, w), v);
+}
+template <bool PK>
+VK_D void acck(float2& a, float2 p) {
+    if constexpr (PK) {
+        a = __fadd2_rn(a, p);
+    } else {
+        a.x = fadd(a.x, p.x);
+        a.y = fadd(a.y, p.y);
+    }
+}
+
+template <int R, int C, bool PK>
+VK_D void z4_arrive(float2 (&r0)[2 * R + 1], float2 (&r1)[2 * R + 1], float4 v, const Taps& taps, float4& o) {
+    constexpr int P = 2 * R + 1;
+    const float2 va = make_float2(v.x, v.y), vb = make_float2(v.z, v.w);
+#pragma unroll
+    for (int d = 0; d <= R; ++d) {
+        const float w = taps.w[R + d];
+        const float2 pa = prodk<PK>(taps, w, va), pb = prodk<PK>(taps, w, vb);
+        if (d == 0) {
+            acck<PK>(r0[C], pa);
+            acck<PK>(r1[C], pb);
+        } else {
+            const int up = (C + d) % P, dn = (C - d + P) % P;
+            if (d == R) {
+                r0[up] = pa;
+                r1[up] = pb;
+            } else {
+                acck<PK>(r0[up], pa);
+                acck<PK>(r1[up], pb);
+            }
+            acck<PK>(r0[dn], pa);
+            acck<PK>(r1[dn], pb);
+        }
+    }
+    constexpr int OUT = (C - R + P) % P;
+    o = make_float4(r0[OUT].x, r0[OUT].y, r1[OUT].x, r1[OUT].y);
+}
+
+template <int R, int LO, int HI, bool PK>
+VK_D void z4_dispatch2(int c, float2 (&r0)[2 * R + 1], float2 (&r1)[2 * R + 1], float4 v0, float4 v1,
+                       const Taps& taps, float4& o0, float4& o1) {
+    if constexpr (HI - LO == 1) {
+        z4_arrive<R, LO, PK>(r0, r1, v0, taps, o0);
+        z4_arrive<R, (LO + 1) % (2 * R + 1), PK>(r0, r1, v1, taps, o1);
+    } else {
+        constexpr int MID = (LO + HI) / 2;
+        if (c < MID) z4_dispatch2<R, LO, MID, PK>(c, r0, r1, v0, v1, taps, o0, o1);
+        else z4_dispatch2<R, MID, HI, PK>(c, r0, r1, v0, v1, taps, o0, o1);
+    }
+}
+
+template <int R>
+constexpr int z4_min_blocks() { return R >= 8 ? 3 : 4; }
+
+template <int R, bool HALF, bool PK>
+__global__ void __launch_bounds__(kZ4Threads, z4_min_blocks<R>())
+blur_z4_kernel(const float* __restrict__ tmp, int tp, const float* __restrict__ src, float* __restrict__ dst,
+               float* __restrict__ dog, float* __restrict__ half, int nx, int ny, int nz, int tz, int nzc, Taps taps) {
+    constexpr int P = 2 * R + 1;
+    const int b = blockIdx.z / nzc;
+    const int zc = blockIdx.z - b * nzc;
+    const int z_start = zc * tz;
+    const int z_end = min(nz, z_start + tz);
+    const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+    const int x0 = 4 * (blockIdx.x * 8 + (lane & 7));
+    const int ry = lane >> 3;  // row within the warp's 4
+    const int gy = blockIdx.y * 16 + 4 * wy + ry;
+    const bool oky = gy < ny;
+    const int nvalid = oky ? max(0, min(4, nx - x0)) : 0;  // stored columns of this thread
+    const unsigned plane = (unsigned)nx * (unsigned)ny;
+    const unsigned tplane = (unsigned)tp * (unsigned)ny;
+    const int yc = min(gy, ny - 1);
+    const unsigned t0 = (unsigned)b * tplane * (unsigned)nz + (unsigned)yc * (unsigned)tp + (unsigned)min(x0, tp - 4);
+    const unsigned e0 = (unsigned)b * plane * (unsigned)nz + (unsigned)yc * (unsigned)nx + (unsigned)min(x0, nx - 1);
+    float2 r0[P], r1[P];
+#pragma unroll
+    for (int t = 0; t < P; ++t) r0[t] = r1[t] = make_float2(0.f, 0.f);
+    const int za = z_start - R, zb = z_end - 1 + R;
+    auto ldt = [&](int zp) {
+        return __ldg(reinterpret_cast<const float4*>(tmp + (t0 + (unsigned)clampi(zp, 0, nz - 1) * tplane)));
+    };
+    const bool want_src = dog != nullptr;
+    auto lds = [&](int zp) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (want_src) {
+            const float* t = src + (e0 + (unsigned)zp * plane);
+            if (nvalid > 0) v.x = __ldg(t);
+            if (nvalid > 1) v.y = __ldg(t + 1);
+            if (nvalid > 2) v.z = __ldg(t + 2);
+            if (nvalid > 3) v.w = __ldg(t + 3);
+        }
+        return v;
+    };
+    float4 q0 = ldt(za), q1 = ldt(za + 1), q2 = ldt(za + 2), q3 = ldt(za + 3);
+    float4 s0 = lds(z_start), s1 = z_start + 1 < z_end ? lds(z_start + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+    int c = 0;
+    auto epilogue = [&](int zo, float4 o, float4 sv) {
+        float* dv = dst + (e0 + (unsigned)zo * plane);
+        if (nvalid > 0) dv[0] = o.x;
+        if (nvalid > 1) dv[1] = o.y;
+        if (nvalid > 2) dv[2] = o.z;
+        if (nvalid > 3) dv[3] = o.w;
+        if (want_src) {
+            float* gv = dog + (e0 + (unsigned)zo * plane);
+            if (nvalid > 0) gv[0] = __fsub_rn(sv.x, o.x);
+            if (nvalid > 1) gv[1] = __fsub_rn(sv.y, o.y);
+            if (nvalid > 2) gv[2] = __fsub_rn(sv.z, o.z);
+            if (nvalid > 3) gv[3] = __fsub_rn(sv.w, o.w);
+        }
+        if constexpr (HALF) {
+            // (dx, dy, dz) order of scalespace.py:129-135 for the column pairs
+            // (x0, x0+1) and (x0+2, x0+3); rows y (even ry) and y+1 (lane ^ 8),
+            // planes zo-1 (pv) and zo (o)
+            float4 qv, qo;
+            qv.x = __shfl_xor_sync(0xffffffffu, pv.x, 8);
+            qv.y = __shfl_xor_sync(0xffffffffu, pv.y, 8);
+            qv.z = __shfl_xor_sync(0xffffffffu, pv.z, 8);
+            qv.w = __shfl_xor_sync(0xffffffffu, pv.w, 8);
+            qo.x = __shfl_xor_sync(0xffffffffu, o.x, 8);
+            qo.y = __shfl_xor_sync(0xffffffffu, o.y, 8);
+            qo.z = __shfl_xor_sync(0xffffffffu, o.z, 8);
+            qo.w = __shfl_xor_sync(0xffffffffu, o.w, 8);
+            const int hnx = nx >> 1, hny = ny >> 1, hnz = nz >> 1;
+            const int hy = gy >> 1, hz = zo >> 1;
+            if ((zo & 1) && !(ry & 1) && hy < hny && hz < hnz) {
+                float* hp = half + (((long long)b * hnz + hz) * hny + hy) * hnx;
+                const int hx = x0 >> 1;
+                if (hx < hnx) {
+                    float sm = pv.x;
+                    sm = fadd(sm, o.x);
+                    sm = fadd(sm, qv.x);
+                    sm = fadd(sm, qo.x);
+                    sm = fadd(sm, pv.y);
+                    sm = fadd(sm, o.y);
+                    sm = fadd(sm, qv.y);
+                    sm = fadd(sm, qo.y);
+                    hp[hx] = fmul(sm, 0.125f);
+                }
+                if (hx + 1 < hnx) {
+                    float sm = pv.z;
+                    sm = fadd(sm, o.z);
+                    sm = fadd(sm, qv.z);
+                    sm = fadd(sm, qo.z);
+                    sm = fadd(sm, pv.w);
+                    sm = fadd(sm, o.w);
+                    sm = fadd(sm, qv.w);
+                    sm = fadd(sm, qo.w);
+                    hp[hx + 1] = fmul(sm, 0.125f);
+                }
+            }
+            pv = o;
+        }
+    };
+    for (int zp = za; zp <= zb; zp += 2) {
+        const float4 v0 = q0, v1 = q1;
+        q0 = q2;
+        q1 = q3;
+        if (zp + 4 <= zb) q2 = ldt(zp + 4);
+        if (zp + 5 <= zb) q3 = ldt(zp + 5);
+        const int zo = zp - R;  // outputs zo, zo + 1 (zo and z_start are even)
+        const bool out = zo >= z_start;
+        const float4 sv0 = s0, sv1 = s1;
+        if (out) {
+            if (zo + 2 < z_end) s0 = lds(zo + 2);
+            if (zo + 3 < z_end) s1 = lds(zo + 3);
+        }
+        float4 o0, o1;
+        z4_dispatch2<R, 0, P, PK>(c, r0, r1, v0, v1, taps, o0, o1);
+        c += 2;
+        if (c >= P) c -= P;
+        if (!out) continue;
+        epilogue(zo, o0, sv0);
+        if (zo + 1 < z_end) epilogue(zo + 1, o1, sv1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// z pass fed by the TMA engine (default).  Same thread layout and arithmetic
+// as blur_z4_kernel (4 columns x 1 row per thread, warp = 8 float4 columns x
+// 4 rows, CTA = 32 x 16 columns x a z-range), but no loads are issued by the
+// math threads: a ring of kZtSlots shared-memory slots, each holding
+//  * the 32 x 16 intermediate tile of one arriving plane, loaded by ONE
+//    cp.async.bulk.tensor.3d (tensor map over the pitched intermediate:
+//    dims (tp, ny, nb * nz); rows >= ny / columns >= tp are zero-filled, z
+//    clamping = the plane coordinate we ask for), and
+//  * the 16 source rows (the DoG minuend) of the output plane that arrival
+//    completes (R planes behind), each a 1-D cp.async.bulk of the 16-byte
+//    aligned superset of the row segment (levels keep the unpitched x-fastest
+//    layout of the API),
+// completing on the slot's mbarrier.  Warp 0 refills the two slots of a step
+// right after every thread has copied them to registers, so kZtSlots - 2
+// planes of loads are always in flight per CTA without holding registers.
+#ifndef VK_ZT_SLOTS
+#define VK_ZT_SLOTS 8
+#endif
+#ifndef VK_ZT_SRC_TMA
+#define VK_ZT_SRC_TMA 0  // 1: DoG source rows staged by 1-D bulk copies (measured slower: ~16 small copies per plane)
+#endif
+constexpr int kZtSlots = VK_ZT_SLOTS;
+constexpr int kZtTmpFloats = 32 * 16;   // tmp tile floats per slot (2 KB)
+constexpr int kZtSrcPitch = 40;         // floats per staged source row (<= 36 used)
+constexpr int kZtSrcFloats = 16 * kZtSrcPitch;
+#ifndef VK_ZT_TSTORE
+#define VK_ZT_TSTORE 0  // 1: warp-transposed row stores (measured slower: 214 vs 126 us at R = 10)
+#endif
+constexpr int kZtSmem = kZtSlots * (kZtTmpFloats + kZtSrcFloats) * 4 + 2 * kZtSlots * 8 + 4 * 128 * 4;
+
+constexpr int kZtThreads = kZ4Threads + 32;  // 4 consumer (math) warps + 1 producer warp
+
+template <int R>
+constexpr int zt_min_blocks() { return 3; }
+
+VK_D void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+
+template <int R, bool HALF>
+__global__ void __launch_bounds__(kZtThreads, zt_min_blocks<R>())
+blur_zt_kernel(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ src, float* __restrict__ dst,
+               float* __restrict__ dog, float* __restrict__ half, int nx, int ny, int nz, int tz, int nzc, Taps taps) {
+    constexpr int P = 2 * R + 1;
+    extern __shared__ __align__(128) float4 zsm4[];
+    float* tmp_s = reinterpret_cast<float*>(zsm4);
+    float* src_s = tmp_s + kZtSlots * kZtTmpFloats;
+    uint64_t* full = reinterpret_cast<uint64_t*>(src_s + kZtSlots * kZtSrcFloats);
+    uint64_t* empty = full + kZtSlots;
+    const int b = blockIdx.z / nzc;
+    const int zc = blockIdx.z - b * nzc;
+    const int z_start = zc * tz;
+    const int z_end = min(nz, z_start + tz);
+    const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+    const int X0 = blockIdx.x * 32, Y0 = blockIdx.y * 16;
+    const unsigned plane = (unsigned)nx * (unsigned)ny;
+    const bool want_src = dog != nullptr;
+    const int A = (z_end - z_start) + 2 * R;  // arrivals
+    const int za = z_start - R;
+    if (tid == 0) {
+        for (int k = 0; k < kZtSlots; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], 4);
+        }
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    }
+    __syncthreads();
+    if (wy == 4) {
+        // producer warp: arrival a = tmp plane za + a and the source rows of output plane za + a - R
+        for (int a = 0; a < A; ++a) {
+            const int k = a % kZtSlots;
+            if (a >= kZtSlots) mbar_wait(&empty[k], (unsigned)(a / kZtSlots - 1) & 1u);
+            const int zp = za + a, zs = zp - R;
+            const bool has_src = VK_ZT_SRC_TMA && want_src && zs >= z_start && zs < z_end;
+            const int y = Y0 + lane;
+            uintptr_t a0 = 0;
+            unsigned sz = 0;
+            if (has_src && lane < 16 && y < ny) {
+                const uintptr_t st =
+                    reinterpret_cast<uintptr_t>(src + ((size_t)(b * nz + zs) * plane + (size_t)y * nx + X0));
+                const uintptr_t en = st + 4u * (unsigned)min(32, nx - X0);
+                a0 = st & ~(uintptr_t)15;
+                sz = (unsigned)(((en + 15) & ~(uintptr_t)15) - a0);
+            }
+            unsigned tot = sz;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+            if (lane == 0) {
+                mbar_expect_tx(&full[k], tot + kZtTmpFloats * 4);
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+                    "%4}], [%5];" ::"r"((unsigned)__cvta_generic_to_shared(tmp_s + k * kZtTmpFloats)),
+                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(X0), "r"(Y0), "r"(b * nz + clampi(zp, 0, nz - 1)),
+                    "r"((unsigned)__cvta_generic_to_shared(&full[k]))
+                    : "memory");
+            }
+            __syncwarp();
+            if (sz)
+                bulk_g2s(src_s + k * kZtSrcFloats + lane * kZtSrcPitch, reinterpret_cast<const void*>(a0), sz,
+                         &full[k]);
+        }
+        return;
+    }
+    const int xl = 4 * (lane & 7), ry = lane >> 3, yl = 4 * wy + ry;
+    const int x0 = X0 + xl, gy = Y0 + yl;
+    const bool oky = gy < ny;
+    const int nvalid = oky ? max(0, min(4, nx - x0)) : 0;
+    const int yc = min(gy, ny - 1);
+    const unsigned e0 = (unsigned)b * plane * (unsigned)nz + (unsigned)yc * (unsigned)nx + (unsigned)min(x0, nx - 1);
+    // this thread's float4 of a tmp tile, and its 4 source values of a staged row
+    auto rd_tmp = [&](int k) { return *reinterpret_cast<const float4*>(tmp_s + k * kZtTmpFloats + yl * 32 + xl); };
+    auto rd_src = [&](int k, int zs) {
+        if (!VK_ZT_SRC_TMA) {
+            const float* t = src + (e0 + (unsigned)zs * plane);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (nvalid > 0) v.x = __ldg(t);
+            if (nvalid > 1) v.y = __ldg(t + 1);
+            if (nvalid > 2) v.z = __ldg(t + 2);
+            if (nvalid > 3) v.w = __ldg(t + 3);
+            return v;
+        }
+        const uintptr_t st =
+            reinterpret_cast<uintptr_t>(src + ((size_t)(b * nz + zs) * plane + (size_t)yc * nx + X0));
+        const float* r = src_s + k * kZtSrcFloats + yl * kZtSrcPitch + (int)((st & 15) >> 2) + xl;
+        return make_float4(r[0], r[1], r[2], r[3]);  // columns >= nvalid are never used
+    };
+    float2 r0[P], r1[P];
+#pragma unroll
+    for (int t = 0; t < P; ++t) r0[t] = r1[t] = make_float2(0.f, 0.f);
+    float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+    int c = 0;
+    // Stores: the warp's 4 rows x 32 columns go through a warp-private shared
+    // transpose so that each store instruction writes 32 consecutive floats of
+    // one row (the per-thread float4 columns of the unpitched level would
+    // touch every sector of 4 rows with 4-byte pieces, 4 instructions each).
+    float* wst = reinterpret_cast<float*>(empty + kZtSlots) + wy * 128;
+    const unsigned rb = (unsigned)b * plane * (unsigned)nz + (unsigned)(Y0 + 4 * wy) * (unsigned)nx + (unsigned)(X0 + lane);
+    const int nrows = min(4, ny - (Y0 + 4 * wy));
+    const bool okc = X0 + lane < nx;
+    auto store_rows = [&](float* base, float4 v) {
+        if (VK_ZT_TSTORE) {
+            *reinterpret_cast<float4*>(wst + ry * 32 + xl) = v;
+            __syncwarp();
+            if (okc)
+                for (int r = 0; r < nrows; ++r) base[rb + (unsigned)r * (unsigned)nx] = wst[r * 32 + lane];
+            __syncwarp();
+        } else {
+            float* t = base + e0;
+            if (nvalid > 0) t[0] = v.x;
+            if (nvalid > 1) t[1] = v.y;
+            if (nvalid > 2) t[2] = v.z;
+            if (nvalid > 3) t[3] = v.w;
+        }
+    };
+    auto epilogue = [&](int zo, float4 o, float4 sv) {
+        store_rows(dst + (size_t)zo * plane, o);
+        if (want_src)
+            store_rows(dog + (size_t)zo * plane,
+                       make_float4(__fsub_rn(sv.x, o.x), __fsub_rn(sv.y, o.y), __fsub_rn(sv.z, o.z), __fsub_rn(sv.w, o.w)));
+        if constexpr (HALF) {
+            float4 qv, qo;
+            qv.x = __shfl_xor_sync(0xffffffffu, pv.x, 8);
+            qv.y = __shfl_xor_sync(0xffffffffu, pv.y, 8);
+            qv.z = __shfl_xor_sync(0xffffffffu, pv.z, 8);
+            qv.w = __shfl_xor_sync(0xffffffffu, pv.w, 8);
+            qo.x = __shfl_xor_sync(0xffffffffu, o.x, 8);
+            qo.y = __shfl_xor_sync(0xffffffffu, o.y, 8);
+            qo.z = __shfl_xor_sync(0xffffffffu, o.z, 8);
+            qo.w = __shfl_xor_sync(0xffffffffu, o.w, 8);
+            const int hnx = nx >> 1, hny = ny >> 1, hnz = nz >> 1;
+            const int hy = gy >> 1, hz = zo >> 1;
+            if ((zo & 1) && !(ry & 1) && hy < hny && hz < hnz) {
+                float* hp = half + (((long long)b * hnz + hz) * hny + hy) * hnx;
+                const int hx = x0 >> 1;
+                if (hx < hnx) {
+                    float sm = pv.x;
+                    sm = fadd(sm, o.x);
+                    sm = fadd(sm, qv.x);
+                    sm = fadd(sm, qo.x);
+                    sm = fadd(sm, pv.y);
+                    sm = fadd(sm, o.y);
+                    sm = fadd(sm, qv.y);
+                    sm = fadd(sm, qo.y);
+                    hp[hx] = fmul(sm, 0.125f);
+                }
+                if (hx + 1 < hnx) {
+                    float sm = pv.z;
+                    sm = fadd(sm, o.z);
+                    sm = fadd(sm, qv.z);
+                    sm = fadd(sm, qo.z);
+                    sm = fadd(sm, pv.w);
+                    sm = fadd(sm, o.w);
+                    sm = fadd(sm, qv.w);
+                    sm = fadd(sm, qo.w);
+                    hp[hx + 1] = fmul(sm, 0.125f);
+                }
+            }
+            pv = o;
+        }
+    };
+    for (int a = 0; a < A; a += 2) {
+        const int k0 = a % kZtSlots, k1 = (a + 1) % kZtSlots;
+        const unsigned ph = (unsigned)(a / kZtSlots) & 1u;  // a even, kZtSlots even: a and a+1 share the use count
+        const int zo = za + a - R;                          // outputs zo, zo + 1 complete in this step
+        const bool out = zo >= z_start;
+        mbar_wait(&full[k0], ph);
+        const float4 v0 = rd_tmp(k0);
+        const float4 sv0 = (out && want_src) ? rd_src(k0, zo) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 v1 = make_float4(0.f, 0.f, 0.f, 0.f), sv1 = v1;
+        const bool two = a + 1 < A;
+        if (two) {
+            mbar_wait(&full[k1], ph);
+            v1 = rd_tmp(k1);
+            if (out && want_src && zo + 1 < z_end) sv1 = rd_src(k1, zo + 1);
+        }
+        __syncwarp();
+        if (lane == 0) {  // this warp is done with both slots
+            mbar_arrive(&empty[k0]);
+            if (two) mbar_arrive(&empty[k1]);
+        }
+        float4 o0, o1;
+        z4_dispatch2<R, 0, P, true>(c, r0, r1, v0, v1, taps, o0, o1);
         c += 2;
         if (c >= P) c -= P;
         if (!out) continue;
@@ -984,7 +1471,8 @@ static int launch_ring(const float* src, float* dst, float* dog, float* half, in
 static int kZWaves = 1, kZMinChunkR = 12;  // z chunking: long chunks measured best in the multi-stream bench -- the 2R warm-up
                                           // arrivals per chunk cost more than the lost parallelism (env-overridable)
 template <int R, int TY>
-static int launch_xy(const float* src, float* work, int nb, int nx, int ny, int nz, const Taps& taps, cudaStream_t st) {
+static int launch_xy(const float* src, float* work, int tp, int nb, int nx, int ny, int nz, const Taps& taps,
+                     cudaStream_t st, const float* prev, float* pdog) {
     using G = XyGeom<R, TY>;
     static bool configured = false;
     if (!configured) {
@@ -993,7 +1481,7 @@ static int launch_xy(const float* src, float* work, int nb, int nx, int ny, int 
         configured = true;
     }
     dim3 g1((nx + kXyTX - 1) / kXyTX, (ny + TY - 1) / TY, nb * nz);
-    blur_xy_kernel<R, TY><<<g1, kThreads, G::SMEM, st>>>(src, work, nx, ny, nz, taps);
+    blur_xy_kernel<R, TY><<<g1, kThreads, G::SMEM, st>>>(src, work, tp, nx, ny, nz, taps, prev, pdog);
     count_launch();
     return cuda_status(cudaGetLastError(), "blur xy launch");
 }
@@ -1005,8 +1493,8 @@ static bool plane_kernel_fits(int nx, int ny) {
 }
 
 template <int R>
-static int launch_xy_plane(const float* src, float* work, int nb, int nx, int ny, int nz, const Taps& taps,
-                           cudaStream_t st) {
+static int launch_xy_plane(const float* src, float* work, int tp, int nb, int nx, int ny, int nz, const Taps& taps,
+                           cudaStream_t st, const float* prev, float* pdog) {
     const int smem = nx * ny * 4 + 32;
     static int configured = 0;
     if (configured < smem) {
@@ -1015,36 +1503,138 @@ static int launch_xy_plane(const float* src, float* work, int nb, int nx, int ny
         if (e != cudaSuccess) return cuda_status(e, "blur xy plane attribute");
         configured = 110 * 1024;
     }
-    blur_xy_plane_kernel<R><<<nb * nz, kPlaneThreads, smem, st>>>(src, work, nx, ny, taps);
+    blur_xy_plane_kernel<R><<<nb * nz, kPlaneThreads + (prev ? 64 : 0), smem, st>>>(src, work, tp, nx, ny, taps, prev,
+                                                                                  pdog);
     count_launch();
     return cuda_status(cudaGetLastError(), "blur xy plane launch");
 }
 
 static int g_xy_kernel = 0;  // 0: whole-plane ring kernel where it fits, 1: tile kernel (A/B)
+static int g_z_kernel = 0;  // 0: TMA-fed four-column kernel, 1: register-fed four-column kernel (packed sums),
+                            // 2: four-column scalar sums, 3: column-pair kernel
+static int kZ4Waves = 2, kZ4MinChunkR = 6;
+
+template <int R, bool HALF, bool PK>
+static void launch_z4(const float* work, int tp, const float* src, float* dst, float* dog, float* half, int nb,
+                      int nx, int ny, int nz, const Taps& taps, cudaStream_t st, int zchunk, int sms) {
+    const long long ctas = (long long)((tp + 31) / 32) * ((ny + 15) / 16) * nb;
+    const long long slots = (long long)sms * z4_min_blocks<R>();
+    int nzc = 1;
+    while (ctas * nzc < (long long)kZ4Waves * slots && (nz + nzc) / (nzc + 1) >= kZ4MinChunkR * R && nzc < 64) ++nzc;
+    if (zchunk > 0) nzc = (nz + zchunk - 1) / zchunk;  // caller-chosen granularity (convolve_separable's chunk)
+    int tz = (nz + nzc - 1) / nzc;
+    tz += tz & 1;
+    nzc = (nz + tz - 1) / tz;
+    dim3 g((tp + 31) / 32, (ny + 15) / 16, nb * nzc);
+    blur_z4_kernel<R, HALF, PK><<<g, kZ4Threads, 0, st>>>(work, tp, src, dst, dog, half, nx, ny, nz, tz, nzc, taps);
+    count_launch();
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static int g_encode_state = 0;  // 0 unknown, 1 available, -1 unavailable
+
+static bool get_encode() {
+    if (g_encode_state == 0) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess && fn) {
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+            g_encode_state = 1;
+        } else {
+            g_encode_state = -1;
+        }
+    }
+    return g_encode_state == 1;
+}
+
+// Tensor map over the pitched intermediate (tp, ny, nb * nz), box 32 x 16 x 1.
+static bool encode_tmp_map(CUtensorMap* m, const float* work, int tp, int ny, long long planes) {
+    if (!get_encode() || (tp & 3) || (reinterpret_cast<uintptr_t>(work) & 15)) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)tp, (cuuint64_t)ny, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)tp * 4, (cuuint64_t)tp * ny * 4};
+    cuuint32_t box[3] = {32, 16, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(work), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int kZtWaves = 2, kZtMinChunkR = 6;
+
+template <int R, bool HALF>
+static bool launch_zt(const float* work, int tp, const float* src, float* dst, float* dog, float* half, int nb,
+                      int nx, int ny, int nz, const Taps& taps, cudaStream_t st, int zchunk, int sms) {
+    CUtensorMap m;
+    if (!encode_tmp_map(&m, work, tp, ny, (long long)nb * nz)) return false;
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(blur_zt_kernel<R, HALF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kZtSmem) !=
+            cudaSuccess)
+            return false;
+        configured = true;
+    }
+    const long long ctas = (long long)((tp + 31) / 32) * ((ny + 15) / 16) * nb;
+    const long long slots = (long long)sms * zt_min_blocks<R>();
+    int nzc = 1;
+    while (ctas * nzc < (long long)kZtWaves * slots && (nz + nzc) / (nzc + 1) >= kZtMinChunkR * R && nzc < 64) ++nzc;
+    if (zchunk > 0) nzc = (nz + zchunk - 1) / zchunk;
+    int tz = (nz + nzc - 1) / nzc;
+    tz += tz & 1;
+    nzc = (nz + tz - 1) / tz;
+    dim3 g((tp + 31) / 32, (ny + 15) / 16, nb * nzc);
+    blur_zt_kernel<R, HALF><<<g, kZtThreads, kZtSmem, st>>>(m, src, dst, dog, half, nx, ny, nz, tz, nzc, taps);
+    count_launch();
+    return true;
+}
 
 template <int R>
 static int launch_split(const float* src, float* dst, float* dog, float* half, int nb, int nx, int ny, int nz,
-                        const Taps& taps, float* work, cudaStream_t st, int zchunk) {
+                        const Taps& taps, float* work, int tp, cudaStream_t st, int zchunk, const float* prev,
+                        float* pdog) {
     static bool env_read = false;
     if (!env_read) {
         if (const char* e = getenv("VK_Z_WAVES")) kZWaves = atoi(e) > 0 ? atoi(e) : kZWaves;
         if (const char* e = getenv("VK_Z_MINCHUNK")) kZMinChunkR = atoi(e) > 0 ? atoi(e) : kZMinChunkR;
+        if (const char* e = getenv("VK_Z4_WAVES")) kZ4Waves = atoi(e) > 0 ? atoi(e) : kZ4Waves;
+        if (const char* e = getenv("VK_Z4_MINCHUNK")) kZ4MinChunkR = atoi(e) > 0 ? atoi(e) : kZ4MinChunkR;
+        if (const char* e = getenv("VK_Z_KERNEL")) g_z_kernel = atoi(e);
+        if (const char* e = getenv("VK_ZT_WAVES")) kZtWaves = atoi(e) > 0 ? atoi(e) : kZtWaves;
+        if (const char* e = getenv("VK_ZT_MINCHUNK")) kZtMinChunkR = atoi(e) > 0 ? atoi(e) : kZtMinChunkR;
         env_read = true;
     }
     // taller tiles (less x-pass halo, fewer y-pass loads) unless they waste rows
     const bool tall = ((ny + 95) / 96) * 96 <= ((ny + 63) / 64) * 64;
     // 97..176 rows: one tile spans the whole y extent (no recomputed x-pass halo rows between y tiles;
     // measured 3.6% faster pyramid on 145x174x145 despite 2 CTAs/SM instead of 4)
-    const int rc1 = g_xy_kernel == 0 && plane_kernel_fits(nx, ny) ? launch_xy_plane<R>(src, work, nb, nx, ny, nz, taps, st)
-                    : ny <= 176 && ny > 96 ? launch_xy<R, 176>(src, work, nb, nx, ny, nz, taps, st)
-                    : tall               ? launch_xy<R, 96>(src, work, nb, nx, ny, nz, taps, st)
-                                         : launch_xy<R, 64>(src, work, nb, nx, ny, nz, taps, st);
+    const int rc1 = g_xy_kernel == 0 && plane_kernel_fits(nx, ny)
+                        ? launch_xy_plane<R>(src, work, tp, nb, nx, ny, nz, taps, st, prev, pdog)
+                    : ny <= 176 && ny > 96 ? launch_xy<R, 176>(src, work, tp, nb, nx, ny, nz, taps, st, prev, pdog)
+                    : tall               ? launch_xy<R, 96>(src, work, tp, nb, nx, ny, nz, taps, st, prev, pdog)
+                                         : launch_xy<R, 64>(src, work, tp, nb, nx, ny, nz, taps, st, prev, pdog);
     if (rc1 != VK_OK) return rc1;
-    // z chunks: enough CTAs for ~4 waves, each chunk >= 4R planes (the 2R
-    // warm-up arrivals are overhead), even starts for the subsample epilogue
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_z_kernel == 0) {
+        const bool ok = half ? launch_zt<R, true>(work, tp, src, dst, dog, half, nb, nx, ny, nz, taps, st, zchunk, sms)
+                             : launch_zt<R, false>(work, tp, src, dst, dog, half, nb, nx, ny, nz, taps, st, zchunk, sms);
+        if (ok) return cuda_status(cudaGetLastError(), "blur zt launch");
+        // no tensor-map support: the register-fed four-column kernel
+    }
+    if (g_z_kernel != 3) {
+        const bool pk = g_z_kernel != 2;
+        if (half) {
+            if (pk) launch_z4<R, true, true>(work, tp, src, dst, dog, half, nb, nx, ny, nz, taps, st, zchunk, sms);
+            else launch_z4<R, true, false>(work, tp, src, dst, dog, half, nb, nx, ny, nz, taps, st, zchunk, sms);
+        } else {
+            if (pk) launch_z4<R, false, true>(work, tp, src, dst, dog, half, nb, nx, ny, nz, taps, st, zchunk, sms);
+            else launch_z4<R, false, false>(work, tp, src, dst, dog, half, nb, nx, ny, nz, taps, st, zchunk, sms);
+        }
+        return cuda_status(cudaGetLastError(), "blur z4 launch");
+    }
+    // z chunks: enough CTAs for ~4 waves, each chunk >= 4R planes (the 2R
+    // warm-up arrivals are overhead), even starts for the subsample epilogue
     const long long cols = (long long)((nx + 31) / 32) * ((ny + 15) / 16) * nb;
     int nzc = 1;
     while (cols * nzc < (long long)kZWaves * 8 * sms && (nz + nzc) / (nzc + 1) >= kZMinChunkR * R && nzc < 64) ++nzc;
@@ -1053,7 +1643,7 @@ static int launch_split(const float* src, float* dst, float* dog, float* half, i
     tz += tz & 1;
     nzc = (nz + tz - 1) / tz;
     dim3 g2((nx + 31) / 32, (ny + 15) / 16, nb * nzc);
-    blur_z_kernel<R><<<g2, kThreads, 0, st>>>(work, src, dst, dog, half, nx, ny, nz, tz, nzc, taps);
+    blur_z_kernel<R><<<g2, kThreads, 0, st>>>(work, tp, src, dst, dog, half, nx, ny, nz, tz, nzc, taps);
     count_launch();
     return cuda_status(cudaGetLastError(), "blur split launch");
 }
@@ -1112,14 +1702,36 @@ extern "C" int vk_set_xy_kernel(int k) {
     return VK_OK;
 }
 
+extern "C" int vk_set_z_kernel(int k) {
+    if (k < 0 || k > 3) {
+        set_error("vk_set_z_kernel: 0 (TMA-fed), 1 (four-column, packed sums), 2 (four-column, scalar sums) or "
+                  "3 (column pair)");
+        return VK_ERR_PARAMETER;
+    }
+    g_z_kernel = k;
+    return VK_OK;
+}
+
 static int blur3d_impl(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny, int nz,
                        const float* taps_host, int radius, float* work, long long work_floats, int zchunk,
-                       void* stream);
+                       void* stream, const float* prev = nullptr, float* prev_dog = nullptr);
+extern "C" int vk_difference(const float* a, const float* b, float* out, long long n, void* stream);
 
 extern "C" int vk_blur3d_ws(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny,
                             int nz, const float* taps_host, int radius, float* work, long long work_floats,
                             void* stream) {
     return blur3d_impl(src, dst, dog_out, half_out, nb, nx, ny, nz, taps_host, radius, work, work_floats, 0, stream);
+}
+
+extern "C" int vk_blur3d_ws2(const float* src, float* dst, float* dog_out, float* half_out, const float* prev,
+                             float* prev_dog, int nb, int nx, int ny, int nz, const float* taps_host, int radius,
+                             float* work, long long work_floats, void* stream) {
+    if ((prev == nullptr) != (prev_dog == nullptr)) {
+        set_error("vk_blur3d_ws2: prev and prev_dog must both be given or both be NULL");
+        return VK_ERR_PARAMETER;
+    }
+    return blur3d_impl(src, dst, dog_out, half_out, nb, nx, ny, nz, taps_host, radius, work, work_floats, 0, stream,
+                       prev, prev_dog);
 }
 
 extern "C" int vk_blur3d_chunked(const float* src, float* dst, int nb, int nx, int ny, int nz, const float* taps_host,
@@ -1133,7 +1745,7 @@ extern "C" int vk_blur3d_chunked(const float* src, float* dst, int nb, int nx, i
 
 static int blur3d_impl(const float* src, float* dst, float* dog_out, float* half_out, int nb, int nx, int ny, int nz,
                        const float* taps_host, int radius, float* work, long long work_floats, int zchunk,
-                       void* stream) {
+                       void* stream, const float* prev, float* prev_dog) {
     if (!src || !dst || !taps_host || nb < 0 || nx < 1 || ny < 1 || nz < 1 || radius < 1 ||
         2 * radius + 1 > VK_MAX_TAPS || work_floats < 0) {
         set_error("vk_blur3d: bad arguments (nb=%d dims=%d,%d,%d radius=%d)", nb, nx, ny, nz, radius);
@@ -1152,27 +1764,39 @@ static int blur3d_impl(const float* src, float* dst, float* dog_out, float* half
     // ... and address the batch with 32-bit element offsets.
     const long long total = (long long)nb * nx * ny * nz;
     const bool small = (unsigned long long)total < (1ull << 32);
+    // the (x, y) intermediate of the split path is pitched: rows of tp = nx rounded up to 4 floats
+    const int tp = (nx + 3) & ~3;
+    const long long wtotal = (long long)nb * tp * ny * nz;
+    const bool split = g_blur_path == 0 && symmetric && small && radius <= kMaxRingR &&
+                       (unsigned long long)wtotal < (1ull << 32);
+    if (prev && !split) {  // only the split path's (x, y) kernels fuse the previous pair's DoG
+        const int rc = vk_difference(prev, src, prev_dog, total, stream);
+        if (rc != VK_OK) return rc;
+        prev = nullptr;
+        prev_dog = nullptr;
+    }
     if (!symmetric || !small || radius > kMaxRingR)
         return launch_generic(src, dst, dog_out, half_out, nb, nx, ny, nz, radius, taps, st);
     if (g_blur_path == 0) {
+        if (!split) return launch_generic(src, dst, dog_out, half_out, nb, nx, ny, nz, radius, taps, st);
         float* w = work;
-        const bool own = w == nullptr || work_floats < total;
+        const bool own = w == nullptr || work_floats < wtotal || (reinterpret_cast<uintptr_t>(w) & 15) != 0;
         if (own) {
-            cudaError_t e = cudaMallocAsync(&w, total * 4, st);
+            cudaError_t e = cudaMallocAsync(&w, wtotal * 4, st);
             if (e != cudaSuccess) return cuda_status(e, "blur scratch");
         }
         int rc;
         switch (radius) {
-            case 1: rc = launch_split<1>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
-            case 2: rc = launch_split<2>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
-            case 3: rc = launch_split<3>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
-            case 4: rc = launch_split<4>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
-            case 5: rc = launch_split<5>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
-            case 6: rc = launch_split<6>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
-            case 7: rc = launch_split<7>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
-            case 8: rc = launch_split<8>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
-            case 9: rc = launch_split<9>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
-            default: rc = launch_split<10>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, st, zchunk); break;
+            case 1: rc = launch_split<1>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
+            case 2: rc = launch_split<2>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
+            case 3: rc = launch_split<3>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
+            case 4: rc = launch_split<4>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
+            case 5: rc = launch_split<5>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
+            case 6: rc = launch_split<6>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
+            case 7: rc = launch_split<7>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
+            case 8: rc = launch_split<8>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
+            case 9: rc = launch_split<9>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
+            default: rc = launch_split<10>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
         }
         if (own) cudaFreeAsync(w, st);
         return rc;

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import math
 from contextlib import nullcontext
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -180,7 +181,8 @@ class Extractor:
         else:
             self.input = t.empty((B, nz, ny, nx), dtype=f32, device="cuda")
         # (x, y)-blurred intermediate of the split blur (vk_blur3d_ws), one octave-0 level
-        self.blur_work = t.empty(B * nx * ny * nz, dtype=f32, device="cuda")
+        # with rows pitched to a multiple of 4 floats (16-byte aligned rows for the z pass)
+        self.blur_work = t.empty(B * ((nx + 3) // 4 * 4) * ny * nz, dtype=f32, device="cuda")
         self.levels, self.dogs = [], []
         for (ox, oy, oz) in self.plan.octave_dims:
             self.levels.append([t.empty((B, oz, oy, ox), dtype=f32, device="cuda") for _ in range(L)])
@@ -253,6 +255,10 @@ class Extractor:
             self.desc = t.empty((self.frame_cap, (self.cfg.pairs + 7) // 8), dtype=t.uint8, device="cuda")
         else:
             self.desc = t.empty((self.frame_cap, self.cfg.pairs), dtype=t.int16, device="cuda")
+        # volumes per pyramid chunk (enqueue_pyramid); env override for A/B runs
+        self.pyr_chunk = int(os.environ.get("VK_PYR_CHUNK", "0")) or self.B
+        # DoG of level pair (i-2, i-1) inside level i's (x, y) kernel (1) or in each level's z pass (0)
+        self.dog_in_xy = os.environ.get("VK_DOG_IN_XY", "1") == "1"
         self.graph = None
 
     # ------------------------------------------------------------ pipeline
@@ -262,30 +268,47 @@ class Extractor:
         rec = rec or _no_stage
         handoff = L - 3
         small = self.small_from if with_dog else P.n_octaves
-        for o, (nx, ny, nz) in enumerate(P.octave_dims):
-            if o >= small:
-                break
-            lv, dg = self.levels[o], self.dogs[o]
-            if o == 0:
-                k = P.taps[0]
-                with rec("convolution", o, 0):
-                    _lib.call("vk_blur3d_ws", self.input.data_ptr(), lv[0].data_ptr(), None, None, B, nx, ny, nz,
-                              k.weights.ctypes.data, k.radius, self.blur_work.data_ptr(), self.blur_work.numel(), s)
-            for i in range(1, L):
-                k = P.taps[i]
-                half = self.levels[o + 1][0].data_ptr() if (i == handoff and o + 1 < P.n_octaves) else None
-                with rec("convolution", o, i):
-                    _lib.call("vk_blur3d_ws", lv[i - 1].data_ptr(), lv[i].data_ptr(),
-                              dg[i - 1].data_ptr() if with_dog else None, half, B, nx, ny, nz,
-                              k.weights.ctypes.data, k.radius, self.blur_work.data_ptr(), self.blur_work.numel(), s)
-                # DoG and the handoff subsample are epilogues of that blur launch: their stage
-                # rows (bench.py STAGES) carry only what is left outside it, i.e. ~0
-                if with_dog:
-                    with rec("dog", o, i - 1):
-                        pass
-                if half is not None:
-                    with rec("subsample", o, i):
-                        pass
+        # Volume chunks: every level of a chunk is produced before the next chunk starts, so
+        # the level just written (the next blur's source, the DoG minuend) and the (x, y)
+        # intermediate are still L2-resident when they are read again.
+        ch = max(1, min(B, self.pyr_chunk))
+        for c0 in range(0, B, ch):
+            nb = min(ch, B - c0)
+            for o, (nx, ny, nz) in enumerate(P.octave_dims):
+                if o >= small:
+                    break
+                off = c0 * nx * ny * nz * 4
+                lv, dg = self.levels[o], self.dogs[o]
+                if o == 0:
+                    k = P.taps[0]
+                    with rec("convolution", o, 0):
+                        _lib.call("vk_blur3d_ws", self.input.data_ptr() + off, lv[0].data_ptr() + off, None, None,
+                                  nb, nx, ny, nz, k.weights.ctypes.data, k.radius, self.blur_work.data_ptr(),
+                                  self.blur_work.numel(), s)
+                for i in range(1, L):
+                    k = P.taps[i]
+                    half = None
+                    if i == handoff and o + 1 < P.n_octaves:
+                        hx, hy, hz = P.octave_dims[o + 1]
+                        half = self.levels[o + 1][0].data_ptr() + c0 * hx * hy * hz * 4
+                    # DoG_{i-2} = L_{i-2} - L_{i-1} is written by this level's (x, y) kernel from its staged
+                    # source; only the last pair's DoG (L_{L-2} - L_{L-1}) comes from the z pass
+                    fuse = self.dog_in_xy
+                    dog_out = dg[i - 1].data_ptr() + off if (with_dog and (i == L - 1 or not fuse)) else None
+                    prev = lv[i - 2].data_ptr() + off if (with_dog and fuse and i >= 2) else None
+                    prev_dog = dg[i - 2].data_ptr() + off if (with_dog and fuse and i >= 2) else None
+                    with rec("convolution", o, i):
+                        _lib.call("vk_blur3d_ws2", lv[i - 1].data_ptr() + off, lv[i].data_ptr() + off, dog_out, half,
+                                  prev, prev_dog, nb, nx, ny, nz, k.weights.ctypes.data, k.radius,
+                                  self.blur_work.data_ptr(), self.blur_work.numel(), s)
+                    # DoG and the handoff subsample are epilogues of the blur launches: their stage
+                    # rows (bench.py STAGES) carry only what is left outside them, i.e. ~0
+                    if with_dog:
+                        with rec("dog", o, i - 1):
+                            pass
+                    if half is not None:
+                        with rec("subsample", o, i):
+                            pass
         if small < P.n_octaves:
             import ctypes as C
 

@@ -19,7 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--dims", default="145,174,145")
 ap.add_argument("--octaves", type=int, default=6)
-ap.add_argument("--variants", default="1,0")
+ap.add_argument("--variants", default="0:1,0:0")  # xy kernel : z kernel
 ap.add_argument("--reps", type=int, default=7)
 a = ap.parse_args()
 dims = tuple(int(x) for x in a.dims.split(","))
@@ -33,7 +33,9 @@ lib = _lib.load()
 
 
 def run(variant):
-    lib.vk_set_xy_kernel(variant)
+    xy, z = (int(v) for v in variant.split(":"))
+    lib.vk_set_xy_kernel(xy)
+    lib.vk_set_z_kernel(z)
     ex.enqueue_pyramid(st.cuda_stream)
     torch.cuda.synchronize()
     ts = []
@@ -54,13 +56,15 @@ import json  # noqa: E402
 
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
 res = {}
-for v in [int(x) for x in a.variants.split(',')]:
+for v in a.variants.split(','):
     ms, snap = run(v)
     res[v] = snap
     gbs = pyramid_bytes(ex.plan) * a.batch / (ms / 1e3) / 1e9
-    print(f"xy kernel {v}: pyramid {ms:.4f} ms / {a.batch} volumes = {1e3 * ms / a.batch:.1f} us/volume, "
+    print(f"xy:z kernels {v}: pyramid {ms:.4f} ms / {a.batch} volumes = {1e3 * ms / a.batch:.1f} us/volume, "
           f"{gbs:.0f} GB/s = {gbs / peak:.3f} of peak", flush=True)
-if len(res) == 2:
-    same = all(torch.equal(x, y) for x, y in zip(res[0], res[1]))
-    print("levels + DoG bit-identical between variants:", same)
+keys = list(res)
+for k in keys[1:]:
+    same = all(torch.equal(x, y) for x, y in zip(res[keys[0]], res[k]))
+    print(f"levels + DoG bit-identical {keys[0]} vs {k}:", same)
 lib.vk_set_xy_kernel(0)
+lib.vk_set_z_kernel(0)
