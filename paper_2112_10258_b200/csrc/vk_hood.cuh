@@ -39,11 +39,11 @@ constexpr int kAccumCtasPerSm = VK_ACCUM_CTAS_PER_SM;
 // occupancy the kernel's registers allow, at most kAccumCtasPerSm per SM), so
 // no CTA waits for a second wave with its share of the items.
 template <class Kernel>
-inline int accum_grid(Kernel kernel, int threads, int n_items) {
+inline int accum_grid(Kernel kernel, int threads, int n_items, size_t dyn_smem = 0) {
     int dev = 0, sms = 148, occ = kAccumCtasPerSm;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ < 1) occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, dyn_smem) != cudaSuccess || occ < 1) occ = 1;
     const int g = sms * (occ < kAccumCtasPerSm ? occ : kAccumCtasPerSm);
     return n_items < g ? n_items : g;
 }

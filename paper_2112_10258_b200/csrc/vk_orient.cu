@@ -18,6 +18,7 @@
 // order with fp64 votes (ori_exact_subset).  Either way the frames are the
 // reference's.
 #include "vk_hood.cuh"
+#include "vk_stage.cuh"
 
 namespace vk {
 
@@ -27,6 +28,11 @@ namespace vk {
 constexpr int kOriThreads = VK_ORI_THREADS;
 #ifndef VK_ORI_PREFETCH
 #define VK_ORI_PREFETCH 0  // z-plane lead of an L1 prefetch in the ball walk (0: none)
+#endif
+
+#ifndef VK_ORI_STAGED
+#define VK_ORI_STAGED 0  // 1: interior balls walked from plane-staged shared memory (vk_stage.cuh); measured
+                         // slower on B200 (2.20 vs 2.13 ms / 8 volumes: +23% instructions, barrier stalls)
 #endif
 
 constexpr int kOriQueue = 64;  // per-warp deferred entries of the fast walk (flush at >= 32)
@@ -364,6 +370,62 @@ VK_D int ori_walk(const vk_kp& kp, const vk_level& L, const float* data, const v
     return inside_cnt;
 }
 
+// ori_walk<true> over the plane-staged ball (vk_stage.cuh): the same votes,
+// bins and deferred queue, neighbours from shared memory.  Returns the ball
+// size on thread 0 (every voxel of an interior ball is inside).
+VK_D int ori_walk_staged(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
+                         const int* __restrict__ ball_offsets, const float* __restrict__ win32, const double* dirs,
+                         const IcoSh* icp, const uint8_t* lut, double* hist, int2* queue, float* ring) {
+    const int lane = threadIdx.x & 31;
+    hist = vote_copy(hist);
+    const unsigned plane = (unsigned)L.nx * (unsigned)L.ny;
+    auto resolve = [&](int2 e) {
+        const unsigned c = (unsigned)e.x;
+        const int z = (int)(c / plane), rem = (int)(c - (unsigned)z * plane);
+        const int y = rem / L.nx, x = rem - y * L.nx;
+        const Nb6 nb = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
+        float gx, gy, gz;
+        grad32(nb, gx, gy, gz);
+        red_vote(hist, nearest_dir_ico(dirs, *icp, nullptr, gx, gy, gz, nb), __int_as_float(e.y));
+    };
+    int qn = 0;  // warp-uniform queue fill
+    const unsigned cc = ((unsigned)kp.iz * (unsigned)L.ny + (unsigned)kp.iy) * (unsigned)L.nx + (unsigned)kp.ix;
+    staged_ball_walk(data, L.nx, L.ny, kp, ball, ball_offsets + ball.zstart, ball_offsets + ball.pstart, ring,
+                     [&](bool valid, int ox, int oy, int oz, const Nb6& nb) {
+        int bin = -1;
+        float vote = 0.f;
+        bool miss = false;
+        if (valid && grad_nonzero(nb)) {
+            float gx, gy, gz;
+            grad32(nb, gx, gy, gz);
+            vote = nz_vote(fmul(norm3_f32(gx, gy, gz), __ldg(win32 + (ox * ox + oy * oy + oz * oz))));
+            bin = nearest_dir_lut(lut, gx, gy, gz, fabsf(gx), fabsf(gy), fabsf(gz));
+            miss = bin < 0;
+        }
+        red_vote(hist, bin, vote);
+        const unsigned mm = __ballot_sync(0xffffffffu, miss);
+        if (mm) {
+            if (miss) {
+                const unsigned c = cc + (unsigned)(oz * (int)plane + oy * L.nx + ox);
+                queue[qn + __popc(mm & ((1u << lane) - 1u))] = make_int2((int)c, __float_as_int(vote));
+            }
+            qn += __popc(mm);
+            if (qn >= 32) {
+                __syncwarp();
+                resolve(queue[qn - 32 + lane]);
+                qn -= 32;
+                __syncwarp();
+            }
+        }
+    });
+    if (qn > 0) {
+        __syncwarp();
+        if (lane < qn) resolve(queue[lane]);
+        __syncwarp();
+    }
+    return threadIdx.x == 0 ? ball.count : 0;
+}
+
 // Dense per-voxel gradient data for a batched level: (gx, gy, gz, |g|) with
 // |g| evaluated in fp64 (no fp32 underflow for tiny nonzero gradients) and
 // rounded once, plus the exact nearest icosphere direction (255 for g == 0).
@@ -685,6 +747,9 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
     __shared__ OriShared sh;
     __shared__ IcoSh ic;
     __shared__ __align__(16) uint8_t lut[kLutBytes];
+#if VK_ORI_STAGED
+    extern __shared__ __align__(16) float ring[];  // kStageFloats (dynamic: the static part is ~34 KB)
+#endif
     double* hist = work + (long long)blockIdx.x * kAccumSlot;  // [K] fp64, L2-resident
     const int tid = threadIdx.x;
     for (int i = tid; i < 3 * K; i += kOriThreads) sh.dirs[i] = dirs_g[i];
@@ -748,6 +813,12 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
                 }
                 red_vote(vote_copy(hist), bin, vote);
             }
+        } else if (!exact_only && VK_ORI_STAGED && lutp && ball.r <= kStageMaxR &&
+                   ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz)) {
+#if VK_ORI_STAGED
+            inside_cnt = ori_walk_staged(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, hist,
+                                         sh.queue[tid >> 5], ring);
+#endif
         } else if (!exact_only) {
             inside_cnt = ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz)
                              ? ori_walk<true>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, K, hist,
@@ -955,7 +1026,14 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
         return VK_ERR_PARAMETER;
     }
     if (n_kp_max == 0) return VK_OK;
-    const int grid = accum_grid(orient_kernel, kOriThreads, n_kp_max);
+    const size_t dyn = VK_ORI_STAGED ? kStageFloats * sizeof(float) : 0;
+    static bool configured = false;
+    if (dyn && !configured) {
+        cudaError_t e = cudaFuncSetAttribute(orient_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (e != cudaSuccess) return cuda_status(e, "orient smem attribute");
+        configured = true;
+    }
+    const int grid = accum_grid(orient_kernel, kOriThreads, n_kp_max, dyn);
     IcoT ico{};
     if (ico_host && K == 42) {
         ico.valid = 1;
@@ -965,7 +1043,7 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
             for (int m = 0; m < 5; ++m) ico.kind[v][m] = ico_host[72 + 5 * v + m];
         }
     }
-    orient_kernel<<<grid, kOriThreads, 0, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
+    orient_kernel<<<grid, kOriThreads, dyn, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
                                                                windows, windows32, dirs, K, pair_ok, secondary_ratio,
                                                                max_frames, weights, nframes, prim, sec, status,
                                                                exact_only, ico, ico_lut, grads, work);

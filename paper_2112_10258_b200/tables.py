@@ -303,6 +303,11 @@ class BallTable:
         off = np.concatenate(self._off) if self._off else np.zeros(1, np.int32)
         win = np.concatenate(self._win) if self._win else np.zeros(1, np.float64)
         planes = np.concatenate(self._planes) if self._planes else np.zeros(1, np.int32)
+        # the plane starts ride at the end of the offset table (the kernels read them at
+        # ball_offsets + pstart); pstart becomes relative to the table's start
+        if len(rec):
+            balls["pstart"] += len(off)
+        off = np.concatenate([off, planes]).astype(np.int32)
         return balls, off, win, planes
 
 

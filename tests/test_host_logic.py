@@ -103,7 +103,9 @@ def test_ball_table_and_windows():
     assert sorted(map(tuple, zo)) == sorted(map(tuple, offs))
     assert np.all(np.diff(zo[:, 2] * 10**6 + zo[:, 1] * 10**3 + zo[:, 0]) > 0)
     r = balls[i0]["r"]
-    ps = planes[balls[i0]["pstart"]: balls[i0]["pstart"] + 2 * r + 2]
+    # plane starts travel at the end of the offset table: pstart indexes `off`
+    ps = off[balls[i0]["pstart"]: balls[i0]["pstart"] + 2 * r + 2]
+    assert np.array_equal(ps, planes[: 2 * r + 2])
     for oz in range(-r, r + 1):
         assert np.all(zo[ps[oz + r]: ps[oz + r + 1], 2] == oz)
 
