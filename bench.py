@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--streams", type=int, default=8, help="parallel sub-batches (streams) per GPU")
     ap.add_argument("--slots", type=int, default=2, help="distinct input batches cycled over steps")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--backend", default="nccl", choices=("nccl", "gloo"),
+                    help="process-group backend for N > 1 (gloo: several ranks sharing one GPU, tests only)")
     ap.add_argument("--descriptor", default="siftrank", choices=("siftrank", "brief", "rrief"))
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -236,9 +238,19 @@ def run_ours(a):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    dev_index = local % max(1, torch.cuda.device_count())  # gloo tests run several ranks on one GPU
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if a.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group("gloo")
+
+    def max_over_ranks(v: float) -> float:
+        # the driver's contract: time on the device per rank, report the max over ranks
+        t = torch.tensor([v], device="cuda" if a.backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     import paper_2112_10258_b200 as vk
     from paper_2112_10258_b200 import _lib, synthetic
@@ -280,22 +292,33 @@ def run_ours(a):
     torch.cuda.synchronize()
     exs = [grp.members[0] for grp in groups]
     counts = {k: sum(m.counts()[k] for m in groups[0].members) for k in ("keypoints", "frames")}
-    # ---- cross-rank parity: every rank extracts the same fixed
-    # 2-volume batch; the digests of keypoints + descriptors must agree, so
-    # each GPU's outputs equal the single-GPU ones (which the tests pin to the oracle)
+    # ---- cross-rank parity: every rank extracts the same two
+    # volumes -- the first two of tests/golden/bench.npz, made by the unmodified
+    # reference -- and the per-volume digests (tests/golden/digest.py) are
+    # all-gathered: every GPU's outputs must equal each other AND the reference's
     chk = Extractor(DIMS, cfg, batch=2)
     chk.input.copy_(torch.from_numpy(np.ascontiguousarray(
-        synthetic.batch_from(base, 2, seed=7).transpose(0, 3, 2, 1))).cuda())
+        synthetic.batch_from(base, 2, seed=1000).transpose(0, 3, 2, 1))).cuda())
     chk.enqueue()
     rc = chk.results()
-    digest = hashlib.sha256(b"".join(np.ascontiguousarray(rc[k]).tobytes()
-                                     for k in ("pos", "sigma", "frame_prim", "frame_sec", "desc"))).hexdigest()
+    sys.path.insert(0, os.path.join(REPO, "tests", "golden"))
+    from digest import digest_results
+
+    vd = [digest_results(rc, v) for v in range(2)]
+    digest = hashlib.sha256(json.dumps(vd, sort_keys=True).encode()).hexdigest()
     digests = [digest]
     if world > 1:
         digests = [None] * world
         dist.all_gather_object(digests, digest)
     rank_parity = {"checked_volumes": 2, "keypoints": int(rc["n_keypoints"]), "digest": digest[:16],
                    "ranks": world, "all_ranks_equal": len(set(digests)) == 1}
+    gpath = os.path.join(REPO, "tests", "golden", "bench.npz")
+    if cfg.descriptor == "siftrank" and os.path.exists(gpath):
+        g = np.load(gpath)
+        rank_parity["matches_reference"] = all(
+            d[k] == (int(g[f"bench{v}_{k}"]) if k.startswith("n_") else str(g[f"bench{v}_{k}"]))
+            for v, d in enumerate(vd) for k in ("n_kp", "n_fr", "kp", "fr", "desc"))
+        rank_parity["reference"] = "tests/golden/bench.npz (unmodified volkey, make_bench_golden.py)"
     del chk, rc
     launches0 = _lib.load().vk_launch_count()
     groups[0].enqueue()
@@ -343,7 +366,7 @@ def run_ours(a):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev_index)
     clocks.start()
     time.sleep(0.3)
     torch.cuda.synchronize()
@@ -357,9 +380,7 @@ def run_ours(a):
     ms = e0.elapsed_time(e1)
     if world > 1:
         dist.barrier()
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms)
     value = world * B * a.steps / (ms / 1e3)
 
     # ---- end to end through the public API: pinned host -> HBM -> results -> host.
@@ -426,9 +447,7 @@ def run_ours(a):
         torch.cuda.synchronize()
         ems = f0.elapsed_time(f1)
         if world > 1:
-            t = torch.tensor([ems], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+            ems = max_over_ranks(ems)
         e2e = {"value": world * B * a.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(d2h_tot / a.steps), "ms_per_step": ems / a.steps,
                "path": "ExtractorGroup.run() per step on volumes copied in from pinned host memory (H2D on a copy "
@@ -464,7 +483,8 @@ def run_ours(a):
                    "volume": list(DIMS), "batch_per_gpu": B, "descriptor": a.descriptor,
                    "l2_policy": f"inputs larger than L2: {S} resident input slots x {B} volumes x 14.6 MB cycled",
                    "streams_per_gpu": G, "stage_timing_subbatch": Bs,
-                   "cuda_graph": use_graph, "parallelism": f"dp{world} (independent volumes, no collective)"},
+                   "cuda_graph": use_graph, "parallelism": f"dp{world} (independent volumes, no collective)",
+                   **({"backend": a.backend} if world > 1 else {})},
         "roofline": roofline,
         "stages_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
         "detect_gbs": round(det_gbs, 1),

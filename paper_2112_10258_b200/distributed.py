@@ -32,6 +32,10 @@ def gather_rows(local, group=None):
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
+    if local.is_cuda and dist.get_backend(group) != "nccl":
+        # gloo has no CUDA all-gather: stage through the host (multi-rank tests on one GPU)
+        db, counts = gather_rows(local.cpu(), group)
+        return db.to(local.device), counts
     n = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
     sizes = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(sizes, n, group=group)
