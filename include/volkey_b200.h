@@ -355,6 +355,27 @@ long long vk_format_records(long long n, const double* pos, const double* sigma,
  * (default), 1 = dp4a everywhere (cross-checks and benchmarks). */
 int vk_set_match_path(int path);
 
+/* ------------------------------------------------------ Hough consensus */
+/* Host-side (CPU, native C++) 7-DOF Hough consensus; replaces the scalar
+ * Python of hough_consensus (match.py:227-348) with vote_transform
+ * (match.py:124-133), _rotation_bins (match.py:184-207), _agrees
+ * (match.py:210-224) and similarity_from_correspondences (match.py:136-162).
+ * vk_hough_init binds the ILP64 OpenBLAS numpy links (scipy-openblas64
+ * symbol names), so every BLAS / LAPACK step is the call numpy makes.
+ * vk_hough_dots: directions @ (R @ ex) per match (match.py:191-192); the
+ * host takes np.argsort(-dots)[:, :2] (the reference's own unstable sort
+ * decides exact ties) and passes it as `near` to vk_hough_consensus.
+ * Returns 0, 5 (bad arguments), 6 (no cell reaches min_votes; *cell_votes =
+ * the densest count) or 9 (not initialised). */
+int vk_hough_init(const char* blas_path);
+int vk_hough_dots(int n, const double* rot_a, const double* rot_b, const double* dirs, int K, double* dots);
+int vk_hough_consensus(int n, const int64_t* index_a, const int64_t* index_b, const double* sigma_a,
+                       const double* sigma_b, const double* rot_a, const double* rot_b, const double* pos_a,
+                       const double* pos_b, const int64_t* near, const double* b1, const double* b2, int K,
+                       const double* settings /* log_scale_bin, trans_bin, log_scale_tol, rot_tol_deg, trans_tol */,
+                       int min_votes, int64_t* inliers, int* n_inliers, int* cell_votes, double* scale,
+                       double* rotation, double* translation);
+
 #ifdef __cplusplus
 }
 #endif

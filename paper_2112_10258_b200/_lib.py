@@ -64,6 +64,9 @@ SIGNATURES = {
     "vk_gradients_at": [P, I, I, I, P, LL, P, P],
     "vk_sample_trilinear": [P, I, I, I, P, LL, P, P],
     "vk_match_rows_excluding": [P, I, P, I, I, D, P, P, P, P, P, P],
+    "vk_hough_init": [C.c_char_p],
+    "vk_hough_dots": [I, P, P, P, I, P],
+    "vk_hough_consensus": [I, P, P, P, P, P, P, P, P, P, P, P, I, P, I, P, P, P, P, P, P],
 }
 _RESTYPE = {"vk_last_error": C.c_char_p, "vk_launch_count": C.c_longlong, "vk_accum_work_bytes": C.c_longlong,
             "vk_format_records": C.c_longlong}

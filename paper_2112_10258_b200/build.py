@@ -25,8 +25,15 @@ FLAGS_C = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPI
            "--expt-relaxed-constexpr"]
 
 
+CXX = os.environ.get("CXX", "g++")
+# host C++ (vk_consensus.cpp): IEEE double arithmetic step for step as CPython / numpy
+# do it -- no FMA contraction, no fast-math; -mfma only so that the explicit fma()
+# calls (OpenBLAS kernel restatements) become single instructions
+FLAGS_CXX = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-mfma", "-Wall"]
+
+
 def sources() -> list[str]:
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
 def needs_build() -> bool:
@@ -38,9 +45,13 @@ def needs_build() -> bool:
 
 
 def _compile(src: str, objdir: str, verbose: bool) -> str:
-    obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS_C, "-I", os.path.join(REPO, "include"), "-c", src, "-o", obj]
-    if verbose:
+    base, ext = os.path.splitext(os.path.basename(src))
+    obj = os.path.join(objdir, base + (".o" if ext == ".cu" else "_cpp.o"))
+    if ext == ".cpp":
+        cmd = [CXX, *FLAGS_CXX, "-I", os.path.join(REPO, "include"), "-c", src, "-o", obj]
+    else:
+        cmd = [NVCC, *ARCH, *FLAGS_C, "-I", os.path.join(REPO, "include"), "-c", src, "-o", obj]
+    if verbose and ext == ".cu":
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode != 0:
@@ -59,9 +70,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(PKG, "build_obj")
     os.makedirs(objdir, exist_ok=True)
     srcs = sources()
+    hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + [HEADER]
+    t_hdr = max(os.path.getmtime(p) for p in hdrs)
+
+    def one(src):  # incremental: reuse an object newer than its source and every header
+        base, ext = os.path.splitext(os.path.basename(src))
+        obj = os.path.join(objdir, base + (".o" if ext == ".cu" else "_cpp.o"))
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), t_hdr):
+            return obj
+        return _compile(src, objdir, verbose)
+
     with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, objdir, verbose), srcs))
-    cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", *objs, "-o", LIB + ".tmp"]
+        objs = list(ex.map(one, srcs))
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", *objs, "-ldl", "-o", LIB + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
