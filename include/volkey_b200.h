@@ -355,6 +355,29 @@ long long vk_format_records(long long n, const double* pos, const double* sigma,
  * (default), 1 = dp4a everywhere (cross-checks and benchmarks). */
 int vk_set_match_path(int path);
 
+/* ------------------------------------- fused orientation + SIFT-Rank */
+/* assign_orientations + sift_rank_descriptor (pipeline.py:41-67,
+ * orient.py:89-168, descriptor.py:227-263) in one kernel: per keypoint, the
+ * ball's stencil set is staged once in shared memory (sph_* tables from
+ * tables.sphere_tables: per ball (rows start, n_rows, compact floats, entries
+ * start), rows (dy, dz, m, start), entries (packed offset, c | yh << 16,
+ * yl | zh << 16, zl)), both walks read it, the frames are decided in between.
+ * Writes nframes / prim / sec per keypoint like vk_orient (status[0] bit 1 =
+ * DataError, status[1] / status[2] = orientation / SIFT-Rank repair counts)
+ * and each frame's 64 ranks at desc_kp[(kp * max_frames + f) * 64].  K must be
+ * 42 (icosphere lookup table).  box_cap: staging buffer floats (balls with a
+ * larger stencil, or one leaving the volume, are walked from global memory). */
+int vk_orient_siftrank(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_level* levels,
+                       const vk_ball* balls, const int* ball_offsets, const double* windows, const float* windows32,
+                       const double* dirs, int K, const uint8_t* pair_ok, double secondary_ratio, int max_frames,
+                       const double* rot_table, int* nframes, int* prim, int* sec, uint8_t* desc_kp, int* status,
+                       const int* ico_host, const uint8_t* ico_lut, const int* sph_ball, const int* sph_rows,
+                       const int* sph_ent, int box_cap, double* work, void* stream);
+/* rows[o] = rows_kp[frames[o].kp * max_frames + (o - frame_first[frames[o].kp])]
+ * (64-byte rows) for the n_frames (<= frame_cap) frames of vk_expand_frames. */
+int vk_scatter_frame_rows(const vk_frame* frames, const int* frame_first, const int* n_frames_dev, int frame_cap,
+                          int max_frames, const uint8_t* rows_kp, uint8_t* rows, void* stream);
+
 /* ------------------------------------------------------ Hough consensus */
 /* Host-side (CPU, native C++) 7-DOF Hough consensus; replaces the scalar
  * Python of hough_consensus (match.py:227-348) with vote_transform

@@ -64,6 +64,8 @@ SIGNATURES = {
     "vk_gradients_at": [P, I, I, I, P, LL, P, P],
     "vk_sample_trilinear": [P, I, I, I, P, LL, P, P],
     "vk_match_rows_excluding": [P, I, P, I, I, D, P, P, P, P, P, P],
+    "vk_orient_siftrank": [P, P, I, P, P, P, P, P, P, I, P, D, I, P, P, P, P, P, P, P, P, P, P, P, I, P, P],
+    "vk_scatter_frame_rows": [P, P, P, I, I, P, P, P],
     "vk_hough_init": [C.c_char_p],
     "vk_hough_dots": [I, P, P, P, I, P],
     "vk_hough_consensus": [I, P, P, P, P, P, P, P, P, P, P, P, I, P, I, P, P, P, P, P, P],

@@ -118,6 +118,27 @@ VK_D void prefetch_plane_ahead(const float* __restrict__ d, int nx, int ny, int 
     }
 }
 
+// L2 prefetch of the rows of a keypoint's ball plus its stencil halo (rows
+// with dy^2 + dz^2 <= (r + 1)^2, the whole x span of each, clamped to the
+// volume), issued by the whole CTA for the NEXT keypoint of a persistent walk:
+// the keypoint levels are HBM-resident when the walks start (a batch's levels
+// exceed L2), and the ball gathers then wait on HBM latency.
+#ifndef VK_PREFETCH_NEXT
+#define VK_PREFETCH_NEXT 0  // measured 2.5% slower on B200 (the walks are L1 / issue bound, not HBM-latency bound)
+#endif
+VK_D void prefetch_ball_l2(const float* __restrict__ d, int nx, int ny, int nz, int cx, int cy, int cz, int r) {
+    const int h = r + 1, w = 2 * h + 1;
+    const int x0 = max(cx - h, 0), x1 = min(cx + h, nx - 1);
+    for (int t = threadIdx.x; t < w * w; t += blockDim.x) {
+        const int dy = t % w - h, dz = t / w - h;
+        const int y = cy + dy, z = cz + dz;
+        if (dy * dy + dz * dz > h * h || y < 0 || y >= ny || z < 0 || z >= nz) continue;
+        const float* row = d + ((size_t)z * ny + y) * nx;
+        for (int x = x0; x < x1; x += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + x));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(row + x1));
+    }
+}
+
 // The six axis neighbours of (x, y, z) as loaded fp32 values plus the
 // central/one-sided divisor scale per axis (volume.py:244-264).
 struct Nb6 {

@@ -135,6 +135,15 @@ class DeviceTables:
         self.windows = t.from_numpy(win.copy()).cuda()
         self.plane_starts = t.from_numpy(planes.copy()).cuda()
         self.windows32 = t.from_numpy(win.astype(np.float32)).cuda()
+        # stencil spheres of the balls (fused orientation + SIFT-Rank, vk_orsr.cu)
+        srec, srows, sent, biggest = T.sphere_tables(plan.balls.radii)
+        self.sph_ball = t.from_numpy(srec.reshape(-1).copy()).cuda()
+        self.sph_rows = t.from_numpy(srows.reshape(-1).copy()).cuda()
+        self.sph_ent = t.from_numpy(sent.reshape(-1).copy()).cuda()
+        # staging buffer: the largest stencil (fused kernel only up to 14000 floats = 56 KB:
+        # with the 58 KB CTA state two CTAs fit an SM; larger balls use the separate kernels)
+        self.box_cap = int(biggest)
+        self.box_fits = self.box_cap <= 14000
         self.pairs = None
         self.pts = None
         if cfg.descriptor != "siftrank":
@@ -156,7 +165,7 @@ class Extractor:
 
     def __init__(self, dims, cfg: PipelineConfig | None = None, batch: int = 1, kp_cap: int | None = None,
                  frame_cap: int | None = None, exact_only: bool = False, input=None, gradient_volumes: bool = False,
-                 orient_field: bool = False, cand_cap: int | None = None):
+                 orient_field: bool = False, cand_cap: int | None = None, fused: bool | None = None):
         t = _lib.torch()
         self.cfg = cfg or PipelineConfig()
         self.plan = Plan.build(dims, self.cfg)
@@ -255,6 +264,15 @@ class Extractor:
             self.desc = t.empty((self.frame_cap, (self.cfg.pairs + 7) // 8), dtype=t.uint8, device="cuda")
         else:
             self.desc = t.empty((self.frame_cap, self.cfg.pairs), dtype=t.int16, device="cuda")
+        # fused orientation + SIFT-Rank (vk_orient_siftrank, stencil spheres staged in shared
+        # memory): fast path, SIFT-Rank, no dense gradient / field volumes, every ball's sphere
+        # within the staging cap.  Off by default (fused=None -> VK_FUSED, default 0): on B200
+        # its 2 CTAs/SM (shared-memory bound) measured slower than the separate latency-bound
+        # kernels at 3-4 CTAs/SM
+        want = fused if fused is not None else os.environ.get("VK_FUSED", "0") == "1"
+        self.fused = bool(want and not self.exact_only and kind == "siftrank" and not self.grad_levels
+                          and not self.field_levels and self.tables.box_fits)
+        self.desc_kp = (t.empty((self.kp_cap * self.maxf, 64), dtype=t.uint8, device="cuda") if self.fused else None)
         # volumes per pyramid chunk (enqueue_pyramid); env override for A/B runs
         self.pyr_chunk = int(os.environ.get("VK_PYR_CHUNK", "0")) or self.B
         # DoG of level pair (i-2, i-1) inside level i's (x, y) kernel (1) or in each level's z pass (0)
@@ -380,6 +398,27 @@ class Extractor:
                   self.frames.data_ptr(), self.rot.data_ptr(), self.n_frames.data_ptr(), self.dropped.data_ptr(),
                   self.frame_cap, self.frame_first.data_ptr(), s)
 
+    def enqueue_orient_describe(self, s: int) -> None:
+        """assign_orientations + describe_all for SIFT-Rank in one kernel
+        (pipeline.py:41-67, descriptor.py:227-306): frames per keypoint and
+        their rank vectors, then the frame expansion and the row scatter into
+        frame order."""
+        tb, cfg = self.tables, self.cfg
+        _memset(self.status, s)
+        _lib.call("vk_orient_siftrank", self.kps.data_ptr(), self.total.data_ptr(), self.kp_cap,
+                  self.level_table.data_ptr(), tb.balls.data_ptr(), tb.ball_offsets.data_ptr(), tb.windows.data_ptr(),
+                  tb.windows32.data_ptr(), tb.dirs.data_ptr(), tb.K, tb.pair_ok.data_ptr(), float(cfg.secondary_ratio),
+                  self.maxf, tb.rot_table.data_ptr(), self.nframes.data_ptr(), self.prim.data_ptr(),
+                  self.sec.data_ptr(), self.desc_kp.data_ptr(), self.status.data_ptr(), tb.ico.ctypes.data,
+                  tb.ico_lut.data_ptr(), tb.sph_ball.data_ptr(), tb.sph_rows.data_ptr(), tb.sph_ent.data_ptr(),
+                  tb.box_cap, self.accum.data_ptr(), s)
+        _lib.call("vk_expand_frames", self.nframes.data_ptr(), self.prim.data_ptr(), self.sec.data_ptr(),
+                  self.total.data_ptr(), self.kp_cap, self.maxf, tb.rot_table.data_ptr(), tb.K,
+                  self.frames.data_ptr(), self.rot.data_ptr(), self.n_frames.data_ptr(), self.dropped.data_ptr(),
+                  self.frame_cap, self.frame_first.data_ptr(), s)
+        _lib.call("vk_scatter_frame_rows", self.frames.data_ptr(), self.frame_first.data_ptr(),
+                  self.n_frames.data_ptr(), self.frame_cap, self.maxf, self.desc_kp.data_ptr(), self.desc.data_ptr(), s)
+
     def enqueue_describe(self, s: int) -> None:
         """describe_all (descriptor.py:266-306)."""
         tb, cfg = self.tables, self.cfg
@@ -406,6 +445,12 @@ class Extractor:
         if self.grad_levels:  # optional dense gradient volumes (not a reference stage)
             with rec("gradients", -1, -1):
                 self.enqueue_gradients(s)
+        if self.fused:
+            with rec("orient", -1, -1):  # one kernel: its time is the orient row
+                self.enqueue_orient_describe(s)
+            with rec("descriptor", -1, -1):
+                pass
+            return
         with rec("orient", -1, -1):
             self.enqueue_orient(s)
         with rec("descriptor", -1, -1):

@@ -311,6 +311,76 @@ class BallTable:
         return balls, off, win, planes
 
 
+def ball_sphere(radius: float):
+    """Compact shared-memory layout of a ball and its gradient stencil for the
+    fused orientation + SIFT-Rank kernel (csrc/vk_orsr.cu).
+
+    The stencil set S = ball + the six axis neighbours of every ball voxel.
+    Each (y, z) row of S is a symmetric x interval [-m, m] (every contributing
+    row interval is centred at 0), so S is stored row after row, x fastest.
+    Returns (rows, entries, size):
+      rows    (n_rows, 4) int32: dy, dz, m, first compact index of the row
+      entries (n, 4) int32, one per ball voxel in the z-major walk order:
+              packed offset, c | yh << 16, yl | zh << 16, zl -- the compact
+              index of the voxel (its x neighbours are c -+ 1) and of its
+              y / z neighbours
+      size    compact floats."""
+    rq = int(round(radius * 1024))
+    offs = ball_offsets(rq)
+    if not len(offs):
+        return np.zeros((0, 4), np.int32), np.zeros((0, 4), np.int32), 0
+    zoffs = offs[np.lexsort((offs[:, 0], offs[:, 1], offs[:, 2]))]
+    half: dict[tuple[int, int], int] = {}
+    for x, y, z in offs.tolist():
+        for dy, dz, dx in ((0, 0, 1), (1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0)):
+            key = (y + dy, z + dz)
+            half[key] = max(half.get(key, -1), abs(x) + dx)
+    rows, start, pos = [], 0, {}
+    for (y, z) in sorted(half, key=lambda k: (k[1], k[0])):
+        m = half[(y, z)]
+        rows.append((y, z, m, start))
+        pos[(y, z)] = (start, m)
+        start += 2 * m + 1
+    if start > 65535:
+        raise ParameterError("neighbourhood too large for the compact sphere layout")
+
+    def idx(x, y, z):
+        s0, m = pos[(y, z)]
+        assert -m <= x <= m
+        return s0 + x + m
+
+    ent = np.zeros((len(zoffs), 4), dtype=np.int64)
+    ent[:, 0] = pack_offsets(zoffs)
+    for k, (x, y, z) in enumerate(zoffs.tolist()):
+        c = idx(x, y, z)
+        assert idx(x + 1, y, z) == c + 1 and idx(x - 1, y, z) == c - 1
+        ent[k, 1] = c | (idx(x, y + 1, z) << 16)
+        ent[k, 2] = idx(x, y - 1, z) | (idx(x, y, z + 1) << 16)
+        ent[k, 3] = idx(x, y, z - 1)
+    return np.array(rows, dtype=np.int32), ent.astype(np.uint32).view(np.int32), start
+
+
+def sphere_tables(radii) -> tuple[np.ndarray, np.ndarray, np.ndarray, int]:
+    """ball_sphere for every ball of a BallTable (same ids): per ball
+    (rows start, n_rows, compact size, entries start) int32x4, the
+    concatenated rows and entries, and the largest compact size."""
+    recs, rows, ents = [], [], []
+    nr = ne = 0
+    biggest = 0
+    for radius in radii:
+        r, e, size = ball_sphere(radius)
+        recs.append((nr, len(r), size, ne))
+        rows.append(r)
+        ents.append(e)
+        nr += len(r)
+        ne += len(e)
+        biggest = max(biggest, size)
+    rec = np.array(recs, dtype=np.int32).reshape(-1, 4)
+    row = np.concatenate(rows) if rows else np.zeros((1, 4), np.int32)
+    ent = np.concatenate(ents) if ents else np.zeros((1, 4), np.int32)
+    return rec, np.ascontiguousarray(row), np.ascontiguousarray(ent), biggest
+
+
 # ------------------------------------------------------------ patch & pairs
 PAIR_SUPPORT_RADIUS = 2.0  # descriptor.py:34
 

@@ -633,3 +633,34 @@ def test_orientation_field_walk_equals_gradient_walk():
     a, b = outs
     assert np.array_equal(a["frame_prim"], b["frame_prim"]) and np.array_equal(a["frame_sec"], b["frame_sec"])
     assert np.array_equal(a["desc"], b["desc"]) and len(a["desc"]) > 5000
+
+
+@pytest.mark.parametrize("radius_factor", [2.5, 3.0])
+def test_fused_orientation_siftrank_equals_separate_and_exact(radius_factor):
+    """The fused kernel (vk_orient_siftrank: stencil spheres staged in shared
+    memory, clamped at the volume boundary, frames decided in the CTA) gives
+    the same frames and rank vectors as the separate fast kernels and as the
+    reference-order accumulation (exact_only, pinned to the reference's
+    goldens elsewhere).  Radius factors whose balls fit the staging buffer;
+    octaves 1-2 put many balls across the volume boundary."""
+    dims = (145, 174, 145)
+    base = synthetic.soup_volume(dims, np.random.default_rng(20240817), noise=0.01)
+    host = synthetic.batch_from(base, 2, seed=13)
+    cfg = PipelineConfig(radius_factor=radius_factor)
+    outs = {}
+    for mode in ("fused", "separate", "exact"):
+        ex = vk.Extractor(dims, cfg, batch=2, exact_only=mode == "exact", fused=mode == "fused")
+        assert ex.fused == (mode == "fused")
+        for i, v in enumerate(host):
+            ex.input[i].copy_(vk.volume.to_device(v))
+        ex.enqueue()
+        outs[mode] = ex.results()
+    a = outs["fused"]
+    assert a["n_frames"] > 2000
+    for other in ("separate", "exact"):
+        b = outs[other]
+        assert a["n_frames"] == b["n_frames"] and a["dropped_orientation"] == b["dropped_orientation"]
+        assert np.array_equal(a["frame_kp"], b["frame_kp"])
+        assert np.array_equal(a["frame_prim"], b["frame_prim"]) and np.array_equal(a["frame_sec"], b["frame_sec"])
+        assert np.array_equal(a["rot"], b["rot"])
+        assert np.array_equal(a["desc"], b["desc"]), f"fused descriptors differ from {other}"
