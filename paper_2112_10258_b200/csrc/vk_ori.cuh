@@ -369,6 +369,7 @@ VK_D int ori_walk(const vk_kp& kp, const vk_level& L, const float* data, const v
 #ifndef VK_ORI_DEPTH
 #define VK_ORI_DEPTH 3  // voxels in flight per thread (measured: 2 -> 3 is 2% faster, B200)
 #endif
+template <bool INTERIOR>
 VK_D int ori_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
                        const int* __restrict__ ball_offsets, const float* __restrict__ win32, const double* dirs,
                        const IcoSh* icp, const uint8_t* lut, double* hist, int2* queue) {
@@ -387,10 +388,21 @@ VK_D int ori_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, co
         grad32(nb, gx, gy, gz);
         red_vote(hist, nearest_dir_ico(dirs, *icp, nullptr, gx, gy, gz, nb), __int_as_float(e.y));
     };
-    auto addr = [&](int pk) {
-        return kc + unpack_off(pk, 2) * plane + unpack_off(pk, 1) * nx + unpack_off(pk, 0);
+    // !INTERIOR: voxels outside the volume get n.sx = 0 (a real scale is 0.5 or 1)
+    auto issue = [&](int pk, Nb6& n) {
+        const int ox = unpack_off(pk, 0), oy = unpack_off(pk, 1), oz = unpack_off(pk, 2);
+        if (INTERIOR) {
+            n = load_nb6_interior(data, (unsigned)nx, (unsigned)plane, (unsigned)(kc + oz * plane + oy * nx + ox));
+        } else {
+            const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
+            if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
+                n = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
+            } else {
+                n.sx = 0.f;
+            }
+        }
     };
-    int qn = 0;
+    int qn = 0, cnt = 0;
     // ring: voxel j + d * step has its neighbours loaded (d < D - 1) and its
     // packed offset loaded D - 1 steps ahead of use
     constexpr int D = VK_ORI_DEPTH;
@@ -400,7 +412,7 @@ VK_D int ori_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, co
     for (int d = 0; d < D; ++d) {
         const int jj = tid + d * step;
         pk[d] = jj < count ? __ldg(offs + jj) : 0;
-        if (d < D - 1 && jj < count) nb[d] = load_nb6_interior(data, (unsigned)nx, (unsigned)plane, (unsigned)addr(pk[d]));
+        if (d < D - 1 && jj < count) issue(pk[d], nb[d]);
     }
     for (int base = 0; base < count; base += step) {
         const int j = base + tid;
@@ -412,13 +424,14 @@ VK_D int ori_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, co
             nb[d] = nb[d + 1];
         }
         if (j + (D - 1) * step < count) {
-            nb[D - 2] = load_nb6_interior(data, (unsigned)nx, (unsigned)plane, (unsigned)addr(pk[D - 2]));
+            issue(pk[D - 2], nb[D - 2]);
             if (j + D * step < count) pk[D - 1] = __ldg(offs + j + D * step);
         }        int bin = -1;
         float vote = 0.f;
         bool miss = false;
         int c = 0;
-        if (j < count) {
+        if (j < count && (INTERIOR || cur.sx != 0.f)) {
+            ++cnt;
             float gx, gy, gz;
             grad32(cur, gx, gy, gz);
             if (grad_nonzero(cur)) {
@@ -447,7 +460,7 @@ VK_D int ori_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, co
         if (lane < qn) resolve(queue[lane]);
         __syncwarp();
     }
-    return tid < count ? (count - tid + step - 1) / step : 0;
+    return cnt;
 }
 
 // ori_walk<true> over the plane-staged ball (vk_stage.cuh): the same votes,

@@ -114,6 +114,9 @@ orient_field_kernel(const float* __restrict__ level, float* __restrict__ mag, ui
 
 
 
+#ifndef VK_ORI_PIPE_BORDER
+#define VK_ORI_PIPE_BORDER 0  // pipelined walk also for balls crossing the boundary: spills at 80 regs, measured slower
+#endif
 #ifndef VK_ORI_MIN_BLOCKS
 #define VK_ORI_MIN_BLOCKS 3  // with the pipelined walk: 3 CTAs/SM without spills beat 4 with (B200)
 #endif
@@ -208,9 +211,17 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
                                          sh.queue[tid >> 5], ring);
 #endif
         } else if (!exact_only && VK_ORI_PIPE && lutp && icp &&
-                   ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz)) {
-            inside_cnt = ori_walk_pipe(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, hist,
-                                       sh.queue[tid >> 5]);
+                   (VK_ORI_PIPE_BORDER || ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz))) {
+#if VK_ORI_PIPE_BORDER
+            inside_cnt = ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz)
+                             ? ori_walk_pipe<true>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, hist,
+                                                   sh.queue[tid >> 5])
+                             : ori_walk_pipe<false>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, hist,
+                                                    sh.queue[tid >> 5]);
+#else
+            inside_cnt = ori_walk_pipe<true>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, hist,
+                                             sh.queue[tid >> 5]);
+#endif
         } else if (!exact_only) {
             inside_cnt = ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz)
                              ? ori_walk<true>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp, K, hist,

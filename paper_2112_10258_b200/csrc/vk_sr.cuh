@@ -289,7 +289,7 @@ VK_D void sr_resolve(int4 e, const vk_kp& kp, const vk_level& L, const float* da
 #endif
 constexpr int kSrQueue = 32 + 4 * 32;  // per-warp deferred (voxel, frame) entries: flush at >= 32, one step adds <= 128
 
-template <int NF>
+template <int NF, bool INTERIOR>
 VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
                       const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist, int F,
                       int4* queue, int* qcount) {
@@ -300,11 +300,21 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
     const int zpf = L.nz - kPrefetchPlanes - kp.iz;  // prefetch plane exists while oz < zpf
     const int* offs = ball_offsets + ball.zstart;
     hist = vote_copy(hist);
+    // !INTERIOR: voxels outside the volume get n.sx = 0 (a real scale is 0.5 or 1)
     auto issue = [&](int pk, Nb6& n) {
         const int ox = unpack_off(pk, 0), oy = unpack_off(pk, 1), oz = unpack_off(pk, 2);
-        const int c = kc + oz * plane + oy * nx + ox;
-        if (oz < zpf) asm volatile("prefetch.global.L1 [%0];" ::"l"(data + c + kPrefetchPlanes * plane));
-        n = load_nb6_interior(data, (unsigned)nx, (unsigned)plane, (unsigned)c);
+        if (INTERIOR) {
+            const int c = kc + oz * plane + oy * nx + ox;
+            if (oz < zpf) asm volatile("prefetch.global.L1 [%0];" ::"l"(data + c + kPrefetchPlanes * plane));
+            n = load_nb6_interior(data, (unsigned)nx, (unsigned)plane, (unsigned)c);
+        } else {
+            const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
+            if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
+                n = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
+            } else {
+                n.sx = 0.f;
+            }
+        }
     };
     // ring: voxel j + d * step has its neighbours issued (d < D - 1) and its
     // packed offset loaded D - 1 steps ahead of use
@@ -330,7 +340,8 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
         if (j + (D - 1) * step < ball.count) {
             issue(pk[D - 2], nb[D - 2]);
             if (j + D * step < ball.count) pk[D - 1] = __ldg(offs + j + D * step);
-        }        if (j < ball.count) {
+        }
+        if (j < ball.count && (INTERIOR || cur.sx != 0.f)) {
             ++cnt;
             float gx, gy, gz;
             grad32(cur, gx, gy, gz);
@@ -391,12 +402,15 @@ VK_D int sr_walk_frames(const vk_kp& kp, const vk_level& L, const float* data, c
 #ifndef VK_SR_PIPE
 #define VK_SR_PIPE 1
 #endif
-    if (VK_SR_PIPE && INTERIOR && !g4 && F <= 4) {
+#ifndef VK_SR_PIPE_BORDER
+#define VK_SR_PIPE_BORDER 0  // border-crossing balls pipelined too: needs 2 CTAs/SM (no spills); measured equal within run-to-run noise
+#endif
+    if (VK_SR_PIPE && (INTERIOR || VK_SR_PIPE_BORDER) && !g4 && F <= 4) {
         switch (F) {
-            case 1: return sr_walk_pipe<1>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
-            case 2: return sr_walk_pipe<2>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
-            case 3: return sr_walk_pipe<3>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
-            default: return sr_walk_pipe<4>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
+            case 1: return sr_walk_pipe<1, INTERIOR>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
+            case 2: return sr_walk_pipe<2, INTERIOR>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
+            case 3: return sr_walk_pipe<3, INTERIOR>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
+            default: return sr_walk_pipe<4, INTERIOR>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
         }
     }
     switch (F) {
