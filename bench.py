@@ -156,7 +156,23 @@ def ncu_pyramid_traffic(batch: int):
     for r in rows[hi[0] + 1:]:
         if len(r) > vi and "blur" in r[ki] and r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             tot += float(r[vi].replace(",", ""))
-    captured_batch = 16  # scripts/gpu_bench_full.sh profiles profile_step.py --batch 16
+    # the capture's batch: scripts/profile_step.py prints "batch=N" (older logs: the
+    # per-volume candidate-count array of its counts() line has one entry per volume)
+    log = path[:-4] + ".log"
+    captured_batch = None
+    if os.path.exists(log):
+        import re
+
+        txt = open(log).read()
+        m = re.search(r"batch=(\d+)", txt)
+        if m:
+            captured_batch = int(m.group(1))
+        else:
+            m = re.search(r"'cand': array\(\[([^\]]*)\]", txt)
+            if m:
+                captured_batch = len([v for v in m.group(1).replace("\n", " ").split(",") if v.strip()])
+    if not captured_batch:
+        return None, None
     return tot * batch / captured_batch, os.path.relpath(path, REPO)
 
 

@@ -67,16 +67,16 @@ typedef struct vk_gradlevel {
 typedef struct vk_kp {
     int vol;      /* volume index within the batch */
     int lvl;      /* index into the level table (orientation / SIFT-Rank level) */
-    int ix, iy, iz; /* lattice centre in that level's grid (orient.py:258-268) */
+    int ix, iy, iz; /* lattice centre in that level's grid (orient.py:76-86) */
     int ball;     /* index into the ball table */
     int octave;
     int level;
 } vk_kp;
 
-/* Integer ball of offsets (orient.py:244-255): `count` packed offsets
+/* Integer ball of offsets (orient.py:63-74): `count` packed offsets
  * starting at `start` in the offset table (reference x-major order);
  * windows[window_start + d2] is the orientation window for squared offset
- * length d2 (orient.py:298-299); windows32 (where taken) is its fp32 cast.
+ * length d2 (orient.py:116-117); windows32 (where taken) is its fp32 cast.
  * The same points in z-major order (ox fastest: coalesced gathers) start at
  * `zstart`; plane starts (pstart, r) are kept for tools. */
 typedef struct vk_ball {
@@ -113,12 +113,12 @@ int vk_transpose_zfast_to_xfast(const float* src, float* dst, int nb, int nx, in
 int vk_transpose_xfast_to_zfast(const float* src, float* dst, int nb, int nx, int ny, int nz, void* stream);
 
 /* ----------------------------------------------------------- scale space */
-/* convolve_array / convolve_separable (scalespace.py:73-120): replicate-
+/* convolve_array / convolve_separable (scalespace.py:45-92): replicate-
  * padded separable blur, x then y then z pass, fp32 products added in tap
  * order (no FMA).  taps_host: 2*radius+1 float32 weights (gaussian_kernel,
- * scalespace.py:63-70).  Optional fused epilogues:
- *   dog_out  != NULL: dog_out = src - dst        (build_dog_pyramid, scalespace.py:237-251)
- *   half_out != NULL: half_out = subsample_half(dst) (scalespace.py:123-137)  */
+ * scalespace.py:35-42).  Optional fused epilogues:
+ *   dog_out  != NULL: dog_out = src - dst        (build_dog_pyramid, scalespace.py:209-223)
+ *   half_out != NULL: half_out = subsample_half(dst) (scalespace.py:95-109)  */
 int vk_blur3d(const float* src, float* dst, float* dog_out, float* half_out,
               int nb, int nx, int ny, int nz, const float* taps_host, int radius, void* stream);
 
@@ -161,7 +161,7 @@ int vk_set_xy_kernel(int k);
  * 3 = column-pair kernel. */
 int vk_set_z_kernel(int k);
 
-/* The tail of the pyramid in one launch (scalespace.py:186-251 for octaves
+/* The tail of the pyramid in one launch (scalespace.py:158-223 for octaves
  * whose levels hold <= 16384 voxels): one CTA per volume runs every level of
  * octaves 0..n_oct-1 of this call in shared memory.  dims_host: 3 per octave;
  * level_ptrs_host / dog_ptrs_host: n_oct*levels batched device pointers
@@ -172,10 +172,10 @@ int vk_small_octaves(int n_oct, int levels, int handoff, const int* dims_host, f
                      float* const* dog_ptrs_host, const int* radius_host, const float* taps_host, int nb,
                      void* stream);
 
-/* subsample_half (scalespace.py:123-137): floor dims, ordered 8-sum, /8. */
+/* subsample_half (scalespace.py:95-109): floor dims, ordered 8-sum, /8. */
 int vk_subsample_half(const float* src, float* dst, int nb, int nx, int ny, int nz, void* stream);
 
-/* DoG difference a - b over n elements (scalespace.py:247-248). */
+/* DoG difference a - b over n elements (scalespace.py:219-220). */
 int vk_difference(const float* a, const float* b, float* out, long long n, void* stream);
 
 /* ------------------------------------------------------------- detection */
@@ -204,8 +204,9 @@ int vk_extrema_from_map(const int16_t* map, const float* dog_cur, int nx, int ny
  * segment {octave, level, level_table_index, ball_index}; dog_levels: device
  * vk_level table indexed like seg (for dog_value).  Writes kps[0..total),
  * pos[3*i], sigma[i], dog[i], sign[i] (+1 peak, -1 valley), vol_offset[b]
- * and total[0].  seg_sigma_host: keypoint sigma per segment (detect.py:110,143-146). */
-int vk_order_keypoints(const unsigned long long* cand_keys, const int* cand_count, int nb, int cap,
+ * and total[0].  seg_sigma_host: keypoint sigma per segment (detect.py:110,143-146).
+ * The candidate keys are reordered in place (sorted runs of 2048). */
+int vk_order_keypoints(unsigned long long* cand_keys, const int* cand_count, int nb, int cap,
                        const int* seg_info_host, const double* seg_sigma_host, int nseg,
                        const vk_level* dog_levels, vk_kp* kps, double* pos, double* sigma, float* dog,
                        int8_t* sign, int* vol_offset, int* total, int kp_cap, void* stream);
@@ -216,12 +217,12 @@ int vk_order_keypoints(const unsigned long long* cand_keys, const int* cand_coun
 long long vk_accum_work_bytes(int device);
 
 /* ----------------------------------------------------------- orientation */
-/* gradient_histogram + dominant_orientations (orient.py:271-350) for n_kp
+/* gradient_histogram + dominant_orientations (orient.py:89-168) for n_kp
  * keypoints (n_kp_dev: device count, read by the kernel; n_kp_max bounds it).
  * dirs: K x 3 fp64 directions; pair_ok: K x K uint8 (norm of projection > 1e-6,
- * orient.py:339-343).  Outputs: weights (n x K fp64, nullable), nframes[n],
+ * orient.py:157-161).  Outputs: weights (n x K fp64, nullable), nframes[n],
  * prim/sec[n*max_frames].  status[1] counts exact-order fallbacks.  status[0] |= 1 when a keypoint's neighbourhood lies
- * outside its volume (DataError, orient.py:291-292).  ico_host (nullable, K==42
+ * outside its volume (DataError, orient.py:109-110).  ico_host (nullable, K==42
  * only): int[132] = 12 icosahedron-vertex indices into dirs, 12x5 indices of
  * the edge midpoints around each vertex, and the same 12x5 midpoints ordered
  * by neighbour kind (tables.icosphere_structure), enabling the screened and
@@ -241,13 +242,13 @@ int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_leve
               int exact_only, const int* ico_host, const uint8_t* ico_lut, const vk_gradlevel* grads,
               double* work, void* stream);
 
-/* dominant_orientations (orient.py:310-350) on n caller-supplied K-bin
+/* dominant_orientations (orient.py:128-168) on n caller-supplied K-bin
  * weight vectors (exact comparisons). */
 int vk_frames_from_weights(const double* weights, int n, int K, const uint8_t* pair_ok, double secondary_ratio,
                            int max_frames, int* nframes, int* prim, int* sec, void* stream);
 
 /* Dense gradient volume of a batched level for the orientation / SIFT-Rank
- * fast paths (volume.py:244-264 gradients, orient.py:305 nearest direction
+ * fast paths (volume.py:244-264 gradients, orient.py:123 nearest direction
  * with the default icosphere; ico_host as in vk_orient). */
 /* Orientation field of a batched level (nb x nz x ny x nx, x fastest): mag[v]
  * = fp32 |g| of the fp32 central-difference gradient (the orientation fast
@@ -261,7 +262,7 @@ int vk_gradient_volume(const float* level, void* g4, uint8_t* bin, int nb, int n
 
 /* Expand per-keypoint frames into the ordered frame list (pipeline.py:55-67:
  * keypoints with zero frames are dropped).  rot_table: K*K*9 fp64 rotations
- * (column-stacked axes, orient.py:346-347).  Writes frames[], rot[9*j],
+ * (column-stacked axes, orient.py:164-165).  Writes frames[], rot[9*j],
  * n_frames_dev[0], dropped_dev[0].  scratch: n_kp_max ints (device). */
 int vk_expand_frames(const int* nframes, const int* prim, const int* sec, const int* n_kp_dev,
                      int n_kp_max, int max_frames, const double* rot_table, int K,

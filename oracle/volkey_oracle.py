@@ -47,7 +47,7 @@ class OKp(NamedTuple):
 # --------------------------------------------------------------------------
 
 def gauss_taps(sigma: float):
-    """scalespace.py:63-70 -> (radius, float32 taps)."""
+    """scalespace.py:35-42 -> (radius, float32 taps)."""
     if sigma <= 0:
         raise OracleParameterError(f"sigma must be > 0, got {sigma}")
     r = max(1, math.ceil(3.0 * sigma))
@@ -58,7 +58,7 @@ def gauss_taps(sigma: float):
 
 
 def _axis_pass(a: np.ndarray, w: np.ndarray, axis: int) -> np.ndarray:
-    """One 1-D replicate-padded pass (scalespace.py:91-110): products rounded
+    """One 1-D replicate-padded pass (scalespace.py:63-82): products rounded
     to fp32, then added in tap order -r..+r (no fused multiply-add)."""
     r = (len(w) - 1) // 2
     widths = [(0, 0)] * 3
@@ -78,7 +78,7 @@ def _axis_pass(a: np.ndarray, w: np.ndarray, axis: int) -> np.ndarray:
 
 
 def blur3(a: np.ndarray, w: np.ndarray) -> np.ndarray:
-    """convolve_array (scalespace.py:73-88): x, then y, then z."""
+    """convolve_array (scalespace.py:45-60): x, then y, then z."""
     out = np.asarray(a, dtype=np.float32)
     for axis in (0, 1, 2):
         out = _axis_pass(out, w, axis)
@@ -86,7 +86,7 @@ def blur3(a: np.ndarray, w: np.ndarray) -> np.ndarray:
 
 
 def half(a: np.ndarray) -> np.ndarray:
-    """subsample_half (scalespace.py:123-137): floor-crop, ordered 8-sum, /8."""
+    """subsample_half (scalespace.py:95-109): floor-crop, ordered 8-sum, /8."""
     nx, ny, nz = a.shape
     if min(nx, ny, nz) < 2:
         raise OracleParameterError(f"cannot subsample dims {a.shape}")
@@ -100,7 +100,7 @@ def half(a: np.ndarray) -> np.ndarray:
 
 def octave_schedule(base_sigma: float, levels: int):
     """kappa, octave-local sigmas and the incremental blur sigmas
-    (scalespace.py:182-183, 207-209, 223)."""
+    (scalespace.py:154-155, 207-209, 223)."""
     kappa = 2.0 ** (1.0 / (levels - 3))
     local = [base_sigma * kappa ** i for i in range(levels)]
     inc = [math.sqrt(max(local[i] * local[i] - local[i - 1] * local[i - 1], 0.0))
@@ -109,7 +109,7 @@ def octave_schedule(base_sigma: float, levels: int):
 
 
 def pyramid(vol: np.ndarray, base_sigma=1.6, levels=6, num_octaves=6, min_octave_dim=4):
-    """build_gaussian_pyramid (scalespace.py:186-234).
+    """build_gaussian_pyramid (scalespace.py:158-206).
 
     Returns dict(octaves=[[level arrays]], sigmas=[[abs sigma]], kappa, source).
     """
@@ -135,7 +135,7 @@ def pyramid(vol: np.ndarray, base_sigma=1.6, levels=6, num_octaves=6, min_octave
 
 
 def dog(pyr):
-    """build_dog_pyramid (scalespace.py:237-251)."""
+    """build_dog_pyramid (scalespace.py:209-223)."""
     octs = [[lv[i] - lv[i + 1] for i in range(len(lv) - 1)] for lv in pyr["octaves"]]
     return dict(octaves=octs, sigmas=[s[:-1] for s in pyr["sigmas"]], kappa=pyr["kappa"])
 
@@ -254,7 +254,7 @@ def grads_at(data: np.ndarray, idx: np.ndarray) -> np.ndarray:
 # --------------------------------------------------------------------------
 
 def icosphere() -> np.ndarray:
-    """icosphere_directions (orient.py:215-241): 42 lexsorted unit vectors."""
+    """icosphere_directions (orient.py:34-60): 42 lexsorted unit vectors."""
     phi = (1.0 + math.sqrt(5.0)) / 2.0
     v = []
     for a in (-1.0, 1.0):
@@ -276,7 +276,7 @@ def icosphere() -> np.ndarray:
 
 
 def ball(radius_q: int) -> np.ndarray:
-    """_ball_offsets (orient.py:244-255): x-major, z-minor integer offsets."""
+    """_ball_offsets (orient.py:63-74): x-major, z-minor integer offsets."""
     rad = radius_q / 1024.0
     r = int(math.floor(rad))
     ax = np.arange(-r, r + 1)
@@ -285,7 +285,7 @@ def ball(radius_q: int) -> np.ndarray:
 
 
 def lattice(kp: OKp):
-    """keypoint_local (orient.py:258-268) without the level lookup."""
+    """keypoint_local (orient.py:76-86) without the level lookup."""
     scale = 2.0 ** kp.octave
     off = (scale - 1.0) / 2.0
     return np.array([round((c - off) / scale) for c in kp.position], dtype=np.intp), kp.sigma / scale
@@ -298,7 +298,7 @@ def _level(pyr, kp):
 
 
 def orient_hist(pyr, kp, radius_factor=4.0, dirs=None) -> np.ndarray:
-    """gradient_histogram (orient.py:271-307) -> (K,) fp64 weights."""
+    """gradient_histogram (orient.py:89-125) -> (K,) fp64 weights."""
     if radius_factor <= 0:
         raise OracleParameterError("radius_factor must be > 0")
     dirs = icosphere() if dirs is None else np.asarray(dirs, dtype=np.float64)
@@ -323,7 +323,7 @@ def orient_hist(pyr, kp, radius_factor=4.0, dirs=None) -> np.ndarray:
 
 
 def frames_from_hist(w, dirs=None, secondary_ratio=0.8, max_frames=4):
-    """dominant_orientations (orient.py:310-350) -> list of (3,3) rotations."""
+    """dominant_orientations (orient.py:128-168) -> list of (3,3) rotations."""
     if not 0 < secondary_ratio <= 1 or max_frames < 1:
         raise OracleParameterError("bad frame parameters")
     dirs = icosphere() if dirs is None else np.asarray(dirs, dtype=np.float64)

@@ -321,27 +321,63 @@ __global__ void batch_offsets_kernel(const int* __restrict__ counts, int nb, int
     total[1] = over;
 }
 
+// Keypoint order (detect.py:149-182: octave, level, z, y, x, peak before
+// valley) = numeric order of the 64-bit candidate keys.  Each run of
+// kSortChunk keys of a volume is bitonic-sorted in shared memory (in place),
+// then every key finds its global rank by binary searches over the runs:
+// O(n log n) per volume in total work, with n / kSortChunk searches per key.
+constexpr int kSortChunk = 2048;
+
+__global__ void __launch_bounds__(1024) chunk_sort_kernel(unsigned long long* __restrict__ keys,
+                                                          const int* __restrict__ counts, int cap) {
+    __shared__ unsigned long long s[kSortChunk];
+    const int b = blockIdx.y, c0 = blockIdx.x * kSortChunk;
+    const int n = min(counts[b], cap);
+    if (c0 >= n) return;
+    unsigned long long* kb = keys + (long long)b * cap + c0;
+    const int m = min(kSortChunk, n - c0);
+    for (int i = threadIdx.x; i < kSortChunk; i += blockDim.x) s[i] = i < m ? kb[i] : ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= kSortChunk; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < kSortChunk; i += blockDim.x) {
+                const int p = i ^ j;
+                if (p > i) {
+                    const unsigned long long a = s[i], c = s[p];
+                    if ((a > c) == ((i & k) == 0)) {
+                        s[i] = c;
+                        s[p] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < m; i += blockDim.x) kb[i] = s[i];
+}
+
 __global__ void __launch_bounds__(256)
 order_kernel(const unsigned long long* __restrict__ keys, const int* __restrict__ counts, int cap,
              const int* __restrict__ vol_offset, SegInfo seg, const vk_level* __restrict__ dog_levels,
              vk_kp* __restrict__ kps, double* __restrict__ pos, double* __restrict__ sigma, float* __restrict__ dogv,
              int8_t* __restrict__ sign, int kp_cap) {
-    __shared__ unsigned long long sk[256];
     const int b = blockIdx.y;
     const int n = min(counts[b], cap);
     const int i = blockIdx.x * 256 + threadIdx.x;
-    if (blockIdx.x * 256 >= n) return;
     const unsigned long long* kb = keys + (long long)b * cap;
-    const unsigned long long key = i < n ? kb[i] : ~0ull;
-    int rank = 0;
-    for (int t = 0; t < n; t += 256) {
-        __syncthreads();
-        sk[threadIdx.x] = t + threadIdx.x < n ? kb[t + threadIdx.x] : ~0ull;
-        __syncthreads();
-        const int m = min(256, n - t);
-        for (int j = 0; j < m; ++j) rank += sk[j] < key;
-    }
     if (i >= n) return;
+    const unsigned long long key = kb[i];
+    // keys are unique; each kSortChunk-run of kb is sorted (chunk_sort_kernel):
+    // the rank is the sum of the lower bounds of the key in every run
+    int rank = 0;
+    for (int c0 = 0; c0 < n; c0 += kSortChunk) {
+        int lo = 0, hi = min(kSortChunk, n - c0);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (kb[c0 + mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        rank += lo;
+    }
     const int out = vol_offset[b] + rank;
     if (out >= kp_cap) return;
     const int s = (int)(key >> 52);
@@ -428,7 +464,7 @@ extern "C" int vk_detect_octave(const float* const* dogs_host, int ndog, int nb,
     return cuda_status(cudaGetLastError(), "detect launch");
 }
 
-extern "C" int vk_order_keypoints(const unsigned long long* cand_keys, const int* cand_count, int nb, int cap,
+extern "C" int vk_order_keypoints(unsigned long long* cand_keys, const int* cand_count, int nb, int cap,
                                   const int* seg_info_host, const double* seg_sigma_host, int nseg,
                                   const vk_level* dog_levels, vk_kp* kps, double* pos, double* sigma, float* dog,
                                   int8_t* sign, int* vol_offset, int* total, int kp_cap, void* stream) {
@@ -450,6 +486,9 @@ extern "C" int vk_order_keypoints(const unsigned long long* cand_keys, const int
     batch_offsets_kernel<<<1, 32, 0, st>>>(cand_count, nb, cap, vol_offset, total);
     count_launch();
     if (cap > 0) {
+        chunk_sort_kernel<<<dim3((cap + kSortChunk - 1) / kSortChunk, nb), 1024, 0, st>>>(
+            cand_keys, cand_count, cap);
+        count_launch();
         dim3 grid((cap + 255) / 256, nb);
         order_kernel<<<grid, 256, 0, st>>>(cand_keys, cand_count, cap, vol_offset, s, dog_levels, kps, pos, sigma, dog,
                                            sign, kp_cap);

@@ -649,7 +649,7 @@ VK_D bool warp_mark_uncertain(const double* w, const int* order, int K, double e
     return __any_sync(0xffffffffu, any);
 }
 
-// frames_from with one warp (orient.py:310-350 semantics): primaries are the
+// frames_from with one warp (orient.py:128-168 semantics): primaries are the
 // positions of the (-w, index) order whose weight reaches ratio x top, at most
 // max_frames of them counted whether or not a secondary exists; each
 // secondary is the first bin of the order != primary with pair_ok, found with

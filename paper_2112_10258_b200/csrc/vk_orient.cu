@@ -238,7 +238,7 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         if (inside_cnt) atomicAdd(&sh.n_inside, inside_cnt);
         __syncthreads();
         if (sh.n_inside == 0) {
-            // DataError: orientation neighbourhood entirely outside (orient.py:291-292)
+            // DataError: orientation neighbourhood entirely outside (orient.py:109-110)
             if (tid == 0) {
                 atomicOr(status, 1);
                 nframes[item] = 0;

@@ -4,7 +4,7 @@
 // Reference: orient.py:89-125 (gradient_histogram), orient.py:128-168
 // (dominant_orientations), pipeline.py:41-67 (assign_orientations),
 // descriptor.py:227-263 (sift_rank_descriptor).  Both stages visit the same
-// integer ball around the same lattice centre (orient.py:244-255 offsets,
+// integer ball around the same lattice centre (orient.py:63-74 offsets,
 // keypoint_local) and need the same central-difference gradients
 // (volume.py:244-264).
 //

@@ -1,8 +1,8 @@
 // vk_pyramid.cu -- separable 3-D Gaussian blur with fused DoG and 2x
 // subsample epilogues, standalone subsample / difference, layout transposes.
 //
-// Reference: scalespace.py:73-137 (convolve_array, subsample_half) and
-// scalespace.py:237-251 (build_dog_pyramid).
+// Reference: scalespace.py:45-109 (convolve_array, subsample_half) and
+// scalespace.py:209-223 (build_dog_pyramid).
 //
 // Blur design (x-fastest volumes, one CTA = 32x32 (x,y) columns x a z-range):
 //  * 2.5-D z streaming: every input plane z' (clamped = replicate padding) is
@@ -363,7 +363,7 @@ blur3d_stream_kernel(const float* __restrict__ src, float* __restrict__ dst, flo
                     const int hnx = nx >> 1, hny = ny >> 1, hnz = nz >> 1;
                     const int hx = gx >> 1, hy = gy >> 1, hz = zo >> 1;
                     if (hx < hnx && hy < hny && hz < hnz) {
-                        // (dx, dy, dz) order of scalespace.py:129-135, then /8.
+                        // (dx, dy, dz) order of scalespace.py:101-107, then /8.
                         float sm = pv0.x;
                         sm = fadd(sm, o0.x);
                         sm = fadd(sm, pv1.x);
@@ -774,7 +774,7 @@ blur_z_kernel(const float* __restrict__ tmp, int tp, const float* __restrict__ s
             if (okx1) gv[1] = __fsub_rn(sv.y, o.y);
         }
         if (half != nullptr) {
-            // (dx, dy, dz) order of scalespace.py:129-135: this thread holds
+            // (dx, dy, dz) order of scalespace.py:101-107: this thread holds
             // rows y (lanes 0-15) or y+1 (lanes 16-31) of planes zo-1 (pv), zo (o)
             const float2 qv = make_float2(__shfl_xor_sync(0xffffffffu, pv.x, 16), __shfl_xor_sync(0xffffffffu, pv.y, 16));
             const float2 qo = make_float2(__shfl_xor_sync(0xffffffffu, o.x, 16), __shfl_xor_sync(0xffffffffu, o.y, 16));
@@ -947,7 +947,7 @@ blur_z4_kernel(const float* __restrict__ tmp, int tp, const float* __restrict__ 
             if (nvalid > 3) gv[3] = __fsub_rn(sv.w, o.w);
         }
         if constexpr (HALF) {
-            // (dx, dy, dz) order of scalespace.py:129-135 for the column pairs
+            // (dx, dy, dz) order of scalespace.py:101-107 for the column pairs
             // (x0, x0+1) and (x0+2, x0+3); rows y (even ry) and y+1 (lane ^ 8),
             // planes zo-1 (pv) and zo (o)
             float4 qv, qo;

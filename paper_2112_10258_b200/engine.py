@@ -80,7 +80,7 @@ class Plan:
             T.gaussian_kernel(T.incremental_sigma(p.local[i - 1], p.local[i])) for i in range(1, L)]
         cur = p.dims
         p.octave_dims = [cur]
-        # octave truncation rule of scalespace.py:227-231
+        # octave truncation rule of scalespace.py:199-203
         for o in range(cfg.num_octaves):
             if o + 1 == cfg.num_octaves:
                 break
@@ -104,7 +104,7 @@ class Plan:
                 finer = p.sigmas[o][i] / (2.0 ** o)
                 sl = finer * math.sqrt(p.kappa) * SCALE_CALIBRATION
                 sigma = sl * scale
-                radius = cfg.radius_factor * (sigma / scale)  # orient.py:265-286
+                radius = cfg.radius_factor * (sigma / scale)  # orient.py:83-104
                 s = o * L + i
                 p.seg_info[s] = (o, i, o * L + i, p.balls.index(radius))
                 p.seg_sigma[s] = sigma
@@ -281,7 +281,7 @@ class Extractor:
 
     # ------------------------------------------------------------ pipeline
     def enqueue_pyramid(self, s: int, with_dog: bool = True, rec=None) -> None:
-        """Gaussian levels with fused DoG + handoff subsample (scalespace.py:186-251)."""
+        """Gaussian levels with fused DoG + handoff subsample (scalespace.py:158-223)."""
         L, B, P = self.cfg.levels_per_octave, self.B, self.plan
         rec = rec or _no_stage
         handoff = L - 3

@@ -34,7 +34,7 @@ _ball_offsets = T.ball_offsets
 
 
 def keypoint_local(pyr, kp):
-    """orient.py:258-268 (host bookkeeping; the level data is downloaded)."""
+    """orient.py:76-86 (host bookkeeping; the level data is downloaded)."""
     if not (0 <= kp.octave < len(pyr.octaves)):
         raise ParameterError(f"keypoint octave {kp.octave} outside pyramid")
     octave = pyr.octaves[kp.octave]
@@ -47,7 +47,7 @@ def keypoint_local(pyr, kp):
 
 
 def gradient_histogram(pyr, kp, radius_factor: float = 4.0, directions: np.ndarray | None = None) -> SphericalHistogram:
-    """orient.py:271-307 on the GPU (exact accumulation order)."""
+    """orient.py:89-125 on the GPU (exact accumulation order)."""
     from .stages import run_orientation
 
     dirs = icosphere_directions() if directions is None else np.asarray(directions, dtype=np.float64)
@@ -69,7 +69,7 @@ def _frames(dirs, prim, sec, n) -> list[OrientationFrame]:
 
 
 def dominant_orientations(h: SphericalHistogram, secondary_ratio: float = 0.8, max_frames: int = 4) -> list[OrientationFrame]:
-    """orient.py:310-350: frames for every direction reaching secondary_ratio * max."""
+    """orient.py:128-168: frames for every direction reaching secondary_ratio * max."""
     if not 0 < secondary_ratio <= 1:
         raise ParameterError(f"secondary_ratio must be in (0, 1], got {secondary_ratio}")
     if max_frames < 1:

@@ -1,7 +1,7 @@
 """Gaussian scale space on the GPU -- drop-in for volkey scalespace.py.
 
 Same names, signatures, dataclasses and errors as the reference
-(scalespace.py:35-251); every voxel is computed by ``vk_blur3d`` /
+(scalespace.py:35-235); every voxel is computed by ``vk_blur3d`` /
 ``vk_subsample_half`` / ``vk_difference`` (csrc/vk_pyramid.cu).  Levels are
 returned as ``DeviceVolume`` (a ``Volume`` whose ``.data`` downloads lazily).
 ``workers`` / ``chunk`` are accepted for API compatibility and validated like
@@ -92,13 +92,13 @@ def convolve_array(arr: np.ndarray, kernel: GaussianKernel1D, workers: int = 1, 
 
 
 def convolve_separable(v: Volume, kernel: GaussianKernel1D, workers: int = 1, chunk: int = DEFAULT_CHUNK) -> Volume:
-    """scalespace.py:73-92 (chunk = z planes per CTA of the z pass)."""
+    """scalespace.py:45-64 (chunk = z planes per CTA of the z pass)."""
     _check_exec(workers, chunk)
     return DeviceVolume(blur_device_chunked(device_of(v), kernel, chunk), v.spacing)
 
 
 def subsample_half(v: Volume) -> Volume:
-    """scalespace.py:123-137."""
+    """scalespace.py:95-109."""
     nx, ny, nz = v.dims
     if min(nx, ny, nz) < 2:
         raise ParameterError(f"cannot subsample dims {v.dims}: every dim must be >= 2")
@@ -151,7 +151,7 @@ class DoGPyramid:
 def build_gaussian_pyramid(v: Volume, base_sigma: float = 1.6, levels_per_octave: int = 6, num_octaves: int = 6,
                            workers: int = 1, chunk: int = DEFAULT_CHUNK, min_octave_dim: int = MIN_OCTAVE_DIM,
                            recorder=None) -> GaussianPyramid:
-    """scalespace.py:186-234; the handoff subsample is fused into the blur that
+    """scalespace.py:158-206; the handoff subsample is fused into the blur that
     produces the handoff level (recorded under that level's "convolution")."""
     from .config import PipelineConfig
     from .engine import Plan
@@ -195,7 +195,7 @@ def build_gaussian_pyramid(v: Volume, base_sigma: float = 1.6, levels_per_octave
 
 
 def build_dog_pyramid(g: GaussianPyramid, recorder=None) -> DoGPyramid:
-    """scalespace.py:237-251 (finer minus coarser, per octave)."""
+    """scalespace.py:209-223 (finer minus coarser, per octave)."""
     if g.levels_per_octave < 2:
         raise ParameterError("pyramid needs at least 2 levels per octave")
     rec = _stage(recorder)

@@ -44,7 +44,7 @@ class PyramidView:
 
 
 def keypoint_records(view: PyramidView, keypoints, radius_factor: float, balls: T.BallTable):
-    """vk_kp records via keypoint_local (orient.py:258-268) + ball ids."""
+    """vk_kp records via keypoint_local (orient.py:76-86) + ball ids."""
     if radius_factor <= 0:
         raise ParameterError(f"radius_factor must be > 0, got {radius_factor}")
     n = len(keypoints)

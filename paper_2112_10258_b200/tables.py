@@ -23,7 +23,7 @@ from .errors import ParameterError
 # ---------------------------------------------------------------- Gaussians
 @dataclass(frozen=True)
 class GaussianKernel1D:
-    """Sampled normalised 1-D Gaussian, radius ceil(3 sigma) (scalespace.py:54-70)."""
+    """Sampled normalised 1-D Gaussian, radius ceil(3 sigma) (scalespace.py:35-42)."""
 
     sigma: float
     radius: int
@@ -44,12 +44,12 @@ def gaussian_kernel(sigma: float) -> GaussianKernel1D:
 
 
 def incremental_sigma(current: float, target: float) -> float:
-    """scalespace.py:182-183."""
+    """scalespace.py:154-155."""
     return math.sqrt(max(target * target - current * current, 0.0))
 
 
 def octave_sigmas(base_sigma: float, levels: int):
-    """kappa and octave-local sigmas (scalespace.py:207-209)."""
+    """kappa and octave-local sigmas (scalespace.py:179-181)."""
     kappa = 2.0 ** (1.0 / (levels - 3))
     return kappa, [base_sigma * kappa ** i for i in range(levels)]
 
@@ -57,7 +57,7 @@ def octave_sigmas(base_sigma: float, levels: int):
 # --------------------------------------------------------------- directions
 @lru_cache(maxsize=1)
 def icosphere_directions() -> np.ndarray:
-    """42 lexsorted unit vectors: icosahedron vertices + edge midpoints (orient.py:215-241)."""
+    """42 lexsorted unit vectors: icosahedron vertices + edge midpoints (orient.py:34-60)."""
     phi = (1.0 + math.sqrt(5.0)) / 2.0
     pts = []
     for a in (-1.0, 1.0):
@@ -194,7 +194,7 @@ def icosphere_lut() -> np.ndarray:
 def frame_tables(dirs: np.ndarray):
     """For every (primary p, candidate secondary q): whether q's projection
     orthogonal to p is usable (norm > 1e-6) and the resulting right-handed
-    frame [a1, a2, a1 x a2] (orient.py:333-349), evaluated with the reference's
+    frame [a1, a2, a1 x a2] (orient.py:151-167), evaluated with the reference's
     own numpy calls so the rotations are bit-identical."""
     dirs = np.asarray(dirs, dtype=np.float64)
     K = len(dirs)
@@ -222,7 +222,7 @@ def default_frame_tables():
 # -------------------------------------------------------------------- balls
 @lru_cache(maxsize=256)
 def ball_offsets(radius_q: int) -> np.ndarray:
-    """Integer offsets with |o| <= radius_q/1024, x-major / z-minor (orient.py:244-255)."""
+    """Integer offsets with |o| <= radius_q/1024, x-major / z-minor (orient.py:63-74)."""
     rad = radius_q / 1024.0
     r = int(math.floor(rad))
     ax = np.arange(-r, r + 1)
@@ -242,7 +242,7 @@ def pack_offsets(offs: np.ndarray) -> np.ndarray:
 
 def window_table(radius: float, max_d2: int) -> np.ndarray:
     """Orientation window exp(-|o|^2 / (2 (radius/2)^2)) for |o|^2 = 0..max_d2,
-    the exact numpy expression of orient.py:298-299 (host numpy exp)."""
+    the exact numpy expression of orient.py:116-117 (host numpy exp)."""
     window_sd = radius / 2.0
     d2 = np.arange(max_d2 + 1, dtype=np.float64)
     return np.exp(-d2 / (2.0 * window_sd * window_sd))

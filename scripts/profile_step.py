@@ -25,4 +25,5 @@ ex = Extractor(dims, vk.PipelineConfig(descriptor=a.descriptor), batch=a.batch, 
 for _ in range(a.steps):
     ex.enqueue()
 torch.cuda.synchronize()
+print(f"batch={a.batch} steps={a.steps}")
 print(ex.counts())

@@ -103,7 +103,7 @@ def test_blur_fused_epilogues_batched():
     """vk_blur3d with the DoG and 2x-subsample epilogues on a batch of odd-sized
     volumes (partial tiles, z-chunking, clamped borders) for every radius the
     streaming kernel instantiates: bit-equal to the oracle's blur3 / difference
-    / half (scalespace.py:91-110, 137-151)."""
+    / half (scalespace.py:63-82, 137-151)."""
     import torch
 
     from oracle import volkey_oracle as O

@@ -1,6 +1,6 @@
 """Parameter validation of the drop-in API matches the reference's errors
 (scalespace.py:172-177, detect.py:96-97,163-164, match.py:93-98,
-descriptor.py:99-100,145-160, orient.py:310-320): ParameterError with the
+descriptor.py:99-100,145-160, orient.py:128-138): ParameterError with the
 offending value, raised before any device work."""
 
 import numpy as np

@@ -80,7 +80,7 @@ def test_plan_matches_reference_schedule():
             assert (oo, ii, lvl) == (o, i, o * L + i)
             want = p.sigmas[o][i] / 2.0 ** o * math.sqrt(p.kappa) * math.sqrt(1.5) * 2.0 ** o
             assert p.seg_sigma[s] == want
-    # octave truncation rule (scalespace.py:227-231): 20 -> 10 -> 5 -> (2 < 4)
+    # octave truncation rule (scalespace.py:199-203): 20 -> 10 -> 5 -> (2 < 4)
     assert len(Plan.build((20, 20, 20), PipelineConfig()).octave_dims) == 3
 
 
