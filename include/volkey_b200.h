@@ -356,6 +356,21 @@ long long vk_format_records(long long n, const double* pos, const double* sigma,
  * (default), 1 = dp4a everywhere (cross-checks and benchmarks). */
 int vk_set_match_path(int path);
 
+/* Select the tensor-core kernel of the int8 euclidean path: 0 = warp-
+ * specialised persistent kernel (TMA reference tiles, N = 256, two TMEM
+ * accumulators; default), 1 = the barrier-synchronised N = 128 kernel (A/B). */
+int vk_set_match_tc_kernel(int kernel);
+
+/* Optional sub-voxel / sub-level refinement (an extension: volkey reports
+ * lattice positions): one Newton step of the DoG's quadratic
+ * model in (x, y, z, level) from central differences over the 3x3x3x3
+ * neighbourhood of each keypoint, fp64, fixed operation order.  out[6 * k]:
+ * refined x, y, z (input-volume coordinates), sigma * kappa^d_level,
+ * D + g.d / 2, status (0 converged, 1 |d_i| > 0.5, 2 singular Hessian).
+ * dog_levels: the DoG level table (index octave * levels_per_octave + level). */
+int vk_refine_keypoints(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_level* dog_levels,
+                        int levels_per_octave, double kappa, const double* sigma, double* out, void* stream);
+
 /* ------------------------------------- fused orientation + SIFT-Rank */
 /* assign_orientations + sift_rank_descriptor (pipeline.py:41-67,
  * orient.py:89-168, descriptor.py:227-263) in one kernel: per keypoint, the

@@ -60,12 +60,14 @@ SIGNATURES = {
     "vk_match": [I, P, I, P, I, I, D, P, P, P, P, P],
     "vk_match_excluding": [I, P, I, P, I, I, D, I, I, P, P, P, P, P],
     "vk_set_match_path": [I],
+    "vk_set_match_tc_kernel": [I],
     "vk_format_records": [LL, P, P, P, P, P, P, P, P, I, I, P, LL],
     "vk_gradients_at": [P, I, I, I, P, LL, P, P],
     "vk_sample_trilinear": [P, I, I, I, P, LL, P, P],
     "vk_match_rows_excluding": [P, I, P, I, I, D, P, P, P, P, P, P],
     "vk_orient_siftrank": [P, P, I, P, P, P, P, P, P, I, P, D, I, P, P, P, P, P, P, P, P, P, P, P, I, P, P],
     "vk_scatter_frame_rows": [P, P, P, I, I, P, P, P],
+    "vk_refine_keypoints": [P, P, I, P, I, D, P, P, P],
     "vk_hough_init": [C.c_char_p],
     "vk_hough_dots": [I, P, P, P, I, P],
     "vk_hough_consensus": [I, P, P, P, P, P, P, P, P, P, P, P, I, P, I, P, P, P, P, P, P],

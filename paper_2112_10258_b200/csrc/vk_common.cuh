@@ -224,9 +224,11 @@ static __device__ __noinline__ float norm3_f32_tiny(float x, float y, float z) {
 
 // |v| in fp32: within 4 u32 relative of the exact Euclidean norm when the
 // fp32 sum of squares is normal (it carries <= 3.5 u32, halved by the square
-// root, plus the hardware sqrt.approx.f32 (MUFU.SQRT) error, <= 1.67 x 2^-24
-// relative over every positive finite fp32 input, scripts/micro/sqrt_approx_err.cu
-// exhaustive sweep); below that the squares would underflow (|v| ~ 1e-19 can
+// root, plus the hardware sqrt.approx.f32 (MUFU.SQRT) error, <= 1.678 x 2^-24
+// relative over all 2^31 - 2^23 - 1 positive finite fp32 inputs (exhaustive
+// sweep on B200, scripts/micro/sqrt_approx_err.cu -> profiles/r02/
+// sqrt_approx_sweep.txt: max 1.0001e-7 at x = 3.1166e-36): 1.75 + 1.678 < 4 u32);
+// below that the squares would underflow (|v| ~ 1e-19 can
 // give s == 0), so the rescaled rare path above takes over: everywhere the
 // error is <= 4 u32 relative + 2^-150 absolute.
 #ifndef VK_APPROX_SQRT

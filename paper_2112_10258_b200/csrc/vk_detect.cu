@@ -405,6 +405,108 @@ order_kernel(const unsigned long long* __restrict__ keys, const int* __restrict_
     sign[out] = (key & 1ull) ? -1 : 1;
 }
 
+// Optional sub-voxel / sub-level refinement of the keypoints (not a reference
+// stage: volkey reports lattice positions; north_star asks for
+// the refinement as an extra output).  One Newton step of the quadratic
+// (Taylor) model of the DoG around the extremum, in (x, y, z, level) of its
+// octave: gradient and Hessian by central differences over the 3x3x3x3
+// neighbourhood (DoG levels l-1, l, l+1), H d = -g solved by Gaussian
+// elimination with partial pivoting in fp64, every operation separately
+// rounded in a fixed order (the oracle restates it operation for operation).
+// Output per keypoint (6 doubles): refined position in input-volume
+// coordinates, refined sigma (kp sigma x kappa^d_level), refined DoG value
+// D + g.d / 2, and a status: 0 = converged (|d_i| <= 0.5 on every axis),
+// 1 = offset above 0.5 (the extremum lies nearer another sample), 2 =
+// singular Hessian (offset 0).  The parity fields (kps, pos, sigma, dog) are
+// untouched.
+__global__ void refine_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_dev, int n_max,
+                              const vk_level* __restrict__ dog_levels, int levels_per_octave, double kappa,
+                              const double* __restrict__ sigma, double* __restrict__ out) {
+    const int n = min(*n_dev, n_max);
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const vk_kp kp = kps[k];
+        const int D0 = kp.octave * (levels_per_octave) + kp.level;  // DoG level table index of (octave, level)
+        const vk_level Lm = dog_levels[D0 - 1], Lc = dog_levels[D0], Lp = dog_levels[D0 + 1];
+        const int nx = Lc.nx, ny = Lc.ny, nz = Lc.nz;
+        auto at = [&](const vk_level& L, int dx, int dy, int dz) -> double {
+            const int x = clampi(kp.ix + dx, 0, nx - 1), y = clampi(kp.iy + dy, 0, ny - 1),
+                      z = clampi(kp.iz + dz, 0, nz - 1);
+            return (double)L.base[(long long)kp.vol * L.vol_stride + ((long long)z * ny + y) * nx + x];
+        };
+        // samples along axis a (0..3 = x, y, z, level) at offsets -1, 0, +1 (others 0)
+        auto s1 = [&](int a, int o) -> double {
+            if (a == 3) return at(o < 0 ? Lm : (o > 0 ? Lp : Lc), 0, 0, 0);
+            return at(Lc, a == 0 ? o : 0, a == 1 ? o : 0, a == 2 ? o : 0);
+        };
+        auto s2 = [&](int a, int oa, int b, int ob) -> double {  // a < b
+            const vk_level& L = b == 3 ? (ob < 0 ? Lm : Lp) : Lc;
+            int d[3] = {0, 0, 0};
+            d[a] = oa;
+            if (b < 3) d[b] = ob;
+            return at(L, d[0], d[1], d[2]);
+        };
+        const double c = s1(0, 0);
+        double g[4], H[4][4];
+        for (int a = 0; a < 4; ++a) {
+            const double p = s1(a, 1), m = s1(a, -1);
+            g[a] = dmul(dsub(p, m), 0.5);
+            H[a][a] = dsub(dadd(p, m), dmul(2.0, c));
+        }
+        for (int a = 0; a < 4; ++a)
+            for (int b = a + 1; b < 4; ++b) {
+                const double v = dsub(dsub(s2(a, 1, b, 1), s2(a, 1, b, -1)), dsub(s2(a, -1, b, 1), s2(a, -1, b, -1)));
+                H[a][b] = H[b][a] = dmul(v, 0.25);
+            }
+        // Gaussian elimination with partial pivoting on [H | -g]
+        double A[4][5];
+        for (int i = 0; i < 4; ++i) {
+            for (int j = 0; j < 4; ++j) A[i][j] = H[i][j];
+            A[i][4] = -g[i];
+        }
+        int status = 0;
+        for (int col = 0; col < 4 && status == 0; ++col) {
+            int piv = col;
+            for (int r = col + 1; r < 4; ++r)
+                if (fabs(A[r][col]) > fabs(A[piv][col])) piv = r;
+            if (!(fabs(A[piv][col]) > 0.0)) {
+                status = 2;
+                break;
+            }
+            if (piv != col)
+                for (int j = 0; j < 5; ++j) {
+                    const double t = A[col][j];
+                    A[col][j] = A[piv][j];
+                    A[piv][j] = t;
+                }
+            for (int r = col + 1; r < 4; ++r) {
+                const double f = __ddiv_rn(A[r][col], A[col][col]);
+                for (int j = col; j < 5; ++j) A[r][j] = dsub(A[r][j], dmul(f, A[col][j]));
+            }
+        }
+        double d[4] = {0.0, 0.0, 0.0, 0.0};
+        if (status == 0) {
+            for (int i = 3; i >= 0; --i) {
+                double acc = A[i][4];
+                for (int j = i + 1; j < 4; ++j) acc = dsub(acc, dmul(A[i][j], d[j]));
+                d[i] = __ddiv_rn(acc, A[i][i]);
+            }
+            for (int i = 0; i < 4; ++i)
+                if (fabs(d[i]) > 0.5) status = 1;
+        }
+        const double scale = ldexp(1.0, kp.octave);
+        const double off = (scale - 1.0) / 2.0;
+        double* o = out + 6LL * k;
+        o[0] = dadd(dmul(dadd((double)kp.ix, d[0]), scale), off);
+        o[1] = dadd(dmul(dadd((double)kp.iy, d[1]), scale), off);
+        o[2] = dadd(dmul(dadd((double)kp.iz, d[2]), scale), off);
+        o[3] = dmul(sigma[k], pow(kappa, d[3]));
+        double gd = 0.0;
+        for (int i = 0; i < 4; ++i) gd = dadd(gd, dmul(g[i], d[i]));
+        o[4] = dadd(c, dmul(0.5, gd));
+        o[5] = (double)status;
+    }
+}
+
 }  // namespace vk
 
 using namespace vk;
@@ -510,4 +612,20 @@ extern "C" int vk_extrema_from_map(const int16_t* map, const float* dog_cur, int
         map, dog_cur, nx, ny, nz, seg, band, contrast_min, cand_keys, cand_count, cap);
     count_launch();
     return cuda_status(cudaGetLastError(), "extrema launch");
+}
+
+extern "C" int vk_refine_keypoints(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, const vk_level* dog_levels,
+                                   int levels_per_octave, double kappa, const double* sigma, double* out,
+                                   void* stream) {
+    if (!kps || !n_kp_dev || n_kp_max < 0 || !dog_levels || levels_per_octave < 4 || !(kappa > 1.0) || !sigma ||
+        !out) {
+        set_error("vk_refine_keypoints: bad arguments");
+        return VK_ERR_PARAMETER;
+    }
+    if (n_kp_max == 0) return VK_OK;
+    const int grid = n_kp_max < 256 * 148 ? (n_kp_max + 255) / 256 : 148;
+    refine_kernel<<<grid, 256, 0, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, dog_levels, levels_per_octave, kappa,
+                                                       sigma, out);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "refine launch");
 }

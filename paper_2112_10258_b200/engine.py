@@ -165,7 +165,8 @@ class Extractor:
 
     def __init__(self, dims, cfg: PipelineConfig | None = None, batch: int = 1, kp_cap: int | None = None,
                  frame_cap: int | None = None, exact_only: bool = False, input=None, gradient_volumes: bool = False,
-                 orient_field: bool = False, cand_cap: int | None = None, fused: bool | None = None):
+                 orient_field: bool = False, cand_cap: int | None = None, fused: bool | None = None,
+                 refine: bool = False):
         t = _lib.torch()
         self.cfg = cfg or PipelineConfig()
         self.plan = Plan.build(dims, self.cfg)
@@ -257,6 +258,9 @@ class Extractor:
         self.rot = t.empty(self.frame_cap * 9, dtype=t.float64, device="cuda")
         self.n_frames = t.zeros(1, dtype=i32, device="cuda")
         self.dropped = t.zeros(1, dtype=i32, device="cuda")
+        # optional sub-voxel / sub-level refinement (vk_refine_keypoints; not a reference output)
+        self.refine = bool(refine)
+        self.refined = t.empty(self.kp_cap * 6, dtype=t.float64, device="cuda") if self.refine else None
         kind = self.cfg.descriptor
         if kind == "siftrank":
             self.desc = t.empty((self.frame_cap, 64), dtype=t.uint8, device="cuda")
@@ -369,6 +373,10 @@ class Extractor:
                   self.cand_cap, seg.ctypes.data, sig.ctypes.data, len(sig), self.dog_table.data_ptr(),
                   self.kps.data_ptr(), self.pos.data_ptr(), self.sigma.data_ptr(), self.dogv.data_ptr(),
                   self.sign.data_ptr(), self.vol_offset.data_ptr(), self.total.data_ptr(), self.kp_cap, s)
+        if self.refine:
+            _lib.call("vk_refine_keypoints", self.kps.data_ptr(), self.total.data_ptr(), self.kp_cap,
+                      self.dog_table.data_ptr(), cfg.levels_per_octave, float(P.kappa), self.sigma.data_ptr(),
+                      self.refined.data_ptr(), s)
 
     def enqueue_gradients(self, s: int) -> None:
         """Dense gradient / nearest-direction volumes of the keypoint levels."""
@@ -513,6 +521,7 @@ class Extractor:
             vol_offset=self.vol_offset.cpu().numpy(), frame_kp=fr["kp"].copy(), frame_prim=fr["prim"].copy(),
             frame_sec=fr["sec"].copy(), rot=self.rot[: 9 * m].cpu().numpy().reshape(m, 3, 3),
             desc=self.desc[:m].cpu().numpy(),
+            refined=self.refined[: 6 * n].cpu().numpy().reshape(n, 6) if self.refine else None,
         )
 
 

@@ -38,6 +38,13 @@ class ExtractionResult:
         self._soa, self._kind, self._npairs = _soa, _kind, _npairs
 
     @property
+    def refined(self) -> np.ndarray | None:
+        """(n_keypoints, 6) float64 sub-voxel / sub-level refinement -- x, y, z,
+        sigma, dog_value, status (0 converged, 1 offset > 0.5, 2 singular) --
+        when extract_features(..., refine=True); None otherwise."""
+        return None if self._soa is None else self._soa.get("refined")
+
+    @property
     def soa(self) -> dict | None:
         """Structure-of-arrays results straight from the device (no objects)."""
         return self._soa
@@ -150,8 +157,14 @@ def clear_extractor_cache() -> None:
     _POOL.clear()
 
 
-def extract_features(volume: Volume, config: PipelineConfig | None = None, recorder=None) -> ExtractionResult:
-    """pipeline.py:70-102 on the GPU (Extractor cached per (dims, config))."""
+def extract_features(volume: Volume, config: PipelineConfig | None = None, recorder=None, *,
+                     refine: bool = False) -> ExtractionResult:
+    """pipeline.py:70-102 on the GPU (Extractor cached per (dims, config)).
+
+    refine=True (an extension, off by default: the reference reports lattice
+    positions) adds ``result.refined``: per keypoint the sub-voxel / sub-level
+    quadratic refinement (x, y, z, sigma, dog_value, status) of
+    vk_refine_keypoints; the reference fields are unchanged."""
     import weakref
 
     cfg = config or PipelineConfig()
@@ -159,8 +172,8 @@ def extract_features(volume: Volume, config: PipelineConfig | None = None, recor
         from .descriptor import sample_point_pairs
 
         sample_point_pairs(cfg.method, cfg.pairs, 1.0, cfg.seed)  # validation order of pipeline.py:86-88
-    key = (tuple(volume.dims), cfg.model_dump_json())
-    entry = _POOL.get(key, lambda: Extractor(volume.dims, cfg, batch=1))
+    key = (tuple(volume.dims), cfg.model_dump_json(), bool(refine))
+    entry = _POOL.get(key, lambda: Extractor(volume.dims, cfg, batch=1, refine=refine))
     ex = entry[0]
     while True:
         ex.input[0].copy_(device_of(volume))
@@ -176,7 +189,7 @@ def extract_features(volume: Volume, config: PipelineConfig | None = None, recor
             kp_cap = max(kp_cap, cand_cap)
             frame_cap = max(frame_cap, kp_cap * cfg.max_frames)
         ex = Extractor(volume.dims, cfg, batch=1, kp_cap=kp_cap, frame_cap=frame_cap,
-                       cand_cap=max(ex.cand_cap, cand_cap or 0))
+                       cand_cap=max(ex.cand_cap, cand_cap or 0), refine=refine)
         entry[0] = ex  # the grown Extractor replaces the cached one
     soa = ex.results()
     pyr, dog = _wrap_pyramids(ex, volume)

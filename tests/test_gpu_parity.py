@@ -219,6 +219,16 @@ def test_nn_tensor_core_path_matches_oracle():
         got_dp = _nn_raw(a, b, 0.9, lo, hi, path=1)
         for x, y in zip(got_tc, got_dp):
             assert np.array_equal(x, y), (na, nb, dim, ex)
+        from paper_2112_10258_b200 import _lib as L
+
+        lib = L.load()
+        lib.vk_set_match_tc_kernel(1)  # the barrier-synchronised N = 128 kernel agrees too
+        try:
+            got_t1 = _nn_raw(a, b, 0.9, lo, hi, path=0)
+        finally:
+            lib.vk_set_match_tc_kernel(0)
+        for x, y in zip(got_tc, got_t1):
+            assert np.array_equal(x, y), (na, nb, dim, ex)
         bb = np.concatenate([b[:lo], b[hi:]]).astype(np.int64)
         ref = O.nn_match(a.astype(np.int64), bb, 1.0)
         assert [int(i) for i in got_tc[0]] == [r[1] for r in ref]
