@@ -177,7 +177,10 @@ def extract_features(volume: Volume, config: PipelineConfig | None = None, recor
     ex = entry[0]
     while True:
         ex.input[0].copy_(device_of(volume))
-        ex.enqueue(rec=_stage(recorder) if recorder is not None else None)
+        if recorder is None and ex.graph is not None:
+            ex.graph.replay()  # the cached Extractor's pipeline as one CUDA graph (~60 launches)
+        else:
+            ex.enqueue(rec=_stage(recorder) if recorder is not None else None)
         c = ex.check_capacity()
         if not c["overflow"]:
             break
@@ -192,6 +195,12 @@ def extract_features(volume: Volume, config: PipelineConfig | None = None, recor
                        cand_cap=max(ex.cand_cap, cand_cap or 0), refine=refine)
         entry[0] = ex  # the grown Extractor replaces the cached one
     soa = ex.results()
+    if recorder is None and ex.graph is None:
+        # second call on this Extractor: capture its pipeline for the following calls
+        # (Extractor.capture runs one more eager pass first; the results above are kept)
+        if getattr(ex, "_dropin_calls", 0) >= 1:
+            ex.capture()
+        ex._dropin_calls = getattr(ex, "_dropin_calls", 0) + 1
     pyr, dog = _wrap_pyramids(ex, volume)
     res = ExtractionResult(pyr, dog, dropped_orientation=soa["dropped_orientation"], _soa=soa, _kind=cfg.descriptor,
                            _npairs=cfg.pairs)
