@@ -4,6 +4,7 @@
 # pipeline launch of one 16-volume step, full ncu captures of the hot kernels.
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 O=gpurun_out/full
+rm -rf $O
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $O/gpu.txt 2>&1
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
@@ -21,9 +22,11 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   python scripts/profile_step.py --batch 16 --steps 1 > $O/pyramid_dram.log 2>&1; echo "dram rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"blur_xy" --launch-skip 5 --launch-count 1 \
   -o $O/blur10_full python scripts/profile_step.py --batch 12 --steps 1 > /dev/null 2>&1; echo "blur full rc=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"match_i8_tc" -o $O/match_full \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"match_i8_ws" -o $O/match_full \
   python scripts/match_prof.py > /dev/null 2>&1; echo "match full rc=$?"
 for k in siftrank_kernel orient_kernel; do
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$k" --launch-count 1 \
   -o $O/${k}_full python scripts/profile_step.py --batch 12 --steps 1 > /dev/null 2>&1; echo "$k full rc=$?"
 done
+timeout 600 python scripts/match_bench.py > $O/match_bench.log 2>&1; echo "match bench rc=$?"
+timeout 900 python scripts/database_bench.py > $O/database_bench.json 2> $O/database_bench.err; echo "database rc=$?"
