@@ -663,7 +663,7 @@ def bench_matching() -> dict:
     tops = 2.0 * 64 * pairs_s / 1e12
     subj, per = 1000, 3400
     return {
-        "kernel": "match_i8_tc_kernel (tcgen05.mma kind::i8, s32 TMEM accumulators, top-2 epilogue)",
+        "kernel": "match_i8_ws_kernel (warp-specialised: TMA tiles, tcgen05.mma kind::i8 M=2x128 N=128, s32 TMEM accumulators, top-2 epilogue warps)",
         "image_pair_ms": round(pair_ms, 4), "image_pair_shape": [3400, 3300],
         "database_sample": {"queries": na, "database_rows": nb, "ms": round(db_ms, 3),
                             "pairs_per_s": round(pairs_s), "unit": "descriptor pairs/s"},

@@ -700,10 +700,24 @@ static int launch_ws(const uint8_t* a, int na, const uint8_t* b, int nb, double 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int qtiles = (na + kWsM - 1) / kWsM;
     const int n_tiles = (nb + kWsN - 1) / kWsN;
-    // (query tile, slice) CTAs, one per SM at a time: about four waves, >= 8 tiles per CTA
-    int slices = (4 * sms + qtiles - 1) / qtiles;
-    if (slices > n_tiles / 8) slices = n_tiles / 8;
-    if (slices < 1) slices = 1;
+    // (query tile, slice) CTAs, one per SM at a time, >= 8 reference tiles per CTA: the slice
+    // count whose CTA total fills its last wave best (>= 95% wave efficiency: the smallest such
+    // count, fewer partials to merge), at least one full wave when the shape allows
+    const int s_max = max(1, min(n_tiles / 8, 256));
+    int slices = 1;
+    double best_eff = -1.0;
+    for (int sc = 1; sc <= s_max; ++sc) {
+        const int per_ = (n_tiles + sc - 1) / sc, real = (n_tiles + per_ - 1) / per_;
+        const long long ctas = (long long)qtiles * real;
+        const double eff = (double)ctas / (double)(((ctas + sms - 1) / sms) * sms);
+        const bool full = ctas >= sms;
+        const double score = eff + (full ? 1.0 : 0.0);
+        if (score > best_eff + 1e-9) {
+            best_eff = score;
+            slices = real;
+        }
+        if (full && eff >= 0.95) break;
+    }
     const int per = (n_tiles + slices - 1) / slices;
     slices = (n_tiles + per - 1) / per;
     const int n_pad = n_tiles * kWsN;

@@ -388,18 +388,24 @@ VK_D int ori_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, co
         grad32(nb, gx, gy, gz);
         red_vote(hist, nearest_dir_ico(dirs, *icp, nullptr, gx, gy, gz, nb), __int_as_float(e.y));
     };
-    // !INTERIOR: voxels outside the volume get n.sx = 0 (a real scale is 0.5 or 1)
     auto issue = [&](int pk, Nb6& n) {
         const int ox = unpack_off(pk, 0), oy = unpack_off(pk, 1), oz = unpack_off(pk, 2);
         if (INTERIOR) {
             n = load_nb6_interior(data, (unsigned)nx, (unsigned)plane, (unsigned)(kc + oz * plane + oy * nx + ox));
         } else {
-            const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
-            if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
-                n = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
-            } else {
-                n.sx = 0.f;
-            }
+            // branch-free clamped loads (the centre clamped into the volume too: values of
+            // outside voxels are never used); the scales are recomputed at use, so a ring slot
+            // carries only the six values
+            const int x = clampi(kp.ix + ox, 0, L.nx - 1), y = clampi(kp.iy + oy, 0, L.ny - 1),
+                      z = clampi(kp.iz + oz, 0, L.nz - 1);
+            const unsigned c = ((unsigned)z * (unsigned)L.ny + (unsigned)y) * (unsigned)L.nx + (unsigned)x;
+            const unsigned pl = (unsigned)L.nx * (unsigned)L.ny;
+            n.xh = __ldg(data + (c + (x < L.nx - 1)));
+            n.xl = __ldg(data + (c - (x > 0)));
+            n.yh = __ldg(data + (c + (y < L.ny - 1 ? (unsigned)L.nx : 0u)));
+            n.yl = __ldg(data + (c - (y > 0 ? (unsigned)L.nx : 0u)));
+            n.zh = __ldg(data + (c + (z < L.nz - 1 ? pl : 0u)));
+            n.zl = __ldg(data + (c - (z > 0 ? pl : 0u)));
         }
     };
     int qn = 0, cnt = 0;
@@ -417,7 +423,8 @@ VK_D int ori_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, co
     for (int base = 0; base < count; base += step) {
         const int j = base + tid;
         const int pc = pk[0];
-        const Nb6 cur = nb[0];
+        Nb6 cur0 = nb[0];
+        cur0.sx = cur0.sy = cur0.sz = 0.5f;
 #pragma unroll
         for (int d = 0; d + 1 < D; ++d) {
             pk[d] = pk[d + 1];
@@ -430,7 +437,16 @@ VK_D int ori_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, co
         float vote = 0.f;
         bool miss = false;
         int c = 0;
-        if (j < count && (INTERIOR || cur.sx != 0.f)) {
+        bool in = j < count;
+        Nb6 cur = cur0;
+        if (!INTERIOR && in) {
+            const int x = kp.ix + unpack_off(pc, 0), y = kp.iy + unpack_off(pc, 1), z = kp.iz + unpack_off(pc, 2);
+            in = x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz;
+            cur.sx = (x > 0 && x < L.nx - 1) ? 0.5f : 1.0f;
+            cur.sy = (y > 0 && y < L.ny - 1) ? 0.5f : 1.0f;
+            cur.sz = (z > 0 && z < L.nz - 1) ? 0.5f : 1.0f;
+        }
+        if (in) {
             ++cnt;
             float gx, gy, gz;
             grad32(cur, gx, gy, gz);

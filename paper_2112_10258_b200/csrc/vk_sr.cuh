@@ -300,7 +300,6 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
     const int zpf = L.nz - kPrefetchPlanes - kp.iz;  // prefetch plane exists while oz < zpf
     const int* offs = ball_offsets + ball.zstart;
     hist = vote_copy(hist);
-    // !INTERIOR: voxels outside the volume get n.sx = 0 (a real scale is 0.5 or 1)
     auto issue = [&](int pk, Nb6& n) {
         const int ox = unpack_off(pk, 0), oy = unpack_off(pk, 1), oz = unpack_off(pk, 2);
         if (INTERIOR) {
@@ -308,12 +307,19 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
             if (oz < zpf) asm volatile("prefetch.global.L1 [%0];" ::"l"(data + c + kPrefetchPlanes * plane));
             n = load_nb6_interior(data, (unsigned)nx, (unsigned)plane, (unsigned)c);
         } else {
-            const int x = kp.ix + ox, y = kp.iy + oy, z = kp.iz + oz;
-            if (x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz) {
-                n = load_nb6(data, L.nx, L.ny, L.nz, x, y, z);
-            } else {
-                n.sx = 0.f;
-            }
+            // branch-free clamped loads (the centre clamped into the volume too: values of
+            // outside voxels are never used); the scales are recomputed at use, so a ring slot
+            // carries only the six values
+            const int x = clampi(kp.ix + ox, 0, L.nx - 1), y = clampi(kp.iy + oy, 0, L.ny - 1),
+                      z = clampi(kp.iz + oz, 0, L.nz - 1);
+            const unsigned c = ((unsigned)z * (unsigned)L.ny + (unsigned)y) * (unsigned)L.nx + (unsigned)x;
+            const unsigned pl = (unsigned)L.nx * (unsigned)L.ny;
+            n.xh = __ldg(data + (c + (x < L.nx - 1)));
+            n.xl = __ldg(data + (c - (x > 0)));
+            n.yh = __ldg(data + (c + (y < L.ny - 1 ? (unsigned)L.nx : 0u)));
+            n.yl = __ldg(data + (c - (y > 0 ? (unsigned)L.nx : 0u)));
+            n.zh = __ldg(data + (c + (z < L.nz - 1 ? pl : 0u)));
+            n.zl = __ldg(data + (c - (z > 0 ? pl : 0u)));
         }
     };
     // ring: voxel j + d * step has its neighbours issued (d < D - 1) and its
@@ -331,7 +337,8 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
     for (int base = 0; base < ball.count; base += step) {
         const int j = base + tid;
         const int pc = pk[0];
-        const Nb6 cur = nb[0];
+        Nb6 cur0 = nb[0];
+        cur0.sx = cur0.sy = cur0.sz = 0.5f;
 #pragma unroll
         for (int d = 0; d + 1 < D; ++d) {
             pk[d] = pk[d + 1];
@@ -341,7 +348,16 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
             issue(pk[D - 2], nb[D - 2]);
             if (j + D * step < ball.count) pk[D - 1] = __ldg(offs + j + D * step);
         }
-        if (j < ball.count && (INTERIOR || cur.sx != 0.f)) {
+        bool in = j < ball.count;
+        Nb6 cur = cur0;
+        if (!INTERIOR && in) {
+            const int x = kp.ix + unpack_off(pc, 0), y = kp.iy + unpack_off(pc, 1), z = kp.iz + unpack_off(pc, 2);
+            in = x >= 0 && y >= 0 && z >= 0 && x < L.nx && y < L.ny && z < L.nz;
+            cur.sx = (x > 0 && x < L.nx - 1) ? 0.5f : 1.0f;
+            cur.sy = (y > 0 && y < L.ny - 1) ? 0.5f : 1.0f;
+            cur.sz = (z > 0 && z < L.nz - 1) ? 0.5f : 1.0f;
+        }
+        if (in) {
             ++cnt;
             float gx, gy, gz;
             grad32(cur, gx, gy, gz);

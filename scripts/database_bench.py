@@ -86,10 +86,33 @@ nd = torch.tensor([sum(len(d) for d in descs.values())], device="cuda")
 dist.all_reduce(nd)
 kept = torch.tensor([sum(int(v[3].sum()) for v in res.values())], device="cuda")
 dist.all_reduce(kept)
+spot = None
+if world == 1 and len(descs) >= 3:
+    # spot-check 3 subjects against the reference composition (match.py:81-121 applied to the
+    # subject's rows vs the concatenation of every other subject, in id order), evaluated with the
+    # independent dp4a kernel (vk_set_match_path(1)): best index, d1, d2 and ratio decision
+    ids = sorted(descs)
+    picks = [ids[0], ids[len(ids) // 2], ids[-1]]
+    spot = {"subjects": picks, "equal": True, "kernel": "dp4a (vk_set_match_path 1)"}
+    _lib.call("vk_set_match_path", 1)
+    try:
+        for i in picks:
+            a8 = np.ascontiguousarray(descs[i].astype(np.int8))
+            b8 = np.ascontiguousarray(np.concatenate([descs[j] for j in ids if j != i]).astype(np.int8))
+            A, Bm = torch.from_numpy(a8).cuda(), torch.from_numpy(b8).cuda()
+            n = len(a8)
+            out = [torch.empty(n, dtype=dt, device="cuda") for dt in (torch.int32, torch.float64, torch.float64, torch.uint8)]
+            _lib.call("vk_match", 1, A.data_ptr(), n, Bm.data_ptr(), len(b8), 64, 0.9, *[o.data_ptr() for o in out],
+                      _lib.stream_ptr())
+            got = [o.cpu().numpy() for o in out]
+            spot["equal"] = spot["equal"] and all(np.array_equal(np.asarray(x), np.asarray(y)) for x, y in zip(got, res[i]))
+    finally:
+        _lib.call("vk_set_match_path", 0)
 if rank == 0:
     total = int(nd.item())
     print(json.dumps({"workload": "configs[4]: database matching, SIFT-Rank", "subjects": a.subjects, "n_gpus": world,
                       "descriptors": total, "extract_ms": round(float(t[0]), 1), "gather_match_ms": round(float(t[1]), 1),
                       "wall_ms": round(float(t[2]), 1), "ratio_test_kept": int(kept.item()),
-                      "pairs": total * total, "pairs_per_s_match": round(total * total / (float(t[1]) / 1e3))}))
+                      "pairs": total * total, "pairs_per_s_match": round(total * total / (float(t[1]) / 1e3)),
+                      "spot_check": spot}))
 dist.destroy_process_group()
