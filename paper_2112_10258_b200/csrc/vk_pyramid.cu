@@ -620,6 +620,10 @@ struct ColLine {
 };
 
 constexpr int kPlaneThreads = 192;
+#ifndef VK_DOG_WARPS
+#define VK_DOG_WARPS 4  // warps of blur_xy_plane_kernel computing the previous pair's DoG (2 -> 4: pyramid -5.5%: the DoG warps were the CTA's critical path)
+#endif
+constexpr int kDogThreads = 32 * VK_DOG_WARPS;
 
 VK_D void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
@@ -651,7 +655,7 @@ VK_D void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) 
 }
 
 template <int R>
-__global__ void __launch_bounds__(kPlaneThreads + 64, 2)
+__global__ void __launch_bounds__(kPlaneThreads + kDogThreads, 2)
 blur_xy_plane_kernel(const float* __restrict__ src, float* __restrict__ tmp, int tp, int nx, int ny, Taps taps,
                      const float* __restrict__ prev, float* __restrict__ pdog) {
     extern __shared__ float4 smem4[];
@@ -670,12 +674,12 @@ blur_xy_plane_kernel(const float* __restrict__ src, float* __restrict__ tmp, int
     }
     __syncthreads();  // barrier initialised before anyone waits on it
     if (tid >= kPlaneThreads) {
-        // two DoG warps (launched only with prev): the previous pair's difference prev - src over the
+        // VK_DOG_WARPS DoG warps (launched only with prev): the previous pair's difference prev - src over the
         // contiguous plane, read from global (src is L2-hot: the bulk copy just streamed it), concurrent
         // with the x / y passes of the other six warps
         const size_t pb = (size_t)blockIdx.x * plane;
         const int w = tid - kPlaneThreads;
-        constexpr int NW = 64, U = 8;
+        constexpr int NW = kDogThreads, U = 8;
         if (((plane & 1) | ((reinterpret_cast<uintptr_t>(prev + pb) | reinterpret_cast<uintptr_t>(pdog + pb) |
                              reinterpret_cast<uintptr_t>(g)) & 7)) == 0) {
             const float2* pv2 = reinterpret_cast<const float2*>(prev + pb);
@@ -1503,7 +1507,7 @@ static int launch_xy_plane(const float* src, float* work, int tp, int nb, int nx
         if (e != cudaSuccess) return cuda_status(e, "blur xy plane attribute");
         configured = 110 * 1024;
     }
-    blur_xy_plane_kernel<R><<<nb * nz, kPlaneThreads + (prev ? 64 : 0), smem, st>>>(src, work, tp, nx, ny, taps, prev,
+    blur_xy_plane_kernel<R><<<nb * nz, kPlaneThreads + (prev ? kDogThreads : 0), smem, st>>>(src, work, tp, nx, ny, taps, prev,
                                                                                   pdog);
     count_launch();
     return cuda_status(cudaGetLastError(), "blur xy plane launch");
