@@ -1042,7 +1042,7 @@ blur_z4_kernel(const float* __restrict__ tmp, int tp, const float* __restrict__ 
 constexpr int kZtSlots = VK_ZT_SLOTS;
 constexpr int kZtTmpFloats = 32 * 16;   // tmp tile floats per slot (2 KB)
 constexpr int kZtSrcPitch = 40;         // floats per staged source row (<= 36 used)
-constexpr int kZtSrcFloats = 16 * kZtSrcPitch;
+constexpr int kZtSrcFloats = VK_ZT_SRC_TMA ? 16 * kZtSrcPitch : 0;  // (no staging slots unless used)
 #ifndef VK_ZT_TSTORE
 #define VK_ZT_TSTORE 0  // 1: warp-transposed row stores (measured slower: 214 vs 126 us at R = 10)
 #endif
