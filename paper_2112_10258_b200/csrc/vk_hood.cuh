@@ -16,17 +16,26 @@
 namespace vk {
 
 // Each CTA accumulates into kVoteCopies copies of its histogram, lane l
-// voting into copy l % kVoteCopies: lanes of one warp that pick the same bin
-// hit different L2 addresses instead of serialising on one.  The copies are
-// summed when the histogram is read (fp64, any order: the bounds hold for
-// every summation order).
+// voting into copy l % kVoteCopies; the copies are summed when the histogram
+// is read (fp64, any order: the bounds hold for every summation order).
+// Measured on B200 after the walks were pipelined: 2 copies make the
+// SIFT-Rank walk 13% faster than 1 (4: same as 2, 8 / 16: slower; spreading
+// the entries of one copy over more sectors, VK_BIN_STRIDE, slower).
 #ifndef VK_VOTE_COPIES
-#define VK_VOTE_COPIES 1
+#define VK_VOTE_COPIES 2
 #endif
 constexpr int kVoteCopies = VK_VOTE_COPIES;
+// Histogram entry i lives at hist[i * kBinStride] (entries spread over more
+// L2 sectors / slices).
+#ifndef VK_BIN_STRIDE
+#define VK_BIN_STRIDE 1
+#endif
+constexpr int kBinStride = VK_BIN_STRIDE;
 // Doubles per copy (>= VK_MAX_FRAMES x 64 SIFT-Rank bins and >= VK_MAX_DIRS
-// orientation bins).
-constexpr int kCopyStride = VK_MAX_FRAMES * 64;
+// orientation bins, times the entry stride).
+constexpr int kCopyStride = VK_MAX_FRAMES * 64 * kBinStride;
+// Offset of SIFT-Rank frame f's 64 bins: hist + f * kHistFrame.
+constexpr int kHistFrame = 64 * kBinStride;
 // Histogram slots per CTA in the accumulation workspace.
 constexpr int kAccumSlot = kCopyStride * kVoteCopies;
 // Persistent grids launch at most this many CTAs per SM.
@@ -52,19 +61,19 @@ inline int accum_grid(Kernel kernel, int threads, int n_items, size_t dyn_smem =
 VK_D double* vote_copy(double* hist) { return hist + (threadIdx.x & (kVoteCopies - 1)) * kCopyStride; }
 
 VK_D void red_vote(double* hist, int bin, float v) {
-    if (bin >= 0) atomicAdd(hist + bin, (double)v);  // result unused -> RED.E.ADD.F64.RN
+    if (bin >= 0) atomicAdd(hist + bin * kBinStride, (double)v);  // result unused -> RED.E.ADD.F64.RN
 }
 
 // Zero the first n entries of every copy (the caller synchronises).
 VK_D void zero_hist(double* hist, int n) {
-    for (int i = threadIdx.x; i < n * kVoteCopies; i += blockDim.x) hist[(i / n) * kCopyStride + i % n] = 0.0;
+    for (int i = threadIdx.x; i < n * kVoteCopies; i += blockDim.x) hist[(i / n) * kCopyStride + (i % n) * kBinStride] = 0.0;
 }
 
 // Entry i summed over the copies, after a __syncthreads (L2, bypassing L1).
 VK_D double read_hist(const double* hist, int i) {
-    double s = __ldcg(hist + i);
+    double s = __ldcg(hist + i * kBinStride);
 #pragma unroll
-    for (int c = 1; c < kVoteCopies; ++c) s += __ldcg(hist + c * kCopyStride + i);
+    for (int c = 1; c < kVoteCopies; ++c) s += __ldcg(hist + c * kCopyStride + i * kBinStride);
     return s;
 }
 

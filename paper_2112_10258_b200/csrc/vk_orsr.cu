@@ -227,7 +227,7 @@ VK_D void sr_walk_sphere(const vk_kp& kp, const vk_level& L, const float* data, 
                     int sure;
                     const int bin = sr_bin_try(ox, oy, oz, gx, gy, gz, Rc + kRcPerFrame * f, sure);
                     if (sure == 3) {
-                        red_vote(hist + f * kSrBins, bin, mag);
+                        red_vote(hist + f * kHistFrame, bin, mag);
                     } else {
                         const int pos = atomicAdd(qcount, 1);
                         queue[pos] = make_int4(e.x, f | (bin << 2) | (sure << 8), __float_as_int(mag), 0);
@@ -263,7 +263,7 @@ VK_D void sr_walk_sphere_frames(const vk_kp& kp, const vk_level& L, const float*
         const int n = min(4, F - f0);
         const double* R = Rs + 9 * f0;
         const float4* C = Rc + kRcPerFrame * f0;
-        double* h = hist + kSrBins * f0;
+        double* h = hist + kHistFrame * f0;
         switch (n) {
             case 1: sr_walk_sphere<1, INTERIOR>(kp, L, data, box, ent, count, R, C, h, n, queue, qcount); break;
             case 2: sr_walk_sphere<2, INTERIOR>(kp, L, data, box, ent, count, R, C, h, n, queue, qcount); break;

@@ -261,7 +261,7 @@ VK_D int sr_walk(const vk_kp& kp, const vk_level& L, const float* data, const fl
             const int bin = has ? sr_bin_fast(ox, oy, oz, gx, gy, gz, Rs + 9 * f, Rc + kRcPerFrame * f, data, L.nx, L.ny, L.nz, x,
                                               y, z)
                                 : -1;
-            red_vote(hist + f * kSrBins, bin, mag);
+            red_vote(hist + f * kHistFrame, bin, mag);
         }
     }
     return cnt;
@@ -282,7 +282,7 @@ VK_D void sr_resolve(int4 e, const vk_kp& kp, const vk_level& L, const float* da
     const int sp = (sure & 1) ? (bin >> 3) : sr_obits_exact(ox, oy, oz, Rs + 9 * f);
     const int og = (sure & 2) ? (bin & 7) : sr_gbits_exact(data, L.nx, L.ny, L.nz, kp.ix + ox, kp.iy + oy, kp.iz + oz,
                                                            Rs + 9 * f);
-    red_vote(hist + f * kSrBins, 8 * sp + og, __int_as_float(e.z));
+    red_vote(hist + f * kHistFrame, 8 * sp + og, __int_as_float(e.z));
 }
 #ifndef VK_SR_DEPTH
 #define VK_SR_DEPTH 2  // voxels in flight per thread (sr_walk_pipe)
@@ -373,7 +373,7 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
                     int sure;
                     const int bin = sr_bin_try(ox, oy, oz, gx, gy, gz, Rc + kRcPerFrame * f, sure);
                     if (sure == 3) {
-                        red_vote(hist + f * kSrBins, bin, mag);
+                        red_vote(hist + f * kHistFrame, bin, mag);
                     } else {
                         const int pos = atomicAdd(qcount, 1);
                         queue[pos] = make_int4(pc, f | (bin << 2) | (sure << 8), __float_as_int(mag), 0);
@@ -381,7 +381,7 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
 #else
                     const int bin = sr_bin_fast(ox, oy, oz, gx, gy, gz, Rs + 9 * f, Rc + kRcPerFrame * f, data, L.nx,
                                                 L.ny, L.nz, kp.ix + ox, kp.iy + oy, kp.iz + oz);
-                    red_vote(hist + f * kSrBins, bin, mag);
+                    red_vote(hist + f * kHistFrame, bin, mag);
 #endif
                 }
             }
@@ -436,7 +436,7 @@ VK_D int sr_walk_frames(const vk_kp& kp, const vk_level& L, const float* data, c
         case 4: return sr_walk<4, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F);
         default: {  // > 4 frames: two passes of up to 4 frames
             const int cnt = sr_walk<4, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, 4);
-            sr_walk<4, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs + 36, Rc + 4 * kRcPerFrame, hist + 4 * kSrBins, F - 4);
+            sr_walk<4, INTERIOR>(kp, L, data, g4, ball, ball_offsets, Rs + 36, Rc + 4 * kRcPerFrame, hist + 4 * kHistFrame, F - 4);
             return cnt;
         }
     }
