@@ -367,7 +367,7 @@ VK_D int ori_walk(const vk_kp& kp, const vk_level& L, const float* data, const v
 #define VK_ORI_PIPE 1
 #endif
 #ifndef VK_ORI_DEPTH
-#define VK_ORI_DEPTH 3  // voxels in flight per thread (measured: 2 -> 3 is 2% faster, B200)
+#define VK_ORI_DEPTH 2  // voxels in flight per thread (3 was 2% faster than 2 with one vote copy; 2 is 1% faster with two)
 #endif
 template <bool INTERIOR>
 VK_D int ori_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
