@@ -39,7 +39,10 @@ def hamming_distances(a_packed: np.ndarray, b_packed: np.ndarray) -> np.ndarray:
 
 
 def euclidean_distances(a: np.ndarray, b: np.ndarray) -> np.ndarray:
-    """match.py:70-78 (full matrix, fp64 on the GPU)."""
+    """match.py:70-78 (full matrix, fp64 on the GPU).  Integer-valued rows
+    (ranks, int8 values) give the reference's matrix bit for bit (every product
+    and sum is an exact fp64 integer); non-integer float rows follow cuBLAS's
+    summation order rather than OpenBLAS's (last-ulp differences)."""
     t = _lib.torch()
     A = t.from_numpy(np.asarray(a, dtype=np.float64)).cuda()
     B = t.from_numpy(np.asarray(b, dtype=np.float64)).cuda()

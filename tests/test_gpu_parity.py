@@ -674,3 +674,24 @@ def test_fused_orientation_siftrank_equals_separate_and_exact(radius_factor):
         assert np.array_equal(a["frame_prim"], b["frame_prim"]) and np.array_equal(a["frame_sec"], b["frame_sec"])
         assert np.array_equal(a["rot"], b["rot"])
         assert np.array_equal(a["desc"], b["desc"]), f"fused descriptors differ from {other}"
+
+
+def test_full_distance_matrices_match_oracle():
+    """match.py:64-78 full-matrix helpers on the GPU: popcount distances of
+    packed bits and fp64 euclidean distances of integer rows (ranks, int8
+    values: every product and sum is an exact fp64 integer, so the result is
+    the reference's bit for bit; non-integer float rows follow cuBLAS's
+    summation order instead of OpenBLAS's)."""
+    from oracle import volkey_oracle as O
+
+    rng = np.random.default_rng(8)
+    a = rng.integers(0, 256, size=(57, 16)).astype(np.uint8)
+    b = rng.integers(0, 256, size=(91, 16)).astype(np.uint8)
+    got = vk.match.hamming_distances(a, b)
+    assert np.array_equal(got, O.hamming(a, b))
+    for lo, hi, dim in ((0, 64, 64), (-128, 128, 96)):
+        a = rng.integers(lo, hi, size=(63, dim)).astype(np.int64)
+        b = rng.integers(lo, hi, size=(77, dim)).astype(np.int64)
+        b[5] = a[3]  # an exact zero distance
+        got = vk.match.euclidean_distances(a, b)
+        assert np.array_equal(got, O.euclid(a, b))

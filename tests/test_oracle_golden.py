@@ -149,3 +149,16 @@ def test_brain_pyramid_and_keypoints():
     kps = O.detect(dg)
     assert len(kps) == 1924
     assert np.array_equal(np.array([k.position for k in kps]), g["kp_pos"])
+
+
+def test_brain_frames_and_siftrank():
+    """configs[0] end to end through the oracle: orientation frames (3400) and
+    SIFT-Rank descriptors equal the reference's (the GPU path is checked against
+    the same golden in test_gpu_parity.test_brain_volume)."""
+    g = load_golden("brain.npz")
+    vol = synthetic.brain_volume()
+    res = O.extract(vol, descriptor="siftrank")
+    assert len(res["oriented"]) == len(g["fr_rot"]) == 3400
+    assert np.array_equal(np.array([np.asarray(R) for _, R in res["oriented"]]).reshape(-1, 3, 3), g["fr_rot"])
+    recs, _ = O.describe(res["pyramid"], res["oriented"], "siftrank")
+    assert np.array_equal(O.desc_array(recs, "siftrank").astype(np.int64), g["desc_siftrank"].astype(np.int64))
