@@ -351,7 +351,14 @@ match_i8_tc_kernel(const uint8_t* __restrict__ a, int na, const uint8_t* __restr
 // MMA and epilogue overlap tile by tile.  Same integer arithmetic, tie order
 // and merge as match_i8_tc_kernel.
 constexpr int kWsM = 256, kWsN = 128, kWsStages = 8;
-constexpr int kWsThreads = 320;  // producer warp, MMA warp, 8 epilogue warps
+#ifndef VK_WS_EPI_WARPS
+#define VK_WS_EPI_WARPS 8  // epilogue warps: 8 (one query row x 128 columns each) or 16 (x 64 columns; measured
+                           // 8.96 vs 12.5 Tpairs/s: 113-register budget at 576 threads)
+#endif
+constexpr int kWsEpi = VK_WS_EPI_WARPS;
+static_assert(kWsEpi == 8 || kWsEpi == 16, "8 or 16 epilogue warps");
+constexpr int kWsCols = kWsN * 8 / kWsEpi;  // columns of a tile per epilogue thread
+constexpr int kWsThreads = 64 + 32 * kWsEpi;  // producer warp, MMA warp, epilogue warps
 
 template <int KB>
 struct WsGeom {
@@ -363,7 +370,8 @@ struct WsGeom {
     static constexpr int A_BYTES = kWsM * KBYTES;
     static constexpr int B_BYTES = kWsN * KBYTES;
     static constexpr int OFF_B = A_BYTES;
-    static constexpr int OFF_BAR = OFF_B + kWsStages * B_BYTES;
+    static constexpr int OFF_X = OFF_B + kWsStages * B_BYTES;  // column-part exchange (16 epilogue warps)
+    static constexpr int OFF_BAR = OFF_X + kWsM * 16;
     static constexpr int SMEM = OFF_BAR + 256;
 };
 
@@ -408,7 +416,7 @@ match_i8_ws_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
         }
         for (int x = 0; x < 2; ++x) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(accf(x)));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(acce(x)));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(acce(x)), "n"(kWsEpi));
         }
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(afull));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -476,8 +484,9 @@ match_i8_ws_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
         }
         __syncwarp();
     } else {
-        // ---- epilogue: query row q, all 128 columns of each tile
-        const int m = (warp - 2) >> 2;
+        // ---- epilogue: query row q, kWsCols columns (column part h) of each tile
+        const int e = warp - 2;
+        const int m = (e >> 2) & 1, h = e >> 3;  // query half, column part
         const int lr = 32 * (warp & 3) + lane;
         const int q = q0 + 128 * m + lr;
         const unsigned trow = tmem + ((unsigned)(32 * (warp & 3)) << 16);
@@ -486,18 +495,18 @@ match_i8_ws_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
         Top2 best{INT_MAX, INT_MAX, -1};
         int ex_lo = ex_lo_all, ex_hi = ex_hi_all;
         if (row_ex != nullptr) {
-            const int2 e = row_ex[min(q, na - 1)];
-            ex_lo = e.x;
-            ex_hi = e.y;
+            const int2 e2 = row_ex[min(q, na - 1)];
+            ex_lo = e2.x;
+            ex_hi = e2.y;
         }
         for (int it = 0; it < nt; ++it) {
             const int x = it & 1;
             ws_wait(accf(x), (unsigned)(it >> 1) & 1u);
             tc_fence_after();
-            int v[128];
-            const unsigned tcol = trow + (unsigned)((2 * x + m) * kWsN);
+            int v[kWsCols];
+            const unsigned tcol = trow + (unsigned)((2 * x + m) * kWsN + kWsCols * h);
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4)
+            for (int c4 = 0; c4 < kWsCols / 32; ++c4)
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
                     "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
@@ -515,13 +524,13 @@ match_i8_ws_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
             tc_fence_before();
             __syncwarp();
             if (lane == 0) ws_arrive(acce(x));  // the accumulator may be overwritten (tile it + 2)
-            const int j0 = (t_first + it) * kWsN;
-            if (!((j0 + kWsN > nb) || (j0 < ex_hi && j0 + kWsN > ex_lo))) {
+            const int j0 = (t_first + it) * kWsN + kWsCols * h;
+            if (!((j0 + kWsCols > nb) || (j0 < ex_hi && j0 + kWsCols > ex_lo))) {
                 if (eq) {
                     // d' = C - 2 a.b: only dots above T = floor((C - m2) / 2) can enter the top 2
                     int T = (int)(((long long)cnorm - best.m2) >> 1);
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) {
+                    for (int g = 0; g < kWsCols / 32; ++g) {
                         const int* w = v + 32 * g;
                         int mx = __vimax3_s32(w[0], w[1], w[2]);
 #pragma unroll
@@ -536,7 +545,7 @@ match_i8_ws_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
                 } else {
                     const int* nt_ = bnorm + j0;
 #pragma unroll
-                    for (int g = 0; g < 16; ++g) {
+                    for (int g = 0; g < kWsCols / 8; ++g) {
                         const int4 na_ = __ldg(reinterpret_cast<const int4*>(nt_ + 8 * g));
                         const int4 nb_ = __ldg(reinterpret_cast<const int4*>(nt_ + 8 * g + 4));
                         const int* w = v + 8 * g;
@@ -558,15 +567,32 @@ match_i8_ws_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
                         }
                     }
                 }
-            } else {  // ragged last tile or excluded rows inside this tile
+            } else {  // ragged last tile or excluded rows inside this column part
 #pragma unroll
-                for (int k = 0; k < kWsN; ++k) {
+                for (int k = 0; k < kWsCols; ++k) {
                     const int j = j0 + k;
                     if (j < nb && (j < ex_lo || j >= ex_hi)) top2_push(best, __ldg(bnorm + j) - 2 * v[k], j);
                 }
             }
         }
-        if (q < na) {
+        if (kWsEpi == 16) {
+            // merge the two column parts of each row (epilogue warps only: named barrier 1); the parts
+            // interleave by tile, so ties go to the lower column index
+            int4* xch = reinterpret_cast<int4*>(smem + G::OFF_X);
+            if (h == 1) xch[128 * m + lr] = make_int4(best.m1, best.m2, best.i1, 0);
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kWsEpi) : "memory");
+            if (h == 0) {
+                const int4 o = xch[128 * m + lr];
+                if (o.x < best.m1 || (o.x == best.m1 && (unsigned)o.z < (unsigned)best.i1)) {
+                    best.m2 = min(best.m1, o.y);
+                    best.m1 = o.x;
+                    best.i1 = o.z;
+                } else {
+                    best.m2 = min(best.m2, o.x);
+                }
+            }
+        }
+        if (q < na && (kWsEpi == 8 || h == 0)) {
             int na2 = 0;
             const uint4* row = reinterpret_cast<const uint4*>(a + (long long)q * G::KBYTES);
             for (int c = 0; c < G::CH; ++c) {
