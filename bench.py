@@ -176,6 +176,42 @@ def ncu_pyramid_traffic(batch: int):
     return tot * batch / captured_batch, os.path.relpath(path, REPO)
 
 
+def ncu_blur_kernel_dram(peak_gbs):
+    """Per blur-kernel class, from the same committed capture: DRAM bytes moved
+    per second of kernel time (serialised launches, cold cache) -- how close the
+    kernels run to the HBM peak on the traffic they actually move, beside the
+    stage roofline on compulsory bytes.  {class: {gbs, frac}} or None."""
+    import csv
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(REPO, "profiles", "r*", "pyramid_dram.csv")))
+    if not paths:
+        return None
+    rows = list(csv.reader(open(paths[-1])))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r]
+    if not hi:
+        return None
+    h = rows[hi[0]]
+    ii, ki, mi, vi = h.index("ID"), h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    per = {}
+    for r in rows[hi[0] + 1:]:
+        if len(r) > vi and "blur" in r[ki]:
+            cls = r[ki].split("(")[0].split("<")[0].replace("void ", "").strip()
+            d = per.setdefault((r[ii], cls), {})
+            d[r[mi]] = float(r[vi].replace(",", ""))
+    agg = {}
+    for (_, cls), d in per.items():
+        a = agg.setdefault(cls, [0.0, 0.0])
+        a[0] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+        a[1] += d.get("gpu__time_duration.sum", 0.0)  # ns
+    out = {}
+    for cls, (b, t) in agg.items():
+        if t > 0:
+            gbs = b / t  # bytes per ns == GB/s
+            out[cls] = {"dram_gbs": round(gbs, 1), "frac": round(gbs / peak_gbs, 3) if peak_gbs else None}
+    return out or None
+
+
 def detect_bytes(plan) -> int:
     """Detection reads each of the L-1 DoG levels once per octave."""
     L = plan.cfg.levels_per_octave
@@ -481,11 +517,12 @@ def run_ours(a):
     pbytes = pyramid_bytes(plan) * Bs
     achieved = pbytes / (stage_ms["pyramid"] / 1e3) / 1e9
     traffic, tsrc = ncu_pyramid_traffic(Bs)
-    roofline = {"bound": "hbm", "kernel": "blur_xy_kernel + blur_z_kernel (split separable blur, fused DoG + subsample), "
-                                          "all pyramid launches",
+    roofline = {"bound": "hbm", "kernel": "blur_xy_plane_kernel + blur_zt_kernel (split separable blur, fused DoG + "
+                                          "subsample), all pyramid launches",
                 "achieved": round(achieved, 1), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": round(achieved / peaks["hbm_gbs"], 4) if peaks.get("hbm_gbs") else None,
                 "traffic": round(traffic) if traffic else None, "traffic_source": tsrc,
+                "kernel_dram": ncu_blur_kernel_dram(peaks.get("hbm_gbs")),
                 "algorithmic_bytes": pbytes,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"}
     det_gbs = detect_bytes(plan) * Bs / (stage_ms["detect"] / 1e3) / 1e9
