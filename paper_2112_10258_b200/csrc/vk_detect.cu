@@ -117,7 +117,7 @@ VK_D float min3f(float a, float b, float c) {
 }
 
 #ifndef VK_DET_ROWS
-#define VK_DET_ROWS 2
+#define VK_DET_ROWS 4  // output rows per thread (2 -> 4: detection -6% on B200)
 #endif
 constexpr int kDetRows = VK_DET_ROWS;  // output rows per thread
 __global__ void __launch_bounds__(128)
