@@ -273,10 +273,12 @@ VK_D void sr_walk_sphere_frames(const vk_kp& kp, const vk_level& L, const float*
     }
 }
 
-#ifndef VK_OS_MIN_BLOCKS
-#define VK_OS_MIN_BLOCKS 2
-#endif
-__global__ void __launch_bounds__(kOsThreads, VK_OS_MIN_BLOCKS)
+// STAGE = false: the same fused per-keypoint pipeline without the shared
+// sphere -- both walks gather from global memory (the separate kernels' walks),
+// the SIFT-Rank walk right after the orientation walk on L1 / L2-warm data,
+// at 3 CTAs/SM (the 58 KB CTA state only).
+template <bool STAGE>
+__global__ void __launch_bounds__(kOsThreads, STAGE ? 2 : 3)
 orsr_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, int n_kp_max,
             const vk_level* __restrict__ levels, const vk_ball* __restrict__ balls,
             const int* __restrict__ ball_offsets, const double* __restrict__ windows,
@@ -315,11 +317,13 @@ orsr_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, int
         const int4 sb = sph_ball[kp.ball];  // rows start, n_rows, compact size, entries start
         const bool interior = ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz);
         __syncthreads();  // the previous item is done with box and the shared state
-        if (interior)
-            stage_sphere<false>(data, L.nx, L.ny, L.nz, kp, sph_rows + sb.x, sb.y, box);
-        else
-            stage_sphere<true>(data, L.nx, L.ny, L.nz, kp, sph_rows + sb.x, sb.y, box);
-        {
+        if (STAGE) {
+            if (interior)
+                stage_sphere<false>(data, L.nx, L.ny, L.nz, kp, sph_rows + sb.x, sb.y, box);
+            else
+                stage_sphere<true>(data, L.nx, L.ny, L.nz, kp, sph_rows + sb.x, sb.y, box);
+        }
+        if (STAGE) {
             const int next = item + gridDim.x;
             if (next < n_kp) {
                 const vk_kp nk = kps[next];
@@ -336,15 +340,22 @@ orsr_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, int
             sh.o.n_inside = 0;
             sh.o.repair = 0;
         }
-        cp_async_wait<0>();
+        if (STAGE) cp_async_wait<0>();
         __syncthreads();
         // ---- orientation walk (orient.py:89-125)
         const int4* ent = sph_ent + sb.w;
-        const int inside_cnt =
-            interior ? ori_walk_sphere<true>(kp, L, data, box, ent, ball.count, windows32 + ball.window_start,
-                                             sh.o.dirs, &sh.ic, sh.lut, hist, sh.o.queue[wid])
-                     : ori_walk_sphere<false>(kp, L, data, box, ent, ball.count, windows32 + ball.window_start,
-                                              sh.o.dirs, &sh.ic, sh.lut, hist, sh.o.queue[wid]);
+        int inside_cnt;
+        if (STAGE)
+            inside_cnt =
+                interior ? ori_walk_sphere<true>(kp, L, data, box, ent, ball.count, windows32 + ball.window_start,
+                                                 sh.o.dirs, &sh.ic, sh.lut, hist, sh.o.queue[wid])
+                         : ori_walk_sphere<false>(kp, L, data, box, ent, ball.count, windows32 + ball.window_start,
+                                                  sh.o.dirs, &sh.ic, sh.lut, hist, sh.o.queue[wid]);
+        else
+            inside_cnt = interior ? ori_walk_pipe<true>(kp, L, data, ball, ball_offsets, windows32 + ball.window_start,
+                                                        sh.o.dirs, &sh.ic, sh.lut, hist, sh.o.queue[wid])
+                                  : ori_walk<false>(kp, L, data, ball, ball_offsets, windows32 + ball.window_start,
+                                                    sh.o.dirs, &sh.ic, sh.lut, K, hist, sh.o.queue[wid]);
         if (inside_cnt) atomicAdd(&sh.o.n_inside, inside_cnt);
         __syncthreads();
         const int n_inside = sh.o.n_inside;
@@ -404,12 +415,20 @@ orsr_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, int
         zero_hist(hist, F * kSrBins);
         __syncthreads();
         // ---- SIFT-Rank walk (descriptor.py:227-263) on the same stencils
-        if (interior)
+        if (!STAGE) {
+            if (interior)
+                sr_walk_frames<true>(kp, L, data, nullptr, ball, ball_offsets, sh.Rs, sh.Rc, hist, F, sh.sq[wid],
+                                     sh.sqn + wid);
+            else
+                sr_walk_frames<false>(kp, L, data, nullptr, ball, ball_offsets, sh.Rs, sh.Rc, hist, F, sh.sq[wid],
+                                      sh.sqn + wid);
+        } else if (interior) {
             sr_walk_sphere_frames<true>(kp, L, data, box, ent, ball.count, sh.Rs, sh.Rc, hist, F, sh.sq[wid],
                                         sh.sqn + wid);
-        else
+        } else {
             sr_walk_sphere_frames<false>(kp, L, data, box, ent, ball.count, sh.Rs, sh.Rc, hist, F, sh.sq[wid],
                                          sh.sqn + wid);
+        }
         __syncthreads();
         // ---- certified stable ranks, all frames of the keypoint (siftrank_kernel)
         const double epsrel = 2.0 * (kVoteRel + gamma_k((double)n_inside + 64.0));
@@ -489,18 +508,20 @@ extern "C" int vk_orient_siftrank(const vk_kp* kps, const int* n_kp_dev, int n_k
                                   const int* sph_ent, int box_cap, double* work, void* stream) {
     if (!kps || n_kp_max < 0 || !levels || !balls || !ball_offsets || !windows || !windows32 || !dirs || K != 42 ||
         !pair_ok || !rot_table || !nframes || !prim || !sec || !desc_kp || !status || !ico_host || !ico_lut ||
-        !sph_ball || !sph_rows || !sph_ent || box_cap < 1 || box_cap > 40000 || !work || max_frames < 1 ||
+        !sph_ball || !sph_rows || !sph_ent || box_cap < 0 || box_cap > 40000 || !work || max_frames < 1 ||
         max_frames > VK_MAX_FRAMES || !(secondary_ratio > 0.0 && secondary_ratio <= 1.0)) {
         set_error("vk_orient_siftrank: bad arguments (K=%d max_frames=%d box_cap=%d)", K, max_frames, box_cap);
         return VK_ERR_PARAMETER;
     }
     if (n_kp_max == 0) return VK_OK;
     const size_t dyn = kOsStateBytes + (size_t)box_cap * sizeof(float);
-    static size_t configured = 0;
-    if (dyn > configured) {
-        cudaError_t e = cudaFuncSetAttribute(orsr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    static size_t configured[2] = {0, 0};
+    const int stage = box_cap > 0;
+    if (dyn > configured[stage]) {
+        cudaError_t e = cudaFuncSetAttribute(stage ? orsr_kernel<true> : orsr_kernel<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         if (e != cudaSuccess) return cuda_status(e, "orsr smem attribute");
-        configured = dyn;
+        configured[stage] = dyn;
     }
     IcoT ico{};
     ico.valid = 1;
@@ -509,8 +530,9 @@ extern "C" int vk_orient_siftrank(const vk_kp* kps, const int* n_kp_dev, int n_k
         for (int m = 0; m < 5; ++m) ico.adj[v][m] = ico_host[12 + 5 * v + m];
         for (int m = 0; m < 5; ++m) ico.kind[v][m] = ico_host[72 + 5 * v + m];
     }
-    const int grid = accum_grid(orsr_kernel, kOsThreads, n_kp_max, dyn);
-    orsr_kernel<<<grid, kOsThreads, dyn, as_stream(stream)>>>(
+    auto* kern = stage ? orsr_kernel<true> : orsr_kernel<false>;
+    const int grid = accum_grid(kern, kOsThreads, n_kp_max, dyn);
+    kern<<<grid, kOsThreads, dyn, as_stream(stream)>>>(
         kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets, windows, windows32, dirs, K, pair_ok, secondary_ratio,
         max_frames, rot_table, nframes, prim, sec, desc_kp, status, ico, ico_lut,
         reinterpret_cast<const int4*>(sph_ball), reinterpret_cast<const int4*>(sph_rows),

@@ -165,7 +165,7 @@ class Extractor:
 
     def __init__(self, dims, cfg: PipelineConfig | None = None, batch: int = 1, kp_cap: int | None = None,
                  frame_cap: int | None = None, exact_only: bool = False, input=None, gradient_volumes: bool = False,
-                 orient_field: bool = False, cand_cap: int | None = None, fused: bool | None = None,
+                 orient_field: bool = False, cand_cap: int | None = None, fused: bool | str | None = None,
                  refine: bool = False):
         t = _lib.torch()
         self.cfg = cfg or PipelineConfig()
@@ -273,9 +273,12 @@ class Extractor:
         # within the staging cap.  Off by default (fused=None -> VK_FUSED, default 0): on B200
         # its 2 CTAs/SM (shared-memory bound) measured slower than the separate latency-bound
         # kernels at 3-4 CTAs/SM
-        want = fused if fused is not None else os.environ.get("VK_FUSED", "0") == "1"
+        # fused="global" (or VK_FUSED=2): the fused kernel without the staged spheres (both walks
+        # gather from global memory, the SIFT-Rank walk on L1 / L2-warm data)
+        want = fused if fused is not None else {"1": True, "2": "global"}.get(os.environ.get("VK_FUSED", "0"), False)
+        self.fused_stage = want is True
         self.fused = bool(want and not self.exact_only and kind == "siftrank" and not self.grad_levels
-                          and not self.field_levels and self.tables.box_fits)
+                          and not self.field_levels and (self.tables.box_fits or not self.fused_stage))
         self.desc_kp = (t.empty((self.kp_cap * self.maxf, 64), dtype=t.uint8, device="cuda") if self.fused else None)
         # volumes per pyramid chunk (enqueue_pyramid); env override for A/B runs
         self.pyr_chunk = int(os.environ.get("VK_PYR_CHUNK", "0")) or self.B
@@ -419,7 +422,7 @@ class Extractor:
                   self.maxf, tb.rot_table.data_ptr(), self.nframes.data_ptr(), self.prim.data_ptr(),
                   self.sec.data_ptr(), self.desc_kp.data_ptr(), self.status.data_ptr(), tb.ico.ctypes.data,
                   tb.ico_lut.data_ptr(), tb.sph_ball.data_ptr(), tb.sph_rows.data_ptr(), tb.sph_ent.data_ptr(),
-                  tb.box_cap, self.accum.data_ptr(), s)
+                  tb.box_cap if self.fused_stage else 0, self.accum.data_ptr(), s)
         _lib.call("vk_expand_frames", self.nframes.data_ptr(), self.prim.data_ptr(), self.sec.data_ptr(),
                   self.total.data_ptr(), self.kp_cap, self.maxf, tb.rot_table.data_ptr(), tb.K,
                   self.frames.data_ptr(), self.rot.data_ptr(), self.n_frames.data_ptr(), self.dropped.data_ptr(),

@@ -17,13 +17,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--batch", type=int, default=8)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--dims", default="145,174,145")
-ap.add_argument("--radius-factor", type=float, default=3.0, help="balls must fit the staging buffer")
+ap.add_argument("--radius-factor", type=float, default=4.0, help="staged mode: balls must fit the staging buffer")
+ap.add_argument("--mode", default="global", choices=("stage", "global"))
 a = ap.parse_args()
 dims = tuple(int(v) for v in a.dims.split(","))
 base = synthetic.soup_volume(dims, np.random.default_rng(20240817), noise=0.01)
 host = synthetic.batch_from(base, a.batch, seed=3)
 dev = torch.stack([vk.volume.to_device(v) for v in host])
-ex = Extractor(dims, vk.PipelineConfig(radius_factor=a.radius_factor), batch=a.batch, input=dev, fused=True)
+ex = Extractor(dims, vk.PipelineConfig(radius_factor=a.radius_factor), batch=a.batch, input=dev,
+               fused=True if a.mode == "stage" else "global")
 assert ex.fused, "fused path not selected"
 st = torch.cuda.current_stream()
 s = st.cuda_stream
