@@ -306,19 +306,33 @@ __global__ void extrema_from_map_kernel(const int16_t* __restrict__ map, const f
 }
 
 // Exclusive prefix of min(count, cap) over the batch; total[0] = keypoints,
-// total[1] = 1 if any volume overflowed its candidate capacity.
+// total[1] = 1 if any volume overflowed its candidate capacity.  One warp,
+// 32 volumes per shuffle scan.
 __global__ void batch_offsets_kernel(const int* __restrict__ counts, int nb, int cap, int* __restrict__ vol_offset,
                                      int* __restrict__ total) {
-    if (threadIdx.x != 0) return;
-    int acc = 0, over = 0;
-    for (int b = 0; b < nb; ++b) {
-        vol_offset[b] = acc;
-        int c = counts[b];
-        if (c > cap) { over = 1; c = cap; }
-        acc += c;
+    const int lane = threadIdx.x;
+    if (lane >= 32) return;
+    int carry = 0;
+    bool over = false;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+        const int b = b0 + lane;
+        int c = b < nb ? counts[b] : 0;
+        over = over || c > cap;
+        c = min(c, cap);
+        int v = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (b < nb) vol_offset[b] = carry + v - c;
+        carry += __shfl_sync(0xffffffffu, v, 31);
     }
-    total[0] = acc;
-    total[1] = over;
+    const bool any_over = __any_sync(0xffffffffu, over);
+    if (lane == 0) {
+        total[0] = carry;
+        total[1] = any_over ? 1 : 0;
+    }
 }
 
 // Keypoint order (detect.py:149-182: octave, level, z, y, x, peak before

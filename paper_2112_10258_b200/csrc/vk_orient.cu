@@ -5,13 +5,15 @@
 //
 // orient_kernel: one 256-thread CTA per keypoint, persistent over the keypoint
 // list (the count lives in device memory so the whole pipeline can be
-// graph-captured).  Fast path: the ball is walked in z-major order (coalesced
-// gathers); each voxel's vote is the fp32 |g| x window (within kVoteRel +
+// graph-captured), 3 CTAs/SM.  Fast path: the ball is walked in z-major order
+// (coalesced gathers; interior balls software-pipelined, the neighbour loads of
+// the next voxel in flight while the current one is binned, ori_walk_pipe);
+// each voxel's vote is the fp32 |g| x window (within kVoteRel +
 // kVoteAbs of the reference's fp64 vote) and its bin the exact nearest
 // icosphere direction (lookup table, boundary cells deferred to a per-warp
 // queue and resolved by a screened fp32 argmax with an fp64 fallback).  Votes
 // are added with fire-and-forget fp64 reductions into a per-CTA histogram in
-// L2 (any order).  Every decision the frames depend on (the top of the weight
+// L2 (two copies, by lane parity; any order).  Every decision the frames depend on (the top of the weight
 // order, the secondary_ratio threshold) is checked against a rigorous bound on
 // the difference between that sum and the reference's sequential np.add.at;
 // only the bins of an uncertain decision are re-accumulated in the reference's

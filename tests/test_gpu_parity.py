@@ -695,3 +695,19 @@ def test_full_distance_matrices_match_oracle():
         b[5] = a[3]  # an exact zero distance
         got = vk.match.euclidean_distances(a, b)
         assert np.array_equal(got, O.euclid(a, b))
+
+
+def test_batch_of_70_volumes_offsets():
+    """More volumes than a warp (batch_offsets_kernel scans 32 at a time): the
+    volume-major SoA of a 70-volume batch equals one-volume extractions."""
+    base = small_volume(load_golden("small0.npz"))[:40, :44, :36]
+    rng = np.random.default_rng(70)
+    vols = [np.ascontiguousarray(np.roll(base, int(rng.integers(0, 9)), axis=int(rng.integers(0, 3))) +
+                                 rng.normal(0, 0.01, base.shape).astype(np.float32)) for _ in range(70)]
+    res = vk.extract_batch(np.stack(vols), PipelineConfig())
+    off = list(res["vol_offset"]) + [res["n_keypoints"]]
+    assert len(res["vol_offset"]) == 70
+    for b in (0, 31, 32, 33, 63, 64, 69):
+        single = vk.extract_features(vk.Volume(vols[b]))
+        assert off[b + 1] - off[b] == len(single.keypoints), b
+        assert np.array_equal(res["pos"][off[b]:off[b + 1]], np.array([k.position for k in single.keypoints]).reshape(-1, 3))
