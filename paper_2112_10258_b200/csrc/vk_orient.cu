@@ -122,6 +122,12 @@ orient_field_kernel(const float* __restrict__ level, float* __restrict__ mag, ui
 #ifndef VK_ORI_MIN_BLOCKS
 #define VK_ORI_MIN_BLOCKS 3  // with the pipelined walk: 3 CTAs/SM without spills beat 4 with (B200)
 #endif
+// MODE 0: every keypoint, every path (exact, gradient / field volumes, staged,
+// pipelined, plain).  MODE 1 / 2: the default fast path only (lookup table, no
+// precomputed volumes), for the keypoints whose ball lies inside the volume
+// (1) or crosses its boundary (2) -- two launches, each compiled with only its
+// own pipelined walk, so neither pays the other's registers.
+template <int MODE>
 __global__ void __launch_bounds__(kOriThreads, VK_ORI_MIN_BLOCKS)
 orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, int n_kp_max,
               const vk_level* __restrict__ levels, const vk_ball* __restrict__ balls,
@@ -163,6 +169,10 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         const vk_ball ball = balls[kp.ball];
         const double* win = windows + ball.window_start;
         const float* win32 = windows32 + ball.window_start;
+        if (MODE != 0) {
+            const bool interior = ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz);
+            if ((MODE == 1) != interior) continue;  // CTA-uniform: the other launch takes this keypoint
+        }
         if (VK_PREFETCH_NEXT && item + (int)gridDim.x < n_kp) {
             const vk_kp nk = kps[item + gridDim.x];
             const vk_level NL = levels[nk.lvl];
@@ -174,7 +184,12 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         __syncthreads();
         int inside_cnt = 0;
         const vk_gradlevel GL = grads ? grads[kp.lvl] : vk_gradlevel{};
-        if (!exact_only && GL.bin != nullptr && GL.kind == 1) {
+        if constexpr (MODE != 0) {
+            inside_cnt = MODE == 1 ? ori_walk_pipe<true>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp,
+                                                         hist, sh.queue[tid >> 5])
+                                   : ori_walk_pipe<false>(kp, L, data, ball, ball_offsets, win32, sh.dirs, icp, lutp,
+                                                          hist, sh.queue[tid >> 5]);
+        } else if (!exact_only && GL.bin != nullptr && GL.kind == 1) {
             const float* fm = reinterpret_cast<const float*>(GL.g4) + (long long)kp.vol * GL.vol_stride;
             const uint8_t* fb = GL.bin + (long long)kp.vol * GL.vol_stride;
             inside_cnt = ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz)
@@ -434,11 +449,10 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
     const size_t dyn = VK_ORI_STAGED ? kStageFloats * sizeof(float) : 0;
     static bool configured = false;
     if (dyn && !configured) {
-        cudaError_t e = cudaFuncSetAttribute(orient_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaError_t e = cudaFuncSetAttribute(orient_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         if (e != cudaSuccess) return cuda_status(e, "orient smem attribute");
         configured = true;
     }
-    const int grid = accum_grid(orient_kernel, kOriThreads, n_kp_max, dyn);
     IcoT ico{};
     if (ico_host && K == 42) {
         ico.valid = 1;
@@ -448,7 +462,24 @@ extern "C" int vk_orient(const vk_kp* kps, const int* n_kp_dev, int n_kp_max, co
             for (int m = 0; m < 5; ++m) ico.kind[v][m] = ico_host[72 + 5 * v + m];
         }
     }
-    orient_kernel<<<grid, kOriThreads, dyn, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
+#ifndef VK_ORI_SPLIT
+#define VK_ORI_SPLIT 0  // 1: interior / border keypoints in two launches (measured slower: 2.11 vs 1.87 ms)
+#endif
+    const bool split = VK_ORI_SPLIT && !exact_only && !grads && ico.valid && ico_lut && !VK_ORI_STAGED;
+    if (split) {
+        for (int m = 1; m <= 2; ++m) {
+            auto* kern = m == 1 ? orient_kernel<1> : orient_kernel<2>;
+            const int grid = accum_grid(kern, kOriThreads, n_kp_max, 0);
+            kern<<<grid, kOriThreads, 0, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
+                                                              windows, windows32, dirs, K, pair_ok, secondary_ratio,
+                                                              max_frames, weights, nframes, prim, sec, status,
+                                                              exact_only, ico, ico_lut, grads, work);
+            count_launch();
+        }
+        return cuda_status(cudaGetLastError(), "orient launch");
+    }
+    const int grid = accum_grid(orient_kernel<0>, kOriThreads, n_kp_max, dyn);
+    orient_kernel<0><<<grid, kOriThreads, dyn, as_stream(stream)>>>(kps, n_kp_dev, n_kp_max, levels, balls, ball_offsets,
                                                                windows, windows32, dirs, K, pair_ok, secondary_ratio,
                                                                max_frames, weights, nframes, prim, sec, status,
                                                                exact_only, ico, ico_lut, grads, work);

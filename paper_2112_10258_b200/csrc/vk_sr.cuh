@@ -411,17 +411,18 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
     return cnt;
 }
 
-template <bool INTERIOR>
-VK_D int sr_walk_frames(const vk_kp& kp, const vk_level& L, const float* data, const float4* g4, const vk_ball& ball,
-                        const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist,
-                        int F, int4* queue, int* qcount) {
 #ifndef VK_SR_PIPE
 #define VK_SR_PIPE 1
 #endif
 #ifndef VK_SR_PIPE_BORDER
-#define VK_SR_PIPE_BORDER 0  // border-crossing balls pipelined too: needs 2 CTAs/SM (no spills); measured equal within run-to-run noise
+#define VK_SR_PIPE_BORDER 0  // border-crossing balls pipelined too in the all-keypoints kernel (register pressure)
 #endif
-    if (VK_SR_PIPE && (INTERIOR || VK_SR_PIPE_BORDER) && !g4 && F <= 4) {
+// PIPE_BORDER: also pipeline border-crossing balls (the border-only launch).
+template <bool INTERIOR, bool PIPE_BORDER = (VK_SR_PIPE_BORDER != 0)>
+VK_D int sr_walk_frames(const vk_kp& kp, const vk_level& L, const float* data, const float4* g4, const vk_ball& ball,
+                        const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist,
+                        int F, int4* queue, int* qcount) {
+    if (VK_SR_PIPE && (INTERIOR || PIPE_BORDER) && !g4 && F <= 4) {
         switch (F) {
             case 1: return sr_walk_pipe<1, INTERIOR>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
             case 2: return sr_walk_pipe<2, INTERIOR>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);

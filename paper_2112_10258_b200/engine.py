@@ -389,6 +389,11 @@ class Extractor:
             _lib.call("vk_gradient_volume", self.levels[o][i].data_ptr(), g4.data_ptr(), bn.data_ptr(), self.B, nx, ny,
                       nz, tb.dirs.data_ptr(), tb.ico.ctypes.data, s)
 
+    def _grads_ptr(self):
+        """The gradient / field level table, or NULL when no level has one (the walk kernels
+        then take their default fast path, split into interior and border launches)."""
+        return self.grad_table.data_ptr() if (self.grad_levels or self.field_levels) else None
+
     def enqueue_orient(self, s: int) -> None:
         """assign_orientations (pipeline.py:41-67)."""
         tb, cfg = self.tables, self.cfg
@@ -403,7 +408,7 @@ class Extractor:
                   tb.dirs.data_ptr(), tb.K,
                   tb.pair_ok.data_ptr(), float(cfg.secondary_ratio), self.maxf, None, self.nframes.data_ptr(),
                   self.prim.data_ptr(), self.sec.data_ptr(), self.status.data_ptr(), self.exact_only,
-                  tb.ico.ctypes.data, tb.ico_lut.data_ptr(), self.grad_table.data_ptr(), self.accum.data_ptr(), s)
+                  tb.ico.ctypes.data, tb.ico_lut.data_ptr(), self._grads_ptr(), self.accum.data_ptr(), s)
         _lib.call("vk_expand_frames", self.nframes.data_ptr(), self.prim.data_ptr(), self.sec.data_ptr(),
                   self.total.data_ptr(), self.kp_cap, self.maxf, tb.rot_table.data_ptr(), tb.K,
                   self.frames.data_ptr(), self.rot.data_ptr(), self.n_frames.data_ptr(), self.dropped.data_ptr(),
@@ -439,7 +444,7 @@ class Extractor:
                       self.nframes.data_ptr(), self.total.data_ptr(), self.kp_cap, self.maxf, self.kps.data_ptr(),
                       self.level_table.data_ptr(), tb.balls.data_ptr(), tb.ball_offsets.data_ptr(),
                       self.desc.data_ptr(), self.exact_only, self.status.data_ptr() + 8,
-                      self.grad_table.data_ptr(), self.accum.data_ptr(), s)
+                      self._grads_ptr(), self.accum.data_ptr(), s)
         else:
             code = KIND_CODE[cfg.descriptor]
             _lib.call("vk_describe_patch", code, self.frames.data_ptr(), self.rot.data_ptr(),
