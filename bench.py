@@ -212,6 +212,14 @@ def ncu_blur_kernel_dram(peak_gbs):
     return out or None
 
 
+def _concurrent_pyramid(plan, volumes, ms, peak_gbs):
+    """Pyramid stage of all sub-batches of one step on parallel streams (as in the step)."""
+    gbs = pyramid_bytes(plan) * volumes / (ms / 1e3) / 1e9
+    return {"volumes": volumes, "ms": round(ms, 4), "achieved": round(gbs, 1),
+            "frac": round(gbs / peak_gbs, 4) if peak_gbs else None,
+            "note": "the per-step pyramid of every sub-batch on its own stream (eager, CUDA events)"}
+
+
 def detect_bytes(plan) -> int:
     """Detection reads each of the L-1 DoG levels once per octave."""
     L = plan.cfg.levels_per_octave
@@ -398,6 +406,22 @@ def run_ours(a):
         for k, (e0, e1) in zip(stage_ms, zip(ev[:-1], ev[1:])):
             stage_ms[k].append(e0.elapsed_time(e1))
     stage_ms = {k: statistics.median(v) for k, v in stage_ms.items()}
+    # the pyramid stage of a whole step as the step runs it: the G sub-batch pyramids on G
+    # parallel streams (eager, CUDA events on the joining stream), compulsory bytes of all B volumes
+    conc_ms = []
+    for _ in range(3):
+        subs_s = [torch.cuda.Stream() for _ in groups[0].members]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for ss, ex in zip(subs_s, groups[0].members):
+            ss.wait_stream(st)
+            ex.enqueue_pyramid(ss.cuda_stream)
+        for ss in subs_s:
+            st.wait_stream(ss)
+        e1.record(st)
+        torch.cuda.synchronize()
+        conc_ms.append(e0.elapsed_time(e1))
+    pyramid_concurrent_ms = statistics.median(conc_ms)
     # ball-voxel visits of the timed sub-batch (orientation / SIFT-Rank work units)
     r0 = exs[0].results()
     bcount = exs[0].tables.balls.cpu().numpy().view(_lib.BALL_DTYPE)["count"].astype(np.int64)
@@ -523,6 +547,7 @@ def run_ours(a):
                 "frac": round(achieved / peaks["hbm_gbs"], 4) if peaks.get("hbm_gbs") else None,
                 "traffic": round(traffic) if traffic else None, "traffic_source": tsrc,
                 "kernel_dram": ncu_blur_kernel_dram(peaks.get("hbm_gbs")),
+                "concurrent": _concurrent_pyramid(plan, B, pyramid_concurrent_ms, peaks.get("hbm_gbs")),
                 "algorithmic_bytes": pbytes,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"}
     det_gbs = detect_bytes(plan) * Bs / (stage_ms["detect"] / 1e3) / 1e9
