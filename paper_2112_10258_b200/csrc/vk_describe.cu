@@ -71,7 +71,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
     const int tid = threadIdx.x;
     const int n = n_items_dev ? min(*n_items_dev, n_items_max) : n_items_max;
     if (tid < kSrThreads / 32) sqn[tid] = 0;  // (first use is after the item's __syncthreads)
-    for (int item = blockIdx.x; item < n; item += gridDim.x) {
+    for (int item = first_item(); item < n; item += gridDim.x) {
         const int F = min(item_count[item], max_f);
         if (F <= 0) continue;
         const int first = item_first[item];

@@ -162,7 +162,7 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
             reinterpret_cast<uint32_t*>(lut)[i] = __ldg(reinterpret_cast<const uint32_t*>(ico_lut) + i);
     __syncthreads();
 
-    for (int item = blockIdx.x; item < n_kp; item += gridDim.x) {
+    for (int item = first_item(); item < n_kp; item += gridDim.x) {
         const vk_kp kp = kps[item];
         const vk_level L = levels[kp.lvl];
         const float* data = L.base + (long long)kp.vol * L.vol_stride;
