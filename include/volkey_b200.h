@@ -152,7 +152,9 @@ int vk_set_blur_path(int path);
 
 /* (x, y) kernel of the split path: 0 = whole-plane register-ring kernel
  * (bulk-copy staged plane, thread per row / column; default wherever the
- * plane fits two CTAs per SM), 1 = tiled kernel.  Results are bit-identical. */
+ * plane fits two CTAs per SM), 1 = tiled kernel, 2 = persistent plane kernel
+ * (one CTA per SM, two out-of-phase plane groups fed from a work counter).
+ * Results are bit-identical. */
 int vk_set_xy_kernel(int k);
 
 /* z-pass kernel selection (A/B; results are bit-identical): 0 = TMA-fed

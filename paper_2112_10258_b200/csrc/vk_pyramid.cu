@@ -722,6 +722,119 @@ blur_xy_plane_kernel(const float* __restrict__ src, float* __restrict__ tmp, int
     }
 }
 
+// Persistent variant of blur_xy_plane_kernel (VK_XY_STREAM): one CTA per SM
+// holds two independent plane groups (6 pass warps + one staged plane each)
+// that take planes from a work counter.  Group 1 starts its first load only
+// once group 0's first plane has landed, so the two run out of phase: one
+// group's bulk copy streams while the other computes (two plane CTAs per SM
+// start, load and compute in lockstep).  The DoG warps take planes from a
+// second counter and run independently.  counters[0..1] are zero at launch
+// (the launcher memsets them).
+constexpr int kStreamDogThreads = 2 * kDogThreads;
+template <int R>
+__global__ void __launch_bounds__(2 * kPlaneThreads + kStreamDogThreads, 1)
+blur_xy_stream_kernel(const float* __restrict__ src, float* __restrict__ tmp, int tp, int nx, int ny, int nplanes,
+                      unsigned buf_floats, Taps taps, const float* __restrict__ prev, float* __restrict__ pdog,
+                      unsigned* __restrict__ counters) {
+    extern __shared__ float4 smem4[];
+    __shared__ uint64_t bar[2];
+    __shared__ int cur_plane[2];
+    const unsigned plane = (unsigned)nx * (unsigned)ny;
+    if (threadIdx.x >= 2 * kPlaneThreads) {
+        // DoG warps: one plane per warp at a time, prev - src, read from global
+        const int lane = threadIdx.x & 31;
+        for (;;) {
+            unsigned p = 0;
+            if (lane == 0) p = atomicAdd(&counters[1], 1u);
+            p = __shfl_sync(0xffffffffu, p, 0);
+            if (p >= (unsigned)nplanes) break;
+            const size_t pb = (size_t)p * plane;
+            const float* g = src + pb;
+            constexpr int U = 8;
+            if (((plane & 1) | ((reinterpret_cast<uintptr_t>(prev + pb) | reinterpret_cast<uintptr_t>(pdog + pb) |
+                                 reinterpret_cast<uintptr_t>(g)) & 7)) == 0) {
+                const float2* pv2 = reinterpret_cast<const float2*>(prev + pb);
+                const float2* sv2 = reinterpret_cast<const float2*>(g);
+                float2* pd2 = reinterpret_cast<float2*>(pdog + pb);
+                const unsigned n2 = plane / 2;
+                for (unsigned i0 = lane; i0 < n2; i0 += 32 * U) {
+                    float2 a[U], c[U];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const unsigned i = i0 + j * 32;
+                        if (i < n2) {
+                            a[j] = __ldg(pv2 + i);
+                            c[j] = __ldg(sv2 + i);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const unsigned i = i0 + j * 32;
+                        if (i < n2) pd2[i] = make_float2(__fsub_rn(a[j].x, c[j].x), __fsub_rn(a[j].y, c[j].y));
+                    }
+                }
+            } else {
+                for (unsigned i = lane; i < plane; i += 32) pdog[pb + i] = __fsub_rn(__ldg(prev + pb + i), __ldg(g + i));
+            }
+        }
+        return;
+    }
+    const int grp = threadIdx.x >= kPlaneThreads;
+    const int tid = threadIdx.x - grp * kPlaneThreads;
+    float* buf = reinterpret_cast<float*>(smem4) + (size_t)grp * buf_floats;
+    __shared__ volatile int started;  // group 0's first plane has landed (or it had none)
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        started = 0;
+    }
+    asm volatile("bar.sync 3, %0;" ::"n"(2 * kPlaneThreads) : "memory");  // the pass warps of both groups
+    // named barriers 1 / 2: the two groups
+    for (int it = 0;; ++it) {
+        if (tid == 0) {
+            if (grp == 1 && it == 0)
+                while (!started) __nanosleep(64);  // start out of phase with group 0
+            const int p = (int)atomicAdd(&counters[0], 1u);
+            cur_plane[grp] = p;
+            if (p < nplanes) {
+                const uintptr_t ga = reinterpret_cast<uintptr_t>(src + (size_t)p * plane);
+                const uintptr_t a0 = ga & ~(uintptr_t)15;
+                const unsigned bytes = (unsigned)(((ga + 4ull * plane) - a0 + 15) & ~(uintptr_t)15);
+                // the previous plane's generic-proxy accesses of the buffer precede the async-proxy write
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&bar[grp], bytes);
+                bulk_g2s(buf, reinterpret_cast<const void*>(a0), bytes, &bar[grp]);
+            }
+        }
+        if (grp == 0) asm volatile("bar.sync 1, %0;" ::"n"(kPlaneThreads) : "memory");
+        else asm volatile("bar.sync 2, %0;" ::"n"(kPlaneThreads) : "memory");
+        const int p = cur_plane[grp];
+        if (p >= nplanes) {
+            if (grp == 0 && tid == 0) started = 1;
+            break;
+        }
+        const uintptr_t ga = reinterpret_cast<uintptr_t>(src + (size_t)p * plane);
+        float* s = buf + (ga & 15) / 4;
+        mbar_wait(&bar[grp], (unsigned)it & 1u);
+        if (grp == 0 && tid == 0 && it == 0) started = 1;
+        if (tid < ny) {
+            RowLine ln{s + tid * nx, nx, R};
+            ring_line<R>(nx, ln, taps);
+        }
+        if (grp == 0) asm volatile("bar.sync 1, %0;" ::"n"(kPlaneThreads) : "memory");
+        else asm volatile("bar.sync 2, %0;" ::"n"(kPlaneThreads) : "memory");
+        float* out = tmp + (size_t)p * (unsigned)tp * (unsigned)ny + tid;
+        if (tid < nx) {
+            ColLine ln{s + tid, out, ny, R, (unsigned)nx, (unsigned)tp};
+            ring_line<R>(ny, ln, taps);
+        } else if (tid < tp) {
+            for (int y = 0; y < ny; ++y) out[(unsigned)y * (unsigned)tp] = 0.f;
+        }
+        if (grp == 0) asm volatile("bar.sync 1, %0;" ::"n"(kPlaneThreads) : "memory");
+        else asm volatile("bar.sync 2, %0;" ::"n"(kPlaneThreads) : "memory");
+    }
+}
+
 // z pass over the (x, y)-blurred intermediate: thread = column pair
 // (gx, gx+1) of row gy; warp = 16 column pairs x rows (y, y+1) so the 2x2x2
 // subsample block of a thread is completed by lane ^ 16.  Planes outside
@@ -1513,7 +1626,38 @@ static int launch_xy_plane(const float* src, float* work, int tp, int nb, int nx
     return cuda_status(cudaGetLastError(), "blur xy plane launch");
 }
 
-static int g_xy_kernel = 0;  // 0: whole-plane ring kernel where it fits, 1: tile kernel (A/B)
+// Persistent double-buffered plane kernel: two staged planes per CTA, one CTA per SM.
+static bool plane_stream_fits(int nx, int ny) {
+    return nx <= kPlaneThreads && ny <= kPlaneThreads && 2 * ((long long)nx * ny * 4 + 32) <= 220 * 1024;
+}
+
+template <int R>
+static int launch_xy_stream(const float* src, float* work, int tp, int nb, int nx, int ny, int nz, const Taps& taps,
+                            cudaStream_t st, const float* prev, float* pdog, unsigned* counters, int sms) {
+    const unsigned buf_floats = (unsigned)(((long long)nx * ny + 8 + 3) & ~3LL);  // + 16-byte alignment slack
+    const int smem = (int)(2 * buf_floats * 4);
+    static int configured = 0;
+    if (configured < smem) {
+        cudaError_t e = cudaFuncSetAttribute(blur_xy_stream_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             220 * 1024);
+        if (e != cudaSuccess) return cuda_status(e, "blur xy stream attribute");
+        configured = 220 * 1024;
+    }
+    cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return cuda_status(e, "blur xy stream counters");
+    const int nplanes = nb * nz;
+    const int grid = nplanes < sms ? nplanes : sms;
+    blur_xy_stream_kernel<R><<<grid, 2 * kPlaneThreads + (prev ? kStreamDogThreads : 0), smem, st>>>(
+        src, work, tp, nx, ny, nplanes, buf_floats, taps, prev, pdog, counters);
+    count_launch();
+    return cuda_status(cudaGetLastError(), "blur xy stream launch");
+}
+
+#ifndef VK_XY_STREAM
+#define VK_XY_STREAM 0
+#endif
+static int g_xy_kernel = VK_XY_STREAM ? 2 : 0;  // 0: whole-plane ring kernel where it fits, 1: tile kernel (A/B),
+                                               // 2: persistent double-buffered plane kernel
 static int g_z_kernel = 0;  // 0: TMA-fed four-column kernel, 1: register-fed four-column kernel (packed sums),
                             // 2: four-column scalar sums, 3: column-pair kernel
 static int kZ4Waves = 2, kZ4MinChunkR = 6;
@@ -1595,7 +1739,7 @@ static bool launch_zt(const float* work, int tp, const float* src, float* dst, f
 template <int R>
 static int launch_split(const float* src, float* dst, float* dog, float* half, int nb, int nx, int ny, int nz,
                         const Taps& taps, float* work, int tp, cudaStream_t st, int zchunk, const float* prev,
-                        float* pdog) {
+                        float* pdog, unsigned* counters) {
     static bool env_read = false;
     if (!env_read) {
         if (const char* e = getenv("VK_Z_WAVES")) kZWaves = atoi(e) > 0 ? atoi(e) : kZWaves;
@@ -1603,23 +1747,26 @@ static int launch_split(const float* src, float* dst, float* dog, float* half, i
         if (const char* e = getenv("VK_Z4_WAVES")) kZ4Waves = atoi(e) > 0 ? atoi(e) : kZ4Waves;
         if (const char* e = getenv("VK_Z4_MINCHUNK")) kZ4MinChunkR = atoi(e) > 0 ? atoi(e) : kZ4MinChunkR;
         if (const char* e = getenv("VK_Z_KERNEL")) g_z_kernel = atoi(e);
+        if (const char* e = getenv("VK_XY_KERNEL")) g_xy_kernel = atoi(e);
         if (const char* e = getenv("VK_ZT_WAVES")) kZtWaves = atoi(e) > 0 ? atoi(e) : kZtWaves;
         if (const char* e = getenv("VK_ZT_MINCHUNK")) kZtMinChunkR = atoi(e) > 0 ? atoi(e) : kZtMinChunkR;
         env_read = true;
     }
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // taller tiles (less x-pass halo, fewer y-pass loads) unless they waste rows
     const bool tall = ((ny + 95) / 96) * 96 <= ((ny + 63) / 64) * 64;
     // 97..176 rows: one tile spans the whole y extent (no recomputed x-pass halo rows between y tiles;
     // measured 3.6% faster pyramid on 145x174x145 despite 2 CTAs/SM instead of 4)
-    const int rc1 = g_xy_kernel == 0 && plane_kernel_fits(nx, ny)
+    const int rc1 = g_xy_kernel == 2 && counters && plane_stream_fits(nx, ny)
+                        ? launch_xy_stream<R>(src, work, tp, nb, nx, ny, nz, taps, st, prev, pdog, counters, sms)
+                    : g_xy_kernel != 1 && plane_kernel_fits(nx, ny)
                         ? launch_xy_plane<R>(src, work, tp, nb, nx, ny, nz, taps, st, prev, pdog)
                     : ny <= 176 && ny > 96 ? launch_xy<R, 176>(src, work, tp, nb, nx, ny, nz, taps, st, prev, pdog)
                     : tall               ? launch_xy<R, 96>(src, work, tp, nb, nx, ny, nz, taps, st, prev, pdog)
                                          : launch_xy<R, 64>(src, work, tp, nb, nx, ny, nz, taps, st, prev, pdog);
     if (rc1 != VK_OK) return rc1;
-    int sms = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_z_kernel == 0) {
         const bool ok = half ? launch_zt<R, true>(work, tp, src, dst, dog, half, nb, nx, ny, nz, taps, st, zchunk, sms)
                              : launch_zt<R, false>(work, tp, src, dst, dog, half, nb, nx, ny, nz, taps, st, zchunk, sms);
@@ -1698,8 +1845,9 @@ extern "C" int vk_set_blur_path(int path) {
 }
 
 extern "C" int vk_set_xy_kernel(int k) {
-    if (k < 0 || k > 1) {
-        set_error("vk_set_xy_kernel: 0 (whole-plane ring kernel) or 1 (tile kernel)");
+    if (k < 0 || k > 2) {
+        set_error("vk_set_xy_kernel: 0 (whole-plane ring kernel), 1 (tile kernel) or 2 (persistent double-buffered "
+                  "plane kernel)");
         return VK_ERR_PARAMETER;
     }
     g_xy_kernel = k;
@@ -1786,21 +1934,24 @@ static int blur3d_impl(const float* src, float* dst, float* dog_out, float* half
         float* w = work;
         const bool own = w == nullptr || work_floats < wtotal || (reinterpret_cast<uintptr_t>(w) & 15) != 0;
         if (own) {
-            cudaError_t e = cudaMallocAsync(&w, wtotal * 4, st);
+            cudaError_t e = cudaMallocAsync(&w, (wtotal + 4) * 4, st);
             if (e != cudaSuccess) return cuda_status(e, "blur scratch");
         }
+        // work counters of the persistent (x, y) kernel: 4 floats past the intermediate, when the caller's
+        // work buffer has them (else that kernel is not used)
+        unsigned* counters = (own || work_floats >= wtotal + 4) ? reinterpret_cast<unsigned*>(w + wtotal) : nullptr;
         int rc;
         switch (radius) {
-            case 1: rc = launch_split<1>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
-            case 2: rc = launch_split<2>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
-            case 3: rc = launch_split<3>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
-            case 4: rc = launch_split<4>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
-            case 5: rc = launch_split<5>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
-            case 6: rc = launch_split<6>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
-            case 7: rc = launch_split<7>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
-            case 8: rc = launch_split<8>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
-            case 9: rc = launch_split<9>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
-            default: rc = launch_split<10>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog); break;
+            case 1: rc = launch_split<1>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog, counters); break;
+            case 2: rc = launch_split<2>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog, counters); break;
+            case 3: rc = launch_split<3>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog, counters); break;
+            case 4: rc = launch_split<4>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog, counters); break;
+            case 5: rc = launch_split<5>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog, counters); break;
+            case 6: rc = launch_split<6>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog, counters); break;
+            case 7: rc = launch_split<7>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog, counters); break;
+            case 8: rc = launch_split<8>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog, counters); break;
+            case 9: rc = launch_split<9>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog, counters); break;
+            default: rc = launch_split<10>(src, dst, dog_out, half_out, nb, nx, ny, nz, taps, w, tp, st, zchunk, prev, prev_dog, counters); break;
         }
         if (own) cudaFreeAsync(w, st);
         return rc;

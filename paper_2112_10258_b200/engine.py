@@ -192,7 +192,7 @@ class Extractor:
             self.input = t.empty((B, nz, ny, nx), dtype=f32, device="cuda")
         # (x, y)-blurred intermediate of the split blur (vk_blur3d_ws), one octave-0 level
         # with rows pitched to a multiple of 4 floats (16-byte aligned rows for the z pass)
-        self.blur_work = t.empty(B * ((nx + 3) // 4 * 4) * ny * nz, dtype=f32, device="cuda")
+        self.blur_work = t.empty(B * ((nx + 3) // 4 * 4) * ny * nz + 4, dtype=f32, device="cuda")  # + work counters
         self.levels, self.dogs = [], []
         for (ox, oy, oz) in self.plan.octave_dims:
             self.levels.append([t.empty((B, oz, oy, ox), dtype=f32, device="cuda") for _ in range(L)])

@@ -136,6 +136,44 @@ def test_blur_fused_epilogues_batched():
             assert np.array_equal(ghalf[i], O.half(want)), f"half sigma {sigma} radius {r}"
 
 
+def test_xy_kernels_with_previous_pair_dog():
+    """Every (x, y) kernel of the split blur (vk_set_xy_kernel 0 = plane, 1 =
+    tile, 2 = persistent two-group plane kernel) with the previous pair's DoG
+    fused in (vk_blur3d_ws2): level, DoG of the blurred pair and the previous
+    pair's DoG bit-equal to the oracle (scalespace.py:63-82, 137-151)."""
+    import torch
+
+    from oracle import volkey_oracle as O
+    from paper_2112_10258_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(23)
+    try:
+        for k in (0, 1, 2):
+            assert lib.vk_set_xy_kernel(k) == 0
+            for sigma, dims in ((0.9, (145, 37, 19)), (2.2, (61, 174, 23)), (3.6, (33, 50, 41))):
+                nb = 3
+                r, w = O.gauss_taps(sigma)
+                a = rng.standard_normal((nb,) + dims).astype(np.float32)  # [b][x][y][z]
+                p = rng.standard_normal((nb,) + dims).astype(np.float32)
+                tx = lambda v: torch.from_numpy(np.ascontiguousarray(v.transpose(0, 3, 2, 1))).cuda()  # noqa: E731
+                src, prev = tx(a), tx(p)
+                dst, dog, pdog = torch.empty_like(src), torch.empty_like(src), torch.empty_like(src)
+                wt = np.ascontiguousarray(w, dtype=np.float32)
+                _lib.call("vk_blur3d_ws2", src.data_ptr(), dst.data_ptr(), dog.data_ptr(), None, prev.data_ptr(),
+                          pdog.data_ptr(), nb, *dims, wt.ctypes.data, r, None, 0, _lib.stream_ptr())
+                torch.cuda.synchronize()
+                back = lambda t: t.cpu().numpy().transpose(0, 3, 2, 1)  # noqa: E731
+                got, gdog, gp = back(dst), back(dog), back(pdog)
+                for i in range(nb):
+                    want = O.blur3(a[i], w)
+                    assert np.array_equal(got[i], want), f"xy kernel {k} sigma {sigma} dims {dims}"
+                    assert np.array_equal(gdog[i], a[i] - want), f"xy kernel {k} dog sigma {sigma}"
+                    assert np.array_equal(gp[i], p[i] - a[i]), f"xy kernel {k} previous-pair dog sigma {sigma}"
+    finally:
+        lib.vk_set_xy_kernel(0)
+
+
 def test_subsample_units(golden_unit):
     g = golden_unit
     for i in range(4):
