@@ -607,16 +607,35 @@ struct RowLine {
 };
 
 // y-pass line: a column of the shared plane (stride nx) -> the intermediate.
+#ifndef VK_COL_RUNNING
+#define VK_COL_RUNNING 1  // running load / store offsets (y pass: 5-6 address instructions per arrival -> 2)
+#endif
 struct ColLine {
     const float* col;
     float* out;
     int n, R;
     unsigned nx, tp;
+#if VK_COL_RUNNING
+    // at() is called for consecutive positions -R, -R+1, ... and put() for consecutive outputs 0, 1, ...:
+    // the next load position's element offset and the next store's pointer advance by one stride per call
+    const float* ip = col - R * (int)nx;
+    template <bool SAFE>
+    VK_D float at(int k0, int j) {
+        const float v = SAFE ? *ip : col[(unsigned)clampi(k0 + j - R, 0, n - 1) * nx];
+        ip += nx;
+        return v;
+    }
+    VK_D void put(int, int, float v) {
+        *out = v;
+        out += tp;
+    }
+#else
     template <bool SAFE>
     VK_D float at(int k0, int j) const {
         return SAFE ? col[(unsigned)(k0 - R + j) * nx] : col[(unsigned)clampi(k0 + j - R, 0, n - 1) * nx];
     }
     VK_D void put(int k0, int j, float v) const { out[(unsigned)(k0 + j - 2 * R) * tp] = v; }
+#endif
 };
 
 constexpr int kPlaneThreads = 192;
