@@ -194,9 +194,9 @@ VK_D int nearest_dir_lut(const uint8_t* lut, float gx, float gy, float gz, float
 // Rare path: tiny gradients (|g|_1 < 1e-30, down to fp32 subnormals or an
 // fp32 gradient that rounded to 0), where the fp32 scores and margins below
 // lose their relative accuracy: the reference's 42 fp64 dots directly.
-static __device__ __noinline__ int nearest_dir_tiny(const double* dirs, const Nb6& nb) {
-    double x64, y64, z64;
-    grad64(nb, x64, y64, z64);
+// (fp64 gradient formed by the caller: a noinline callee taking the Nb6 by
+// reference would force every walk iteration to store it to the stack)
+static __device__ __noinline__ int nearest_dir_tiny(const double* dirs, double x64, double y64, double z64) {
     return nearest_dir(dirs, 42, x64, y64, z64);
 }
 
@@ -209,7 +209,11 @@ VK_D int nearest_dir_ico(const double* dirs, const IcoSh& ic, const uint8_t* lut
         if (k >= 0) return k;
     }
     const float l1 = ax + ay + az;
-    if (!(l1 >= 1.0e-30f)) return nearest_dir_tiny(dirs, nb);
+    if (!(l1 >= 1.0e-30f)) {
+        double x64, y64, z64;
+        grad64(nb, x64, y64, z64);
+        return nearest_dir_tiny(dirs, x64, y64, z64);
+    }
     const float vA = fmaf(PHI, az, ay), vB = fmaf(PHI, ay, ax), vC = fmaf(PHI, ax, az);
     const float m = 1.0e-5f * 2.7f * l1;
     const int fast = nearest_dir_fast(ic, gx, gy, gz, ax, ay, az, l1, vA, vB, vC, m);
