@@ -284,6 +284,9 @@ VK_D void sr_resolve(int4 e, const vk_kp& kp, const vk_level& L, const float* da
                                                            Rs + 9 * f);
     red_vote(hist + f * kHistFrame, 8 * sp + og, __int_as_float(e.z));
 }
+#ifndef VK_SR_PIPE_PREFETCH
+#define VK_SR_PIPE_PREFETCH 1  // L1 prefetch kPrefetchPlanes planes ahead in the pipelined interior walk
+#endif
 #ifndef VK_SR_DEPTH
 #define VK_SR_DEPTH 2  // voxels in flight per thread (sr_walk_pipe)
 #endif
@@ -304,7 +307,9 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
         const int ox = unpack_off(pk, 0), oy = unpack_off(pk, 1), oz = unpack_off(pk, 2);
         if (INTERIOR) {
             const int c = kc + oz * plane + oy * nx + ox;
+#if VK_SR_PIPE_PREFETCH
             if (oz < zpf) asm volatile("prefetch.global.L1 [%0];" ::"l"(data + c + kPrefetchPlanes * plane));
+#endif
             n = load_nb6_interior(data, (unsigned)nx, (unsigned)plane, (unsigned)c);
         } else {
             // branch-free clamped loads (the centre clamped into the volume too: values of
