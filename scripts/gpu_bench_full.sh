@@ -15,6 +15,9 @@ if [ -z "$NOREF" ]; then
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_reference.jsonl 2> $O/bench_reference.err; echo "ref rc=$?"
 tail -1 $O/bench_reference.jsonl | cut -c1-300
 fi
+# matching benches before the ncu sessions (a GPU fresh from ncu replays measured 10-30% slow)
+timeout 600 python scripts/match_bench.py > $O/match_bench.log 2>&1; echo "match bench rc=$?"
+timeout 900 python scripts/database_bench.py 2> $O/database_bench.err | grep "^{" > $O/database_bench.json; echo "database rc=${PIPESTATUS[0]}"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-matching > $O/launches_run.log 2>&1; echo "launches rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
@@ -28,5 +31,3 @@ for k in siftrank_kernel orient_kernel; do
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$k" --launch-count 1 \
   -o $O/${k}_full python scripts/profile_step.py --batch 12 --steps 1 > /dev/null 2>&1; echo "$k full rc=$?"
 done
-timeout 600 python scripts/match_bench.py > $O/match_bench.log 2>&1; echo "match bench rc=$?"
-timeout 900 python scripts/database_bench.py > $O/database_bench.json 2> $O/database_bench.err; echo "database rc=$?"
