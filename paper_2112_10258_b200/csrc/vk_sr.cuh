@@ -287,6 +287,9 @@ VK_D void sr_resolve(int4 e, const vk_kp& kp, const vk_level& L, const float* da
 #ifndef VK_SR_PIPE_PREFETCH
 #define VK_SR_PIPE_PREFETCH 1  // L1 prefetch kPrefetchPlanes planes ahead in the pipelined interior walk
 #endif
+#ifndef VK_SR_X_LATE
+#define VK_SR_X_LATE 0  // 1: next voxel's x loads issued after the frames (no spill of them; measured 1.5% slower: exposed latency)
+#endif
 #ifndef VK_SR_DEPTH
 #define VK_SR_DEPTH 2  // voxels in flight per thread (sr_walk_pipe)
 #endif
@@ -303,14 +306,21 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
     const int zpf = L.nz - kPrefetchPlanes - kp.iz;  // prefetch plane exists while oz < zpf
     const int* offs = ball_offsets + ball.zstart;
     hist = vote_copy(hist);
-    auto issue = [&](int pk, Nb6& n) {
+    auto issue = [&](int pk, Nb6& n, bool with_x) {
         const int ox = unpack_off(pk, 0), oy = unpack_off(pk, 1), oz = unpack_off(pk, 2);
         if (INTERIOR) {
             const int c = kc + oz * plane + oy * nx + ox;
 #if VK_SR_PIPE_PREFETCH
             if (oz < zpf) asm volatile("prefetch.global.L1 [%0];" ::"l"(data + c + kPrefetchPlanes * plane));
 #endif
-            n = load_nb6_interior(data, (unsigned)nx, (unsigned)plane, (unsigned)c);
+            if (with_x) {
+                n = load_nb6_interior(data, (unsigned)nx, (unsigned)plane, (unsigned)c);
+            } else {  // x neighbours issued after the current voxel's frames (VK_SR_X_LATE)
+                n.yh = __ldg(data + ((unsigned)c + (unsigned)nx));
+                n.yl = __ldg(data + ((unsigned)c - (unsigned)nx));
+                n.zh = __ldg(data + ((unsigned)c + (unsigned)plane));
+                n.zl = __ldg(data + ((unsigned)c - (unsigned)plane));
+            }
         } else {
             // branch-free clamped loads (the centre clamped into the volume too: values of
             // outside voxels are never used); the scales are recomputed at use, so a ring slot
@@ -330,13 +340,16 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
     // ring: voxel j + d * step has its neighbours issued (d < D - 1) and its
     // packed offset loaded D - 1 steps ahead of use
     constexpr int D = VK_SR_DEPTH;
+    // x neighbours of the next voxel issued late (after this voxel's frames) in the interior walk: at the
+    // 80-register cap the compiler otherwise spilled those two in-flight loads, waiting on them at the store
+    constexpr bool kXLate = VK_SR_X_LATE && INTERIOR && D == 2;
     int pk[D];
     Nb6 nb[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
         const int jj = tid + d * step;
         pk[d] = jj < ball.count ? __ldg(offs + jj) : 0;
-        if (d < D - 1 && jj < ball.count) issue(pk[d], nb[d]);
+        if (d < D - 1 && jj < ball.count) issue(pk[d], nb[d], true);
     }
     int cnt = 0;
     for (int base = 0; base < ball.count; base += step) {
@@ -350,7 +363,7 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
             nb[d] = nb[d + 1];
         }
         if (j + (D - 1) * step < ball.count) {
-            issue(pk[D - 2], nb[D - 2]);
+            issue(pk[D - 2], nb[D - 2], !kXLate);
             if (j + D * step < ball.count) pk[D - 1] = __ldg(offs + j + D * step);
         }
         bool in = j < ball.count;
@@ -390,6 +403,12 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
 #endif
                 }
             }
+        }
+        if (kXLate && j + step < ball.count) {
+            const int p2 = pk[0];  // the next voxel (D == 2: shifted into slot 0 above)
+            const unsigned c = (unsigned)(kc + unpack_off(p2, 2) * plane + unpack_off(p2, 1) * nx + unpack_off(p2, 0));
+            nb[0].xh = __ldg(data + (c + 1u));
+            nb[0].xl = __ldg(data + (c - 1u));
         }
 #if VK_SR_DEFER
         __syncwarp();
