@@ -25,11 +25,12 @@ VK_HD T clampi(T v, T lo, T hi) { return v < lo ? lo : (v > hi ? hi : v); }
 // ---- cp.async (LDGSTS) helpers -------------------------------------------
 VK_D void cp_async4(void* smem, const void* gmem) {
     unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-VK_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+// (memory clobbers: shared-memory reads of the landed data must not move above the wait)
+VK_D void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
-VK_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+VK_D void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // ---- exact-rounding arithmetic (no contraction) ---------------------------
 // The reference evaluates every product and sum as a separately rounded numpy

@@ -68,6 +68,7 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
     __shared__ int4 sq[kSrThreads / 32][kSrQueue];  // deferred uncertain votes, per warp
     __shared__ int sqn[kSrThreads / 32];
     __shared__ unsigned wmask[kSrThreads / 32];
+    __shared__ float sring[kSrRingFloats];  // VK_SR_ASYNC: in-flight neighbour gathers of the interior walk
     const int tid = threadIdx.x;
     const int n = n_items_dev ? min(*n_items_dev, n_items_max) : n_items_max;
     if (tid < kSrThreads / 32) sqn[tid] = 0;  // (first use is after the item's __syncthreads)
@@ -113,13 +114,13 @@ siftrank_kernel(const vk_frame* __restrict__ frames, const double* __restrict__ 
             }
             if constexpr (MODE == 1)
                 cnt = sr_walk_frames<true>(kp, L, data, nullptr, ball, ball_offsets, Rs, Rc, hist, F, sq[tid >> 5],
-                                           sqn + (tid >> 5));
+                                           sqn + (tid >> 5), sring);
             else if constexpr (MODE == 2)
                 cnt = sr_walk_frames<false, true>(kp, L, data, nullptr, ball, ball_offsets, Rs, Rc, hist, F,
                                                   sq[tid >> 5], sqn + (tid >> 5));
             else if (ball_interior(kp.ix, kp.iy, kp.iz, ball.r, L.nx, L.ny, L.nz))
                 cnt = sr_walk_frames<true>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F, sq[tid >> 5],
-                                           sqn + (tid >> 5));
+                                           sqn + (tid >> 5), sring);
             else
                 cnt = sr_walk_frames<false>(kp, L, data, g4, ball, ball_offsets, Rs, Rc, hist, F, sq[tid >> 5],
                                             sqn + (tid >> 5));

@@ -24,13 +24,30 @@ constexpr int kOriThreads = VK_ORI_THREADS;
 
 constexpr int kOriQueue = 64;  // per-warp deferred entries of the fast walk (flush at >= 32)
 
+// pair_ok (orient.py:128-168's usable secondary pairs) as a bitset in shared memory: 512 B instead of 4 KB,
+// which keeps orient_kernel's static shared memory under 1/3 of a 100 KB carveout (3 CTAs/SM with the larger
+// L1 share)
+constexpr int kOkWords = VK_MAX_DIRS * VK_MAX_DIRS / 32;
+VK_D bool ok_bit(const unsigned* okb, int i) { return (okb[i >> 5] >> (i & 31)) & 1u; }
+VK_D void load_ok_bits(unsigned* okb, const uint8_t* __restrict__ pair_ok, int K) {
+    const int n = K * K;
+    for (int w = threadIdx.x; w < (n + 31) / 32; w += blockDim.x) {
+        unsigned v = 0u;
+        for (int b = 0; b < 32; ++b) {
+            const int i = 32 * w + b;
+            if (i < n && pair_ok[i]) v |= 1u << b;
+        }
+        okb[w] = v;
+    }
+}
+
 struct OriShared {
     double xv[kOriThreads];
     int xb[kOriThreads];
     double dirs[VK_MAX_DIRS * 3];
     double w[VK_MAX_DIRS];
     int order[VK_MAX_DIRS];
-    uint8_t ok[VK_MAX_DIRS * VK_MAX_DIRS];
+    unsigned okb[kOkWords];  // pair_ok as bits (bytes would cost 3.5 KB more: see load_ok_bits)
     int unc[VK_MAX_DIRS];
     unsigned wmask[kOriThreads / 32];
     int2 queue[kOriThreads / 32][kOriQueue];  // deferred boundary-cell voxels of the fast walk (ori_walk)
@@ -597,7 +614,7 @@ VK_D int field_walk(const vk_kp& kp, const vk_level& L, const float* __restrict_
 
 // Frames from a weight vector whose comparisons are exact (dominant_orientations).
 // order[] must hold the bins sorted by (-w, index).
-VK_D int frames_from(const double* w, const int* order, int K, const uint8_t* ok, double ratio, int max_frames,
+VK_D int frames_from(const double* w, const int* order, int K, const unsigned* okb, double ratio, int max_frames,
                      int* prim, int* sec) {
     const double top = w[order[0]];
     if (!(top > 0.0)) return 0;
@@ -610,7 +627,7 @@ VK_D int frames_from(const double* w, const int* order, int K, const uint8_t* ok
         for (int q2 = 0; q2 < K; ++q2) {
             const int q = order[q2];
             if (q == p) continue;
-            if (ok[p * K + q]) {
+            if (ok_bit(okb, p * K + q)) {
                 prim[nf] = p;
                 sec[nf] = q;
                 ++nf;
@@ -674,7 +691,7 @@ VK_D bool warp_mark_uncertain(const double* w, const int* order, int K, double e
 // max_frames of them counted whether or not a secondary exists; each
 // secondary is the first bin of the order != primary with pair_ok, found with
 // a ballot over the order.  Writes nframes[0], prim[0..], sec[0..].
-VK_D void warp_frames_from(const double* w, const int* order, int K, const uint8_t* ok, double ratio, int max_frames,
+VK_D void warp_frames_from(const double* w, const int* order, int K, const unsigned* okb, double ratio, int max_frames,
                            int* nframes, int* prim, int* sec) {
     const int lane = threadIdx.x & 31;
     int nf = 0;
@@ -689,8 +706,8 @@ VK_D void warp_frames_from(const double* w, const int* order, int K, const uint8
                 const int p = order[32 * h + __ffs(qm) - 1];
                 ++taken;
                 const int oa = order[lane], ob = lane + 32 < K ? order[lane + 32] : p;
-                const unsigned m0 = __ballot_sync(0xffffffffu, lane < K && oa != p && ok[p * K + oa]);
-                const unsigned m1 = __ballot_sync(0xffffffffu, ob != p && ok[p * K + ob]);
+                const unsigned m0 = __ballot_sync(0xffffffffu, lane < K && oa != p && ok_bit(okb, p * K + oa));
+                const unsigned m1 = __ballot_sync(0xffffffffu, ob != p && ok_bit(okb, p * K + ob));
                 const int q2 = m0 ? __ffs(m0) - 1 : (m1 ? 32 + __ffs(m1) - 1 : -1);
                 if (q2 >= 0) {
                     if (lane == 0) {

@@ -153,7 +153,7 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         ic.cd[tid] = make_float4((float)dirs_g[3 * k], (float)dirs_g[3 * k + 1], (float)dirs_g[3 * k + 2], 0.f);
         ic.fk[tid] = c == 0 ? ico.vert[v] : ico.kind[v][c - 1];
     }
-    for (int i = tid; i < K * K; i += kOriThreads) sh.ok[i] = pair_ok[i];
+    load_ok_bits(sh.okb, pair_ok, K);
     const int n_kp = n_kp_dev ? min(*n_kp_dev, n_kp_max) : n_kp_max;
     const IcoSh* icp = ico.valid ? &ic : nullptr;
     const uint8_t* lutp = ico.valid && ico_lut ? lut : nullptr;
@@ -322,7 +322,7 @@ orient_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, i
         }
         if (weights)
             for (int b = tid; b < K; b += kOriThreads) weights[(long long)item * K + b] = sh.w[b];
-        if (tid < 32) warp_frames_from(sh.w, sh.order, K, sh.ok, ratio, max_frames, nframes + item,
+        if (tid < 32) warp_frames_from(sh.w, sh.order, K, sh.okb, ratio, max_frames, nframes + item,
                                        prim + (long long)item * max_frames, sec + (long long)item * max_frames);
         __syncthreads();
     }
@@ -334,8 +334,8 @@ __global__ void frames_from_weights_kernel(const double* __restrict__ weights, i
                                            int* __restrict__ nframes, int* __restrict__ prim, int* __restrict__ sec) {
     __shared__ double w[VK_MAX_DIRS];
     __shared__ int order[VK_MAX_DIRS];
-    __shared__ uint8_t ok[VK_MAX_DIRS * VK_MAX_DIRS];
-    for (int i = threadIdx.x; i < K * K; i += blockDim.x) ok[i] = pair_ok[i];
+    __shared__ unsigned okb[kOkWords];
+    load_ok_bits(okb, pair_ok, K);
     for (int item = blockIdx.x; item < n; item += gridDim.x) {
         __syncthreads();
         for (int b = threadIdx.x; b < K; b += blockDim.x) w[b] = weights[(long long)item * K + b];
@@ -344,7 +344,7 @@ __global__ void frames_from_weights_kernel(const double* __restrict__ weights, i
         __syncthreads();
         if (threadIdx.x == 0) {
             int pr[VK_MAX_FRAMES], se[VK_MAX_FRAMES];
-            const int nf = frames_from(w, order, K, ok, ratio, max_frames, pr, se);
+            const int nf = frames_from(w, order, K, okb, ratio, max_frames, pr, se);
             nframes[item] = nf;
             for (int f = 0; f < nf; ++f) {
                 prim[item * max_frames + f] = pr[f];

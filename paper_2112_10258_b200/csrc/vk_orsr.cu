@@ -303,7 +303,7 @@ orsr_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, int
         sh.ic.cd[tid] = make_float4((float)dirs_g[3 * k], (float)dirs_g[3 * k + 1], (float)dirs_g[3 * k + 2], 0.f);
         sh.ic.fk[tid] = c == 0 ? ico.vert[v] : ico.kind[v][c - 1];
     }
-    for (int i = tid; i < K * K; i += kOsThreads) sh.o.ok[i] = pair_ok[i];
+    load_ok_bits(sh.o.okb, pair_ok, K);
     for (int i = tid; i < kLutBytes / 4; i += kOsThreads)
         reinterpret_cast<uint32_t*>(sh.lut)[i] = __ldg(reinterpret_cast<const uint32_t*>(ico_lut) + i);
     if (tid < kOsThreads / 32) sh.sqn[tid] = 0;
@@ -389,7 +389,7 @@ orsr_kernel(const vk_kp* __restrict__ kps, const int* __restrict__ n_kp_dev, int
             __syncthreads();
         }
         if (tid < 32)
-            warp_frames_from(sh.o.w, sh.o.order, K, sh.o.ok, ratio, max_frames, &sh.nf, sh.prim, sh.sec);
+            warp_frames_from(sh.o.w, sh.o.order, K, sh.o.okb, ratio, max_frames, &sh.nf, sh.prim, sh.sec);
         __syncthreads();
         const int F = sh.nf;
         if (tid < max_frames) {

@@ -435,6 +435,129 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
     return cnt;
 }
 
+// Interior walk with the neighbour gathers in flight in SHARED memory instead
+// of registers (VK_SR_ASYNC): each voxel's six neighbours are copied by
+// cp.async (LDGSTS, L1-allocating) into the thread's slot of a per-CTA ring,
+// VK_SR_ADEPTH voxels ahead, and read back with conflict-free LDS once their
+// group has landed.  In-flight loads then cost no registers (the register
+// pipeline above spills two of its six at the 80-register cap and so waits on
+// them), and the depth is free.
+#ifndef VK_SR_ASYNC
+#define VK_SR_ASYNC 0
+#endif
+#ifndef VK_SR_ADEPTH
+#define VK_SR_ADEPTH 3
+#endif
+constexpr int kSrRingFloats = VK_SR_ASYNC ? VK_SR_ADEPTH * 6 * kSrThreads : 1;
+
+template <int NF>
+VK_D int sr_walk_async(const vk_kp& kp, const vk_level& L, const float* data, const vk_ball& ball,
+                       const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist,
+                       int F, int4* queue, int* qcount, float* ring) {
+    static_assert(VK_SR_DEFER, "the shared-memory pipelined walk defers uncertain octants");
+    const int tid = threadIdx.x;
+    const int step = blockDim.x;
+    const int nx = L.nx, plane = L.nx * L.ny;
+    const int kc = (kp.iz * L.ny + kp.iy) * nx + kp.ix;
+    const int zpf = L.nz - kPrefetchPlanes - kp.iz;
+    const int* offs = ball_offsets + ball.zstart;
+    hist = vote_copy(hist);
+    constexpr int D = VK_SR_ADEPTH;
+    float* mine = ring + tid;  // slot s, value k at mine[(6 s + k) * kSrThreads]
+    auto issue = [&](int pk, int slot) {
+        const int ox = unpack_off(pk, 0), oy = unpack_off(pk, 1), oz = unpack_off(pk, 2);
+        const unsigned c = (unsigned)(kc + oz * plane + oy * nx + ox);
+#if VK_SR_PIPE_PREFETCH
+        if (oz < zpf) asm volatile("prefetch.global.L1 [%0];" ::"l"(data + c + kPrefetchPlanes * plane));
+#endif
+        float* d = mine + 6 * slot * kSrThreads;
+        cp_async4(d, data + (c + 1u));
+        cp_async4(d + kSrThreads, data + (c - 1u));
+        cp_async4(d + 2 * kSrThreads, data + (c + (unsigned)nx));
+        cp_async4(d + 3 * kSrThreads, data + (c - (unsigned)nx));
+        cp_async4(d + 4 * kSrThreads, data + (c + (unsigned)plane));
+        cp_async4(d + 5 * kSrThreads, data + (c - (unsigned)plane));
+    };
+    // packed offsets of voxels j .. j + (D - 1) step: pk[d]; groups in flight for j .. j + (D - 2) step
+    int pk[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        const int jj = tid + d * step;
+        pk[d] = jj < ball.count ? __ldg(offs + jj) : 0;
+        if (d < D - 1) {
+            if (jj < ball.count) issue(pk[d], d);
+            cp_async_commit();
+        }
+    }
+    int cnt = 0, slot = 0;
+    for (int base = 0; base < ball.count; base += step) {
+        const int j = base + tid;
+        const int pc = pk[0];
+#pragma unroll
+        for (int d = 0; d + 1 < D; ++d) pk[d] = pk[d + 1];
+        {
+            int ns = slot + (D - 1);
+            if (ns >= D) ns -= D;
+            if (j + (D - 1) * step < ball.count) {
+                issue(pk[D - 2], ns);
+                if (j + D * step < ball.count) pk[D - 1] = __ldg(offs + j + D * step);
+            }
+            cp_async_commit();
+        }
+        cp_async_wait<D - 1>();  // this voxel's group has landed
+        if (j < ball.count) {
+            ++cnt;
+            const float* d = mine + 6 * slot * kSrThreads;
+            Nb6 cur;
+            cur.xh = d[0];
+            cur.xl = d[kSrThreads];
+            cur.yh = d[2 * kSrThreads];
+            cur.yl = d[3 * kSrThreads];
+            cur.zh = d[4 * kSrThreads];
+            cur.zl = d[5 * kSrThreads];
+            cur.sx = cur.sy = cur.sz = 0.5f;
+            float gx, gy, gz;
+            grad32(cur, gx, gy, gz);
+            if (grad_nonzero(cur)) {
+                const float mag = nz_vote(norm3_f32(gx, gy, gz));
+                const int ox = unpack_off(pc, 0), oy = unpack_off(pc, 1), oz = unpack_off(pc, 2);
+#pragma unroll
+                for (int f = 0; f < NF; ++f) {
+                    if (f >= F) break;
+                    int sure;
+                    const int bin = sr_bin_try(ox, oy, oz, gx, gy, gz, Rc + kRcPerFrame * f, sure);
+                    if (sure == 3) {
+                        red_vote(hist + f * kHistFrame, bin, mag);
+                    } else {
+                        const int pos = atomicAdd(qcount, 1);
+                        queue[pos] = make_int4(pc, f | (bin << 2) | (sure << 8), __float_as_int(mag), 0);
+                    }
+                }
+            }
+        }
+        if (++slot == D) slot = 0;
+        __syncwarp();
+        int qn = *reinterpret_cast<volatile int*>(qcount);
+        if (qn >= 32) {
+            do {
+                sr_resolve(queue[qn - 32 + (tid & 31)], kp, L, data, Rs, hist);
+                qn -= 32;
+            } while (qn >= 32);
+            __syncwarp();
+            if ((tid & 31) == 0) *qcount = qn;
+            __syncwarp();
+        }
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    const int qn = *reinterpret_cast<volatile int*>(qcount);
+    if ((tid & 31) < qn) sr_resolve(queue[tid & 31], kp, L, data, Rs, hist);
+    __syncwarp();
+    if ((tid & 31) == 0) *qcount = 0;
+    __syncwarp();
+    return cnt;
+}
+
 #ifndef VK_SR_PIPE
 #define VK_SR_PIPE 1
 #endif
@@ -445,7 +568,15 @@ VK_D int sr_walk_pipe(const vk_kp& kp, const vk_level& L, const float* data, con
 template <bool INTERIOR, bool PIPE_BORDER = (VK_SR_PIPE_BORDER != 0)>
 VK_D int sr_walk_frames(const vk_kp& kp, const vk_level& L, const float* data, const float4* g4, const vk_ball& ball,
                         const int* __restrict__ ball_offsets, const double* Rs, const float4* Rc, double* hist,
-                        int F, int4* queue, int* qcount) {
+                        int F, int4* queue, int* qcount, float* ring = nullptr) {
+    if (VK_SR_ASYNC && INTERIOR && ring != nullptr && !g4 && F <= 4) {
+        switch (F) {
+            case 1: return sr_walk_async<1>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount, ring);
+            case 2: return sr_walk_async<2>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount, ring);
+            case 3: return sr_walk_async<3>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount, ring);
+            default: return sr_walk_async<4>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount, ring);
+        }
+    }
     if (VK_SR_PIPE && (INTERIOR || PIPE_BORDER) && !g4 && F <= 4) {
         switch (F) {
             case 1: return sr_walk_pipe<1, INTERIOR>(kp, L, data, ball, ball_offsets, Rs, Rc, hist, F, queue, qcount);
