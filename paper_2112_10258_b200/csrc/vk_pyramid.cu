@@ -665,6 +665,9 @@ VK_D void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+VK_D void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
 VK_D void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -801,18 +804,17 @@ blur_xy_stream_kernel(const float* __restrict__ src, float* __restrict__ tmp, in
     const int grp = threadIdx.x >= kPlaneThreads;
     const int tid = threadIdx.x - grp * kPlaneThreads;
     float* buf = reinterpret_cast<float*>(smem4) + (size_t)grp * buf_floats;
-    __shared__ volatile int started;  // group 0's first plane has landed (or it had none)
+    __shared__ uint64_t started;  // one phase: group 0's first plane has landed (or it had none)
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
-        started = 0;
+        mbar_init(&started, 1);
     }
     asm volatile("bar.sync 3, %0;" ::"n"(2 * kPlaneThreads) : "memory");  // the pass warps of both groups
     // named barriers 1 / 2: the two groups
     for (int it = 0;; ++it) {
         if (tid == 0) {
-            if (grp == 1 && it == 0)
-                while (!started) __nanosleep(64);  // start out of phase with group 0
+            if (grp == 1 && it == 0) mbar_wait(&started, 0);  // start out of phase with group 0
             const int p = (int)atomicAdd(&counters[0], 1u);
             cur_plane[grp] = p;
             if (p < nplanes) {
@@ -829,13 +831,13 @@ blur_xy_stream_kernel(const float* __restrict__ src, float* __restrict__ tmp, in
         else asm volatile("bar.sync 2, %0;" ::"n"(kPlaneThreads) : "memory");
         const int p = cur_plane[grp];
         if (p >= nplanes) {
-            if (grp == 0 && tid == 0) started = 1;
+            if (grp == 0 && tid == 0 && it == 0) mbar_arrive(&started);
             break;
         }
         const uintptr_t ga = reinterpret_cast<uintptr_t>(src + (size_t)p * plane);
         float* s = buf + (ga & 15) / 4;
         mbar_wait(&bar[grp], (unsigned)it & 1u);
-        if (grp == 0 && tid == 0 && it == 0) started = 1;
+        if (grp == 0 && tid == 0 && it == 0) mbar_arrive(&started);
         if (tid < ny) {
             RowLine ln{s + tid * nx, nx, R};
             ring_line<R>(nx, ln, taps);
@@ -1185,9 +1187,6 @@ constexpr int kZtThreads = kZ4Threads + 32;  // 4 consumer (math) warps + 1 prod
 template <int R>
 constexpr int zt_min_blocks() { return 3; }
 
-VK_D void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
-}
 
 template <int R, bool HALF>
 __global__ void __launch_bounds__(kZtThreads, zt_min_blocks<R>())
