@@ -1414,7 +1414,71 @@ VK_D void small_pass(const float* __restrict__ in, float* __restrict__ out, int 
     }
 }
 
-__global__ void __launch_bounds__(512)
+// Radius-specialised pass: taps unrolled from registers, the line coordinate by
+// multiply-high division (exact for < 2^16 voxels), unclamped taps away from
+// the borders.  Same products and tap-order sums as small_pass.
+template <int R, int AXIS>
+VK_D void small_pass_r(const float* __restrict__ in, float* __restrict__ out, int nx, int ny, int nz, unsigned mx,
+                       unsigned my, const float* w) {
+    constexpr int P = 2 * R + 1;
+    float wr[P];
+#pragma unroll
+    for (int t = 0; t < P; ++t) wr[t] = w[t];
+    const int n = nx * ny * nz;
+    const int st = AXIS == 0 ? 1 : (AXIS == 1 ? nx : nx * ny);
+    const int len = AXIS == 0 ? nx : (AXIS == 1 ? ny : nz);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned q1 = mx ? __umulhi((unsigned)i, mx) : (unsigned)i;  // i / nx
+        int c;
+        if (AXIS == 0) {
+            c = i - (int)q1 * nx;
+        } else {
+            const unsigned q2 = my ? __umulhi(q1, my) : q1;  // i / (nx ny)
+            c = AXIS == 1 ? (int)q1 - (int)q2 * ny : (int)q2;
+        }
+        const float* base = in + (i - c * st);
+        float acc;
+        if (c >= R && c + R < len) {
+            const float* q = base + (c - R) * st;
+            acc = fmul(wr[0], q[0]);
+#pragma unroll
+            for (int t = 1; t < P; ++t) acc = fadd(acc, fmul(wr[t], q[t * st]));
+        } else {
+            acc = fmul(wr[0], base[clampi(c - R, 0, len - 1) * st]);
+#pragma unroll
+            for (int t = 1; t < P; ++t) acc = fadd(acc, fmul(wr[t], base[clampi(c - R + t, 0, len - 1) * st]));
+        }
+        out[i] = acc;
+    }
+}
+
+template <int AXIS>
+VK_D void small_pass_any(const float* in, float* out, int nx, int ny, int nz, unsigned mx, unsigned my, int R,
+                         const float* w) {
+    switch (R) {
+        case 1: small_pass_r<1, AXIS>(in, out, nx, ny, nz, mx, my, w); break;
+        case 2: small_pass_r<2, AXIS>(in, out, nx, ny, nz, mx, my, w); break;
+        case 3: small_pass_r<3, AXIS>(in, out, nx, ny, nz, mx, my, w); break;
+        case 4: small_pass_r<4, AXIS>(in, out, nx, ny, nz, mx, my, w); break;
+        case 5: small_pass_r<5, AXIS>(in, out, nx, ny, nz, mx, my, w); break;
+        case 6: small_pass_r<6, AXIS>(in, out, nx, ny, nz, mx, my, w); break;
+        case 7: small_pass_r<7, AXIS>(in, out, nx, ny, nz, mx, my, w); break;
+        case 8: small_pass_r<8, AXIS>(in, out, nx, ny, nz, mx, my, w); break;
+        case 9: small_pass_r<9, AXIS>(in, out, nx, ny, nz, mx, my, w); break;
+        case 10: small_pass_r<10, AXIS>(in, out, nx, ny, nz, mx, my, w); break;
+        default: small_pass(in, out, nx, ny, nz, AXIS, R, w); break;
+    }
+}
+
+#ifndef VK_SMALL_THREADS
+#define VK_SMALL_THREADS 1024
+#endif
+#ifndef VK_SMALL_FAST
+#define VK_SMALL_FAST 1  // radius-specialised passes (0: the generic runtime-radius pass)
+#endif
+constexpr int kSmallThreads = VK_SMALL_THREADS;
+
+__global__ void __launch_bounds__(kSmallThreads)
 small_octaves_kernel(SmallOctaves so) {
     extern __shared__ float4 sm4[];
     float* A = reinterpret_cast<float*>(sm4);
@@ -1431,14 +1495,25 @@ small_octaves_kernel(SmallOctaves so) {
         float* src = A;
         float* xb = Bf;
         float* yb = C;
+        // multiply-high reciprocals of nx and nx * ny (0: divisor 1)
+        const unsigned mx = nx > 1 ? 0xFFFFFFFFu / (unsigned)nx + 1u : 0u;
+        const unsigned my = ny > 1 ? 0xFFFFFFFFu / (unsigned)ny + 1u : 0u;
         for (int lvi = 1; lvi < so.levels; ++lvi) {
             const int R = so.radius[lvi];
             const float* w = so.taps[lvi];
-            small_pass(src, xb, nx, ny, nz, 0, R, w);
-            __syncthreads();
-            small_pass(xb, yb, nx, ny, nz, 1, R, w);
-            __syncthreads();
-            small_pass(yb, xb, nx, ny, nz, 2, R, w);  // xb now holds level lvi
+            if (VK_SMALL_FAST) {
+                small_pass_any<0>(src, xb, nx, ny, nz, mx, my, R, w);
+                __syncthreads();
+                small_pass_any<1>(xb, yb, nx, ny, nz, mx, my, R, w);
+                __syncthreads();
+                small_pass_any<2>(yb, xb, nx, ny, nz, mx, my, R, w);  // xb now holds level lvi
+            } else {
+                small_pass(src, xb, nx, ny, nz, 0, R, w);
+                __syncthreads();
+                small_pass(xb, yb, nx, ny, nz, 1, R, w);
+                __syncthreads();
+                small_pass(yb, xb, nx, ny, nz, 2, R, w);
+            }
             __syncthreads();
             float* lo = so.lv[o][lvi] + vb;
             float* dg = so.dog[o][lvi - 1] + vb;
@@ -2093,7 +2168,7 @@ extern "C" int vk_small_octaves(int n_oct, int levels, int handoff, const int* d
         if (e != cudaSuccess) return cuda_status(e, "small octaves attribute");
         configured = true;
     }
-    small_octaves_kernel<<<nb, 512, smem, as_stream(stream)>>>(so);
+    small_octaves_kernel<<<nb, kSmallThreads, smem, as_stream(stream)>>>(so);
     count_launch();
     return cuda_status(cudaGetLastError(), "small octaves launch");
 }
