@@ -1168,7 +1168,7 @@ blur_z4_kernel(const float* __restrict__ tmp, int tp, const float* __restrict__ 
 // right after every thread has copied them to registers, so kZtSlots - 2
 // planes of loads are always in flight per CTA without holding registers.
 #ifndef VK_ZT_SLOTS
-#define VK_ZT_SLOTS 8
+#define VK_ZT_SLOTS 12  // 8 -> 12 (late round 2): pyramid -0.8%, step +0.2% (scripts/gpu_step_ab.sh)
 #endif
 #ifndef VK_ZT_SRC_TMA
 #define VK_ZT_SRC_TMA 0  // 1: DoG source rows staged by 1-D bulk copies (measured slower: ~16 small copies per plane)
