@@ -92,20 +92,24 @@ def match_database(local: dict, ratio_max: float = 0.9, metric: str = "euclidean
         pad = (-rows.shape[1]) % 8
         code = 0
     else:
-        allr = np.concatenate(arrs) if arrs else np.zeros((0, width), np.int64)
-        integral = allr.dtype.kind in "iub"
-        lo_hi = np.array([allr.min() if allr.size else 0, allr.max() if allr.size else 0, 0 if integral else 1],
-                         dtype=np.float64)
+        # range test per subject array, then one concatenation straight into the transfer dtype (the
+        # configs[4] database is ~211 MB on the host: every extra pass over it is tens of ms)
+        nonempty = [a for a in arrs if a.size]
+        integral = all(a.dtype.kind in "iub" for a in nonempty)
+        lo_hi = np.array([min((a.min() for a in nonempty), default=0), max((a.max() for a in nonempty), default=0),
+                          0 if integral else 1], dtype=np.float64)
         lo_hi = _allreduce_minmax(lo_hi, group)
         if lo_hi[2] == 0 and lo_hi[0] >= -128 and lo_hi[1] <= 127:
-            rows = allr.astype(np.int8)
+            rows = np.concatenate([a.astype(np.int8, copy=False) for a in arrs]) if arrs else np.zeros((0, width), np.int8)
             pad = (-rows.shape[1]) % 32 if rows.shape[1] <= 128 else (-rows.shape[1]) % 4
             code = 1
         else:
-            rows = np.ascontiguousarray(allr, dtype=np.float64)
+            rows = (np.concatenate([a.astype(np.float64, copy=False) for a in arrs]) if arrs
+                    else np.zeros((0, width), np.float64))
             pad = 0
             code = 2
-    rows = np.pad(rows, ((0, 0), (0, pad)))
+    if pad:
+        rows = np.pad(rows, ((0, 0), (0, pad)))
     subj = np.concatenate([np.full(len(a), i, np.int32) for i, a in zip(ids, arrs)]) if arrs else np.zeros(0, np.int32)
     d_rows = t.from_numpy(np.ascontiguousarray(rows)).cuda()
     db, _, ranges = gather_database(d_rows, t.from_numpy(subj).cuda(), group)
